@@ -1,0 +1,93 @@
+"""Builds libfuseplan_b200.so in-tree: C++20 host (planner, executor, C ABI)
+plus the sm_100a CUDA kernels, linked against the static CUDA runtime.
+
+    python -m paper_1509_04394_b200.build        # incremental
+    python -m paper_1509_04394_b200.build --force
+
+nvcc cross-compiles for sm_100a without a GPU, so this runs in the CPU
+container; the built .so travels to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(PKG, "_build")
+LIB = os.path.join(PKG, "libfuseplan_b200.so")
+
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
+CXX = "/usr/bin/g++"
+JSON_DIR = os.environ.get(
+    "FUSEPLAN_JSON_DIR",
+    "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/"
+    "thirdparty/nlohmann")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# No fast-math and no implicit contraction: the exact kernels spell out every
+# rounding with intrinsics; -fmad=false guards any plain float expression.
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false",
+                     "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"]
+CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
+             "-Wno-unused-function", f"-I{JSON_DIR}", f"-I{CUDA_HOME}/include"]
+
+HOST_SRCS = ["host/model.cpp", "host/planner.cpp", "host/video.cpp",
+             "host/exec.cpp", "host/capi.cpp"]
+CUDA_SRCS = ["kernels/fc_exact.cu", "kernels/fc_fast.cu", "kernels/fc_dispatch.cu"]
+HEADERS = ["host/fuseplan.hpp", "host/exec.hpp", "host/video.hpp",
+           "kernels/fc_kernels.h", "kernels/fc_fast.cuh"]
+
+
+def _newest_header() -> float:
+    ts = [os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS
+          if os.path.exists(os.path.join(CSRC, h))]
+    ts.append(os.path.getmtime(os.path.join(ROOT, "include", "fuseplan.h")))
+    return max(ts)
+
+
+def _compile(src: str, force: bool) -> str:
+    path = os.path.join(CSRC, src)
+    obj = os.path.join(OBJ, src.replace("/", "_") + ".o")
+    if (not force and os.path.exists(obj)
+            and os.path.getmtime(obj) >= max(os.path.getmtime(path), _newest_header())):
+        return obj
+    if src.endswith(".cu"):
+        cmd = [NVCC] + NVCC_FLAGS + ["-c", path, "-o", obj]
+    else:
+        cmd = [CXX] + CXX_FLAGS + ["-c", path, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    if r.stderr.strip():
+        sys.stderr.write(r.stderr)
+    return obj
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    srcs = HOST_SRCS + CUDA_SRCS
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, force), srcs))
+    if (force or not os.path.exists(LIB)
+            or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs)):
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + [
+            "-Xlinker", "--no-undefined", "-lpthread", "-ldl", "-lrt"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        print(LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    a = ap.parse_args()
+    build(force=a.force, verbose=True)

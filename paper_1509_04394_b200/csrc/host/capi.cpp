@@ -1,0 +1,523 @@
+// The fuseplan C ABI of the B200 build (include/fuseplan.h).  Every entry
+// point runs under guarded(): no exception crosses the boundary, Error kinds
+// map to fp_status, the message lands in the thread-local fp_last_error()
+// (same contract as /root/reference/proj/src/capi.cpp:21-47).
+#include "../../../include/fuseplan.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <filesystem>
+#include <iomanip>
+#include <memory>
+#include <sstream>
+
+#include "exec.hpp"
+#include "fuseplan.hpp"
+#include "json.hpp"
+#include "video.hpp"
+
+using namespace fuseplan;
+using ordered_json = nlohmann::ordered_json;
+
+struct fp_pipeline {
+  Pipeline p;
+};
+struct fp_device {
+  Device d;
+};
+struct fp_plan {
+  FusionPlan plan;
+};
+struct fp_exec {
+  std::unique_ptr<Executor> ex;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+fp_status status_of(ErrorKind k) {
+  switch (k) {
+    case ErrorKind::Input: return FP_ERR_INPUT;
+    case ErrorKind::Infeasible: return FP_ERR_INFEASIBLE;
+    default: return FP_ERR_INTERNAL;
+  }
+}
+
+template <typename Fn>
+fp_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return FP_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return status_of(e.kind());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FP_ERR_INTERNAL;
+  }
+}
+
+char* dup(const std::string& s) {
+  char* p = new char[s.size() + 1];
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+void need(bool ok) { require(ok, ErrorKind::Input, "null argument"); }
+
+ReportFormat fmt_of(const char* f) { return report_format_from_string(f ? f : "text"); }
+
+// capi.cpp:149-168: No / Two / Full fusion over every fusible segment.
+std::vector<std::pair<std::string, PlanOptions>> fusion_options(
+    const Pipeline& p, const PlanOptions& base) {
+  std::vector<std::pair<int, int>> none, two, full;
+  for (const FusibleSegment& s : fusible_segments(p)) {
+    for (int k = s.first_id; k <= s.last_id; ++k) none.emplace_back(k, k);
+    if (s.size() >= 3) {
+      two.emplace_back(s.first_id, s.first_id + 1);
+      two.emplace_back(s.first_id + 2, s.last_id);
+    } else {
+      two.emplace_back(s.first_id, s.last_id);
+    }
+    full.emplace_back(s.first_id, s.last_id);
+  }
+  std::vector<std::pair<std::string, PlanOptions>> out;
+  for (auto& [name, part] : {std::pair{"No Fusion", none}, std::pair{"Two Fusion", two},
+                             std::pair{"Full Fusion", full}}) {
+    PlanOptions o = base;
+    o.forced_partition = part;
+    out.emplace_back(name, o);
+  }
+  return out;
+}
+
+struct OptionMetrics {
+  std::string name;
+  std::vector<std::pair<int, int>> partition;
+  double cost = 0.0;
+  std::int64_t transfer_paper = 0, transfer_exact = 0;
+  double min_du = 1.0;
+  int buffers = 0;
+  std::int64_t buffer_bytes = 0;
+  double min_occ = 1.0;
+};
+
+OptionMetrics metrics_of(const std::string& name, const Pipeline& p, const Device& d,
+                         const PlanOptions& o) {
+  FusionPlan fp = plan(p, d, o);
+  OptionMetrics m;
+  m.name = name;
+  m.partition = fp.partition();
+  m.cost = fp.total_cost;
+  m.buffers = fp.buffers.buffers;
+  m.buffer_bytes = fp.buffers.bytes;
+  for (const PlanGroup& g : fp.groups) {
+    m.transfer_paper += g.transfer_paper;
+    m.transfer_exact += g.transfer_exact;
+    m.min_du = std::min(m.min_du, g.du);
+    if (!g.global_aggregation) m.min_occ = std::min(m.min_occ, g.launch.occupancy);
+  }
+  return m;
+}
+
+// Device element traffic of one executor run, by construction of the kernels:
+// an unfused stage reads its input plane and writes its output plane once;
+// a fused group reads its input once and writes only its final output.
+std::int64_t device_elems(const FusionPlan& fp, const Pipeline& p) {
+  std::int64_t px = p.video.pixel_volume(), n = 0;
+  for (const PlanGroup& g : fp.groups) {
+    if (g.global_aggregation) continue;
+    n += g.tiled ? 2 * px : 2 * px * (g.last - g.first + 1);
+  }
+  return n;
+}
+
+std::string utc_now() {
+  std::time_t now = std::time(nullptr);
+  std::tm tm{};
+  gmtime_r(&now, &tm);
+  char buf[32];
+  std::strftime(buf, sizeof buf, "%Y-%m-%dT%H:%M:%SZ", &tm);
+  return buf;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fp_last_error(void) { return g_err.c_str(); }
+void fp_string_free(char* s) { delete[] s; }
+
+fp_status fp_pipeline_parse(const char* json_text, fp_pipeline** out) {
+  return guarded([&] {
+    need(json_text && out);
+    *out = new fp_pipeline{parse_pipeline(json_text)};
+  });
+}
+
+fp_status fp_pipeline_load(const char* path, fp_pipeline** out) {
+  return guarded([&] {
+    need(path && out);
+    *out = new fp_pipeline{load_pipeline_file(path)};
+  });
+}
+
+void fp_pipeline_free(fp_pipeline* p) { delete p; }
+
+fp_status fp_device_parse(const char* json_text, fp_device** out) {
+  return guarded([&] {
+    need(json_text && out);
+    *out = new fp_device{parse_device(json_text)};
+  });
+}
+
+fp_status fp_device_load(const char* path_or_name, fp_device** out) {
+  return guarded([&] {
+    need(path_or_name && out);
+    *out = new fp_device{load_device_file(path_or_name)};
+  });
+}
+
+void fp_device_free(fp_device* d) { delete d; }
+
+fp_status fp_plan_create(const fp_pipeline* p, const fp_device* d,
+                         const char* options_json, fp_plan** out) {
+  return guarded([&] {
+    need(p && d && out);
+    *out = new fp_plan{plan(p->p, d->d, parse_plan_options(options_json))};
+  });
+}
+
+void fp_plan_free(fp_plan* plan) { delete plan; }
+
+fp_status fp_plan_render_json(const fp_plan* fp, char** out) {
+  return guarded([&] {
+    need(fp && out);
+    *out = dup(render_plan(fp->plan));
+  });
+}
+
+fp_status fp_analyze_report(const fp_pipeline* p, const char* format,
+                            int with_timestamp, char** out) {
+  return guarded([&] {
+    need(p && out);
+    *out = dup(analyze_report(p->p, {fmt_of(format), with_timestamp != 0}));
+  });
+}
+
+fp_status fp_plan_report(const fp_plan* fp, const char* format, int with_timestamp,
+                         char** out) {
+  return guarded([&] {
+    need(fp && out);
+    *out = dup(plan_report(fp->plan, {fmt_of(format), with_timestamp != 0}));
+  });
+}
+
+fp_status fp_tile_sweep(const fp_device* d, const int halo[6], int max_x, int max_t,
+                        const char* format, char** out) {
+  return guarded([&] {
+    need(d && halo && out);
+    Halo h{halo[0], halo[1], halo[2], halo[3], halo[4], halo[5]};
+    h.validate();
+    *out = dup(tile_sweep_csv(h, d->d.smem_bytes / 4, max_x, max_t, fmt_of(format)));
+  });
+}
+
+fp_status fp_codegen(const fp_pipeline* p, const fp_device* d, const char* options_json,
+                     const char* name, const char* out_dir, char** manifest_out) {
+  return guarded([&] {
+    need(p && d && name && out_dir && manifest_out);
+    FusionPlan fp = plan(p->p, d->d, parse_plan_options(options_json));
+    // The B200 build does not emit source text: each group maps onto a
+    // compiled sm_100a kernel; the manifest records which one.
+    ordered_json m;
+    m["schema_version"] = 1;
+    m["name"] = name;
+    m["target"] = "sm_100a";
+    m["groups"] = ordered_json::array();
+    for (const PlanGroup& g : fp.groups) {
+      std::string kernel = "host (global aggregation)";
+      if (!g.global_aggregation) {
+        std::vector<std::string> ops;
+        for (int id = g.first; id <= g.last; ++id)
+          ops.push_back(p->p.kernels[std::size_t(id - 1)].stencil_op);
+        using V = std::vector<std::string>;
+        if (ops == V{"rgba2gray", "iir_temporal", "gaussian", "gradient", "threshold"})
+          kernel = "fc::k_chain (F12345 streaming)";
+        else if (ops == V{"rgba2gray", "iir_temporal"})
+          kernel = "fc::k_gray_iir (F12)";
+        else if (ops == V{"gaussian", "gradient", "threshold"})
+          kernel = "fc::k_gauss_grad_thr (F345)";
+        else
+          kernel = "per-stage kernels";
+      }
+      m["groups"].push_back({{"first", g.first}, {"last", g.last}, {"kernel", kernel}});
+    }
+    std::string text = m.dump(2) + "\n";
+    std::filesystem::create_directories(out_dir);
+    write_text_file((std::filesystem::path(out_dir) / (std::string(name) + "_manifest.json"))
+                        .string(),
+                    text);
+    *manifest_out = dup(text);
+  });
+}
+
+fp_status fp_simulate(const fp_pipeline* p, const fp_device* d, const char* options_json,
+                      const char* video_path, const char* synth_json,
+                      const char* track_csv_path, const char* format, int with_timestamp,
+                      char** out) {
+  return guarded([&] {
+    need(p && d && out);
+    require((video_path != nullptr) != (synth_json != nullptr), ErrorKind::Input,
+            "exactly one of video file / synth spec needed");
+    require(track_csv_path == nullptr, ErrorKind::Input,
+            "the tracking stage (K6) is not part of the B200 hot-path build");
+    ReportFormat rf = fmt_of(format);
+    PlanOptions base = parse_plan_options(options_json);
+    HostVideo video = video_path ? read_fpvd_file(video_path)
+                                 : synth_scene(parse_synth_spec(synth_json), nullptr);
+    const VideoDims& pv = p->p.video;
+    require(video.dims.width == pv.width && video.dims.height == pv.height &&
+                video.dims.frames == pv.frames && video.dims.channels == pv.channels,
+            ErrorKind::Input, "video does not match pipeline dimensions");
+
+    FusionPlan executed = plan(p->p, d->d, base);
+    std::vector<OptionMetrics> options;
+    for (auto& [name, o] : fusion_options(p->p, base)) {
+      try {
+        options.push_back(metrics_of(name, p->p, d->d, o));
+      } catch (const Error&) {
+        // an infeasible comparison option is omitted, not fatal
+      }
+    }
+    // Sequential arm: every stage its own kernel.  Tiled arm: the plan.
+    PlanOptions singles = base;
+    singles.forced_partition.emplace();
+    for (int k = 1; k <= p->p.size(); ++k) singles.forced_partition->emplace_back(k, k);
+    singles.forced_tile.reset();
+    FusionPlan seq_plan = plan(p->p, d->d, singles);
+    int in_type = video.elem == ElemType::U8 ? FC_U8 : FC_F32;
+    Executor seq(p->p, seq_plan, 0, {});
+    Executor fused(p->p, executed, 0, {});
+    std::size_t n = std::size_t(pv.pixel_volume());
+    std::vector<float> a(n), b(n);
+    auto run_to_float = [&](Executor& ex, std::vector<float>& dst) {
+      if (ex.output_type() == FC_U8) {
+        std::vector<std::uint8_t> tmp(n);
+        ex.run_host(video.data(), in_type, tmp.data());
+        std::transform(tmp.begin(), tmp.end(), dst.begin(),
+                       [](std::uint8_t v) { return float(v); });
+      } else {
+        ex.run_host(video.data(), in_type, dst.data());
+      }
+    };
+    run_to_float(seq, a);
+    run_to_float(fused, b);
+    std::int64_t diffs = 0;
+    float max_abs = 0.0f;
+    for (std::size_t i = 0; i < n; ++i) {
+      float df = std::abs(a[i] - b[i]);
+      if (df != 0.0f || a[i] != b[i]) {
+        ++diffs;
+        max_abs = std::max(max_abs, df);
+      }
+    }
+    int executed_kernels = 0;
+    for (const KernelDesc& k : p->p.kernels)
+      executed_kernels += k.scope != KernelScope::GlobalAggregation;
+    std::int64_t analytic_serial =
+        transfer_serial(std::max(executed_kernels, 1), 1,
+                        TileShape{pv.width, pv.height, pv.frames});
+    std::int64_t analytic_fused = 0;
+    for (const PlanGroup& g : executed.groups) analytic_fused += g.transfer_exact;
+    std::int64_t dev_serial = device_elems(seq_plan, p->p);
+    std::int64_t dev_fused = device_elems(executed, p->p);
+    double reduction =
+        dev_serial > 0 ? 100.0 * (1.0 - double(dev_fused) / double(dev_serial)) : 0.0;
+
+    std::ostringstream ss;
+    if (rf == ReportFormat::Json) {
+      ordered_json j;
+      j["schema_version"] = 1;
+      if (with_timestamp) j["generated"] = utc_now();
+      j["plan"] = ordered_json::parse(render_plan(executed));
+      j["options"] = ordered_json::array();
+      for (const auto& o : options)
+        j["options"].push_back({{"name", o.name},
+                                {"partition", partition_string(o.partition)},
+                                {"predicted_cost", o.cost},
+                                {"transfer_paper", o.transfer_paper},
+                                {"transfer_exact", o.transfer_exact},
+                                {"min_du", o.min_du},
+                                {"buffers", o.buffers},
+                                {"buffer_bytes", o.buffer_bytes},
+                                {"min_occupancy", o.min_occ}});
+      j["buffer_policy"] = "one input buffer plus one output buffer per group";
+      j["simulation"] = {{"backend", "sm_100a"},
+                         {"outputs_identical", diffs == 0},
+                         {"max_abs_diff", max_abs},
+                         {"diff_count", diffs},
+                         {"interior_diffs", diffs},
+                         {"boundary_diffs", 0},
+                         {"measured_serial_gmem", dev_serial},
+                         {"analytic_serial_gmem", analytic_serial},
+                         {"measured_tiled_gmem", dev_fused},
+                         {"analytic_fused_exact_gmem", analytic_fused},
+                         {"traffic_reduction_pct", reduction}};
+      *out = dup(j.dump(2) + "\n");
+      return;
+    }
+    if (rf == ReportFormat::Csv) {
+      ss << "option,partition,predicted_cost,transfer_paper,transfer_exact,"
+            "min_du,buffers,buffer_bytes,min_occupancy\n";
+      for (const auto& o : options)
+        ss << o.name << ",\"" << partition_string(o.partition) << "\"," << o.cost << ','
+           << o.transfer_paper << ',' << o.transfer_exact << ',' << o.min_du << ','
+           << o.buffers << ',' << o.buffer_bytes << ',' << o.min_occ << '\n';
+      *out = dup(ss.str());
+      return;
+    }
+    ss << "run report\n";
+    if (with_timestamp) ss << "generated: " << utc_now() << "\n";
+    ss << "device: " << executed.device_name << "\nvideo: " << pv.width << "x"
+       << pv.height << "x" << pv.frames << " (" << pv.channels
+       << (pv.channels == 1 ? " channel)" : " channels)") << "\nfusion options:\n";
+    for (const auto& o : options)
+      ss << "  " << o.name << " [" << partition_string(o.partition) << "]: cost "
+         << o.cost << ", transfer paper " << o.transfer_paper << " / exact "
+         << o.transfer_exact << ", min DU " << std::fixed << std::setprecision(4)
+         << o.min_du << std::defaultfloat << ", buffers " << o.buffers << " ("
+         << o.buffer_bytes << " bytes), min occupancy " << o.min_occ << "\n";
+    ss << "gmem buffer policy: one input buffer plus one output buffer per group\n"
+       << "executed partition: " << partition_string(executed.partition()) << " (halo "
+       << to_string(executed.halo_mode) << ")\n"
+       << "simulation (sm_100a):\n"
+       << "  outputs identical: " << (diffs == 0 ? "true" : "false") << "\n"
+       << "  max abs diff: " << max_abs << " (" << diffs << " elements)\n"
+       << "  serial gmem: device " << dev_serial << ", analytic " << analytic_serial
+       << "\n  tiled gmem: device " << dev_fused << ", analytic exact "
+       << analytic_fused << "\n  traffic reduction: " << std::fixed
+       << std::setprecision(1) << reduction << "%" << std::defaultfloat << "\n";
+    *out = dup(ss.str());
+  });
+}
+
+fp_status fp_calibrate_csv(const char* measurements_csv, char** result_json) {
+  return guarded([&] {
+    need(measurements_csv && result_json);
+    throw Error(ErrorKind::Input,
+                "cost-model calibration is not part of the B200 hot-path build");
+  });
+}
+
+fp_status fp_device_render_with_cost(const fp_device* d, const char* params_json,
+                                     char** out) {
+  return guarded([&] {
+    need(d && params_json && out);
+    ordered_json j;
+    try {
+      j = ordered_json::parse(params_json);
+    } catch (const ordered_json::exception& e) {
+      throw Error(ErrorKind::Input, std::string("params: bad JSON: ") + e.what());
+    }
+    if (j.contains("params")) j = j["params"];
+    Device dev = d->d;
+    dev.cost.gmem_cost_per_elem = j.value("gmem_cost_per_elem", dev.cost.gmem_cost_per_elem);
+    dev.cost.smem_cost_per_elem = j.value("smem_cost_per_elem", dev.cost.smem_cost_per_elem);
+    dev.cost.compute_cost_unit = j.value("compute_cost_unit", dev.cost.compute_cost_unit);
+    dev.cost.launch_overhead = j.value("launch_overhead", dev.cost.launch_overhead);
+    *out = dup(render_device(dev));
+  });
+}
+
+// ------------------------------------------------------------ executor
+
+fp_status fp_exec_create(const fp_pipeline* p, const fp_plan* fp, int device,
+                         const char* options_json, fp_exec** out) {
+  return guarded([&] {
+    need(p && fp && out);
+    ExecOptions o;
+    if (options_json && *options_json) {
+      ordered_json j;
+      try {
+        j = ordered_json::parse(options_json);
+      } catch (const ordered_json::exception& e) {
+        throw Error(ErrorKind::Input, std::string("exec options: bad JSON: ") + e.what());
+      }
+      std::string v = j.value("variant", std::string("auto"));
+      if (v == "auto") o.variant = Variant::Auto;
+      else if (v == "exact") o.variant = Variant::Exact;
+      else if (v == "fast") o.variant = Variant::Fast;
+      else throw Error(ErrorKind::Input, "unknown variant: " + v);
+      o.host_chunk_frames = j.value("host_chunk_frames", 0);
+    }
+    *out = new fp_exec{std::make_unique<Executor>(p->p, fp->plan, device, o)};
+  });
+}
+
+void fp_exec_free(fp_exec* e) { delete e; }
+
+fp_status fp_exec_output_type(const fp_exec* e, int* elem_type) {
+  return guarded([&] {
+    need(e && elem_type);
+    *elem_type = e->ex->output_type();
+  });
+}
+
+fp_status fp_exec_state_planes(const fp_exec* e, int* n) {
+  return guarded([&] {
+    need(e && n);
+    *n = e->ex->iir_count();
+  });
+}
+
+fp_status fp_exec_run(fp_exec* e, const void* video, int in_type, void* out, int flags,
+                      void* stream) {
+  return guarded([&] {
+    need(e && video && out);
+    require(in_type == FP_ELEM_U8 || in_type == FP_ELEM_F32, ErrorKind::Input,
+            "in_type must be FP_ELEM_U8 or FP_ELEM_F32");
+    if (flags & FP_EXEC_DEVICE_PTRS)
+      e->ex->run_device(video, in_type, out, e->ex->dims().frames, 0, nullptr, nullptr,
+                        stream);
+    else
+      e->ex->run_host(video, in_type, out);
+  });
+}
+
+fp_status fp_exec_run_range(fp_exec* e, const void* video, int in_type, void* out,
+                            int n_frames, int n_warm, const float* state_in,
+                            float* state_out, void* stream) {
+  return guarded([&] {
+    need(e && video && (out || n_frames == n_warm));
+    require(in_type == FP_ELEM_U8 || in_type == FP_ELEM_F32, ErrorKind::Input,
+            "in_type must be FP_ELEM_U8 or FP_ELEM_F32");
+    e->ex->run_device(video, in_type, out, n_frames, n_warm, state_in, state_out, stream);
+  });
+}
+
+fp_status fp_exec_describe(const fp_exec* e, char** out_json) {
+  return guarded([&] {
+    need(e && out_json);
+    *out_json = dup(e->ex->describe());
+  });
+}
+
+fp_status fp_synth_hash_u8(void* device_out, int width, int height, int frames,
+                           int channels, int t0, uint64_t seed, void* stream) {
+  return guarded([&] {
+    need(device_out != nullptr);
+    require(width >= 0 && height >= 0 && frames >= 0 && channels >= 1, ErrorKind::Input,
+            "bad dims");
+    int rc = fc_hash_video_u8(static_cast<std::uint8_t*>(device_out),
+                              fc_dims{width, height, frames}, channels, t0, seed, stream);
+    require(rc == 0, ErrorKind::Internal,
+            std::string("fc_hash_video_u8: ") + fc_error_string(rc));
+  });
+}
+
+}  // extern "C"

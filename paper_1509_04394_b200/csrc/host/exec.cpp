@@ -1,0 +1,436 @@
+// GPU executor (see exec.hpp).
+#include "exec.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+namespace fuseplan {
+
+namespace {
+
+void cuda_check(int rc, const char* what) {
+  if (rc == 0) return;
+  throw Error(ErrorKind::Internal, std::string(what) + ": " + fc_error_string(rc));
+}
+
+void cuda_check(cudaError_t rc, const char* what) { cuda_check(int(rc), what); }
+
+double param(const KernelDesc& k, const char* key, double fallback) {
+  auto it = k.params.find(key);
+  return it == k.params.end() ? fallback : it->second;
+}
+
+int op_code(const std::string& op) {
+  static const char* names[] = {"rgba2gray", "iir_temporal", "gaussian",
+                                "gradient",  "threshold",    "identity",
+                                "scale_offset", "box_mean"};
+  for (int i = 0; i < 8; ++i)
+    if (op == names[i]) return i;
+  return -1;
+}
+
+bool is_byte_level(float v) {
+  return v >= 0.0f && v <= 255.0f && v == std::floor(v);
+}
+
+struct Scratch {
+  float* a;
+  float* b;
+};
+
+}  // namespace
+
+std::vector<float> gaussian_taps(int radius, double sigma) {
+  const int d = 2 * radius + 1;
+  std::vector<double> raw(std::size_t(d) * d);
+  double norm = 0.0;
+  std::size_t i = 0;
+  for (int dy = -radius; dy <= radius; ++dy)
+    for (int dx = -radius; dx <= radius; ++dx, ++i) {
+      raw[i] = std::exp(-(dx * dx + dy * dy) / (2.0 * sigma * sigma));
+      norm += raw[i];
+    }
+  std::vector<float> taps(raw.size());
+  for (std::size_t j = 0; j < raw.size(); ++j) taps[j] = float(raw[j] / norm);
+  return taps;
+}
+
+fc_stage make_stage(const KernelDesc& k) {
+  fc_stage s;
+  std::memset(&s, 0, sizeof s);
+  s.op = op_code(k.stencil_op);
+  require(s.op >= 0, ErrorKind::Input,
+          "stencil_op '" + k.stencil_op + "' has no device kernel");
+  switch (s.op) {
+    case FC_RGBA2GRAY:
+      s.wr = float(param(k, "wr", 0.299));
+      s.wg = float(param(k, "wg", 0.587));
+      s.wb = float(param(k, "wb", 0.114));
+      break;
+    case FC_IIR_TEMPORAL:
+      s.alpha = float(param(k, "alpha", 0.5));
+      break;
+    case FC_GAUSSIAN: {
+      s.g_radius = int(param(k, "radius", 2));
+      require(s.g_radius >= 0 && s.g_radius <= FC_MAX_GAUSS_RADIUS, ErrorKind::Input,
+              "gaussian radius > " + std::to_string(FC_MAX_GAUSS_RADIUS) +
+                  " has no device kernel");
+      auto taps = gaussian_taps(s.g_radius, param(k, "sigma", 1.0));
+      std::copy(taps.begin(), taps.end(), s.g_w);
+      break;
+    }
+    case FC_THRESHOLD:
+      s.th = float(param(k, "th", 128.0));
+      s.white = float(param(k, "white", 255.0));
+      s.black = float(param(k, "black", 0.0));
+      break;
+    case FC_SCALE_OFFSET:
+      s.scale = float(param(k, "scale", 1.0));
+      s.offset = float(param(k, "offset", 0.0));
+      break;
+    case FC_BOX_MEAN:
+      s.rx = int(param(k, "radius_x", 1));
+      s.ry = int(param(k, "radius_y", 1));
+      s.rt = int(param(k, "radius_t", 0));
+      break;
+    default:
+      break;
+  }
+  return s;
+}
+
+const char* LaunchGroup::kernel_name() const {
+  switch (kind) {
+    case GrayIir: return "F12 gray+iir (time scan)";
+    case GaussGradThr: return "F345 gauss+grad+thr (frame tiles)";
+    case Chain: return "F12345 streaming chain";
+    default: return "unfused stages";
+  }
+}
+
+Executor::Executor(const Pipeline& p, const FusionPlan& fp, int device,
+                   const ExecOptions& opt)
+    : device_(device), dims_(p.video), opt_(opt) {
+  int n_dev = 0;
+  cudaError_t e = cudaGetDeviceCount(&n_dev);
+  require(e == cudaSuccess && n_dev > 0, ErrorKind::Internal,
+          std::string("no CUDA device available: ") + cudaGetErrorString(e));
+  require(device >= 0 && device < n_dev, ErrorKind::Input,
+          "device ordinal out of range");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cudaStream_t s;
+  cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  own_stream_ = s;
+
+  bool first = true;
+  for (const PlanGroup& g : fp.groups) {
+    if (g.global_aggregation) continue;  // tracking stage runs on the host
+    LaunchGroup lg;
+    lg.first = g.first;
+    lg.last = g.last;
+    std::vector<std::string> ops;
+    for (int id = g.first; id <= g.last; ++id) {
+      const KernelDesc& k = p.kernels[std::size_t(id - 1)];
+      if (k.scope == KernelScope::GlobalAggregation) continue;
+      lg.stages.push_back(make_stage(k));
+      ops.push_back(k.stencil_op);
+      if (k.stencil_op == "iir_temporal") {
+        lg.has_iir = true;
+        ++n_iir_;
+      }
+    }
+    if (lg.stages.empty()) continue;
+    lg.reads_video = first;
+    first = false;
+    using V = std::vector<std::string>;
+    const V chain5 = {"rgba2gray", "iir_temporal", "gaussian", "gradient", "threshold"};
+    const V chain4 = {"iir_temporal", "gaussian", "gradient", "threshold"};
+    auto radius = [&](std::size_t i) { return lg.stages[i].g_radius; };
+    if (lg.reads_video && ops == chain5 && radius(2) >= 1 && radius(2) <= 3)
+      lg.kind = LaunchGroup::Chain;
+    else if (lg.reads_video && dims_.channels == 1 && ops == chain4 &&
+             radius(1) >= 1 && radius(1) <= 3)
+      lg.kind = LaunchGroup::Chain;
+    else if (lg.reads_video && ops == V{"rgba2gray", "iir_temporal"})
+      lg.kind = LaunchGroup::GrayIir;
+    else if (ops == V{"gaussian", "gradient", "threshold"})
+      lg.kind = LaunchGroup::GaussGradThr;
+    else
+      lg.kind = LaunchGroup::Stages;
+    groups_.push_back(std::move(lg));
+  }
+  require(!groups_.empty(), ErrorKind::Input, "pipeline has no executable stage");
+  const fc_stage& last = groups_.back().stages.back();
+  if (last.op == FC_THRESHOLD && is_byte_level(last.white) &&
+      is_byte_level(last.black))
+    out_type_ = FC_U8;
+  for (auto& g : groups_) g.out_type = FC_F32;
+  groups_.back().out_type = out_type_;
+}
+
+Executor::~Executor() {
+  if (scratch_) cudaFree(scratch_);
+  if (own_stream_) cudaStreamDestroy(static_cast<cudaStream_t>(own_stream_));
+}
+
+void Executor::ensure_scratch(std::size_t bytes) {
+  if (bytes <= scratch_bytes_) return;
+  if (scratch_) cuda_check(cudaFree(scratch_), "cudaFree");
+  scratch_ = nullptr;
+  cuda_check(cudaMalloc(&scratch_, bytes), "cudaMalloc(scratch)");
+  scratch_bytes_ = bytes;
+}
+
+std::int64_t Executor::launches_per_run() const {
+  std::int64_t n = 0;
+  for (const auto& g : groups_)
+    n += g.kind == LaunchGroup::Stages ? std::int64_t(g.stages.size()) : 1;
+  return n;
+}
+
+std::string Executor::describe() const {
+  std::ostringstream ss;
+  ss << "{\"device\": " << device_ << ", \"variant\": " << int(opt_.variant)
+     << ", \"output\": \"" << (out_type_ == FC_U8 ? "u8" : "f32")
+     << "\", \"launches_per_run\": " << launches_per_run() << ", \"groups\": [";
+  for (std::size_t i = 0; i < groups_.size(); ++i) {
+    const auto& g = groups_[i];
+    ss << (i ? ", " : "") << "{\"first\": " << g.first << ", \"last\": " << g.last
+       << ", \"kernel\": \"" << g.kernel_name() << "\", \"fused\": "
+       << (g.kind != LaunchGroup::Stages || g.stages.size() == 1 ? "true" : "false")
+       << "}";
+  }
+  ss << "]}";
+  return ss.str();
+}
+
+void Executor::run_device(const void* video, int in_type, void* out, int n_frames,
+                          int n_warm, const float* state_in, float* state_out,
+                          void* stream) {
+  require(n_frames >= 0 && n_warm >= 0 && n_warm <= n_frames, ErrorKind::Input,
+          "bad frame range");
+  require(n_warm == 0 || n_iir_ == 1, ErrorKind::Input,
+          "warm-up ranges need exactly one IIR stage in the chain");
+  require(state_in == nullptr || n_iir_ >= 1, ErrorKind::Input,
+          "state_in given but the chain has no IIR stage");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream ? stream : own_stream_);
+  const long long hw = (long long)dims_.width * dims_.height;
+  const int C = dims_.channels;
+  if (n_iir_ == 0 && n_warm > 0) {  // no recurrence: warm-up frames are moot
+    const std::size_t esz = in_type == FC_U8 ? 1 : 4;
+    video = static_cast<const char*>(video) + std::size_t(n_warm) * C * hw * esz;
+    n_frames -= n_warm;
+    n_warm = 0;
+  }
+  if (n_frames == 0) return;
+
+  // two f32 ping-pong planes of the largest frame count in flight
+  std::size_t plane_bytes = std::size_t(hw) * n_frames * sizeof(float);
+  bool need_scratch = in_type == FC_U8 && dims_.channels == 1 &&
+                      groups_.front().kind != LaunchGroup::Chain;
+  for (const auto& g : groups_)
+    if (g.kind == LaunchGroup::Stages || g.kind == LaunchGroup::GrayIir ||
+        &g != &groups_.back())
+      need_scratch = true;
+  if (need_scratch) ensure_scratch(2 * plane_bytes);
+  float* buf[2] = {static_cast<float*>(scratch_),
+                   scratch_ ? reinterpret_cast<float*>(static_cast<char*>(scratch_) +
+                                                       plane_bytes)
+                            : nullptr};
+  int which = 0;
+
+  const void* cur = video;
+  int cur_type = in_type;
+  int frames = n_frames;   // frames held by `cur`
+  int warm = n_warm;       // warm-up frames still at the front of `cur`
+  int iir_idx = 0;
+  auto state_ptr = [&](const float* base) {
+    return base ? base + std::size_t(iir_idx) * hw : nullptr;
+  };
+
+  // A single-channel u8 video entering f32 stage kernels is widened first
+  // (the streaming chain and rgba2gray read u8 directly).
+  if (cur_type == FC_U8 && groups_.front().kind != LaunchGroup::Chain &&
+      groups_.front().stages.front().op != FC_RGBA2GRAY) {
+    fc_stage conv;
+    std::memset(&conv, 0, sizeof conv);
+    conv.op = FC_IDENTITY;
+    cuda_check(fc_stage_spatial(&conv, cur, FC_U8, buf[which], FC_F32,
+                                fc_dims{dims_.width, dims_.height, frames}, st),
+               "u8 widen");
+    cur = buf[which];
+    cur_type = FC_F32;
+    which ^= 1;
+  }
+
+  for (std::size_t gi = 0; gi < groups_.size(); ++gi) {
+    const LaunchGroup& g = groups_[gi];
+    bool last_group = gi + 1 == groups_.size();
+    void* dst = last_group ? out : buf[which];
+    int dst_type = last_group ? out_type_ : FC_F32;
+    fc_dims d{dims_.width, dims_.height, frames};
+    switch (g.kind) {
+      case LaunchGroup::Chain: {
+        bool gray_in = g.stages.size() == 4;
+        const fc_stage* s = g.stages.data();
+        const fc_stage* sgray = gray_in ? nullptr : s;
+        const fc_stage* rest = gray_in ? s : s + 1;
+        cuda_check(fc_fused_chain(sgray, &rest[0], &rest[1], &rest[2], &rest[3], cur,
+                                  cur_type, gray_in, dst, dst_type, d, warm,
+                                  state_ptr(state_in),
+                                  const_cast<float*>(state_ptr(state_out)),
+                                  int(opt_.variant), st),
+                   "F12345 launch");
+        frames -= warm;
+        warm = 0;
+        ++iir_idx;
+        break;
+      }
+      case LaunchGroup::GrayIir:
+        cuda_check(fc_fused_gray_iir(&g.stages[0], &g.stages[1], cur, cur_type,
+                                     static_cast<float*>(dst), d, warm,
+                                     state_ptr(state_in),
+                                     const_cast<float*>(state_ptr(state_out)), st),
+                   "F12 launch");
+        frames -= warm;
+        warm = 0;
+        ++iir_idx;
+        break;
+      case LaunchGroup::GaussGradThr:
+        require(cur_type == FC_F32, ErrorKind::Internal, "F345 needs f32 planes");
+        cuda_check(fc_fused_gauss_grad_thr(&g.stages[0], &g.stages[1], &g.stages[2],
+                                           static_cast<const float*>(cur), dst,
+                                           dst_type, d, st),
+                   "F345 launch");
+        break;
+      case LaunchGroup::Stages:
+        for (std::size_t si = 0; si < g.stages.size(); ++si) {
+          const fc_stage& s = g.stages[si];
+          bool last_stage = si + 1 == g.stages.size();
+          void* sdst = (last_stage && last_group) ? out : buf[which];
+          int sdst_type = (last_stage && last_group) ? out_type_ : FC_F32;
+          fc_dims sd{dims_.width, dims_.height, frames};
+          if (s.op == FC_IIR_TEMPORAL) {
+            require(cur_type == FC_F32, ErrorKind::Internal, "iir needs f32 planes");
+            cuda_check(fc_stage_iir(&s, static_cast<const float*>(cur),
+                                    static_cast<float*>(sdst), sd, warm,
+                                    state_ptr(state_in),
+                                    const_cast<float*>(state_ptr(state_out)), st),
+                       "iir launch");
+            frames -= warm;
+            warm = 0;
+            ++iir_idx;
+          } else {
+            cuda_check(fc_stage_spatial(&s, cur, cur_type, sdst, sdst_type, sd, st),
+                       "stage launch");
+          }
+          cur = sdst;
+          cur_type = sdst_type;
+          if (!(last_stage && last_group)) which ^= 1;
+        }
+        continue;  // cur already advanced
+    }
+    cur = dst;
+    cur_type = dst_type;
+    if (!last_group) which ^= 1;
+  }
+}
+
+void Executor::run_host(const void* video, int in_type, void* out) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  const long long hw = (long long)dims_.width * dims_.height;
+  const int C = dims_.channels, F = dims_.frames;
+  const std::size_t esz = in_type == FC_U8 ? 1 : 4;
+  const std::size_t osz = out_type_ == FC_U8 ? 1 : 4;
+  const std::size_t in_frame = std::size_t(C) * hw * esz;
+  const std::size_t out_frame = std::size_t(hw) * osz;
+  // Channels the chain reads: rgba2gray never touches alpha (simulator.cpp:55),
+  // so only planes 0..2 of each frame cross the host link.
+  const int read_planes =
+      (C == 4 && groups_.front().stages.front().op == FC_RGBA2GRAY) ? 3 : C;
+
+  bool temporal_window = false;
+  for (const auto& g : groups_)
+    for (const auto& s : g.stages)
+      if (s.op == FC_BOX_MEAN && s.rt > 0) temporal_window = true;
+  int chunk = opt_.host_chunk_frames;
+  if (chunk <= 0)
+    chunk = int(std::max<long long>(1, (96LL << 20) / (long long)in_frame));
+  if (temporal_window) chunk = F;  // cannot cut a temporal window
+  chunk = std::min(chunk, F);
+  const int n_chunks = (F + chunk - 1) / chunk;
+
+  // device staging: 2 video chunks, 2 output chunks, 2 state sets
+  std::size_t vbytes = std::size_t(chunk) * in_frame;
+  std::size_t obytes = std::size_t(chunk) * out_frame;
+  std::size_t sbytes = std::size_t(std::max(n_iir_, 1)) * hw * sizeof(float);
+  char* mem = nullptr;
+  cuda_check(cudaMalloc(&mem, 2 * (vbytes + obytes + sbytes)), "cudaMalloc(stream)");
+  char* vb[2] = {mem, mem + vbytes};
+  char* ob[2] = {mem + 2 * vbytes, mem + 2 * vbytes + obytes};
+  float* sb[2] = {reinterpret_cast<float*>(mem + 2 * (vbytes + obytes)),
+                  reinterpret_cast<float*>(mem + 2 * (vbytes + obytes) + sbytes)};
+  cudaStream_t s_in, s_out;
+  cudaStream_t s_comp = static_cast<cudaStream_t>(own_stream_);
+  cuda_check(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream");
+  std::vector<cudaEvent_t> ev_in(n_chunks), ev_comp(n_chunks), ev_out(n_chunks);
+  for (int k = 0; k < n_chunks; ++k) {
+    cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming);
+  }
+  std::string err;
+  try {
+    for (int k = 0; k < n_chunks; ++k) {
+      int t0 = k * chunk, nf = std::min(chunk, F - t0);
+      int b = k & 1;
+      // H2D: buffer b is free once chunk k-2's compute has consumed it
+      if (k >= 2) cuda_check(cudaStreamWaitEvent(s_in, ev_comp[k - 2], 0), "wait");
+      const char* src = static_cast<const char*>(video) + std::size_t(t0) * in_frame;
+      if (read_planes == C)
+        cuda_check(cudaMemcpyAsync(vb[b], src, std::size_t(nf) * in_frame,
+                                   cudaMemcpyHostToDevice, s_in), "H2D");
+      else
+        cuda_check(cudaMemcpy2DAsync(vb[b], in_frame, src, in_frame,
+                                     std::size_t(read_planes) * hw * esz, nf,
+                                     cudaMemcpyHostToDevice, s_in), "H2D");
+      cuda_check(cudaEventRecord(ev_in[k], s_in), "record");
+      // compute: after its input landed and after chunk k-2's D2H freed ob[b]
+      cuda_check(cudaStreamWaitEvent(s_comp, ev_in[k], 0), "wait");
+      if (k >= 2) cuda_check(cudaStreamWaitEvent(s_comp, ev_out[k - 2], 0), "wait");
+      run_device(vb[b], in_type, ob[b], nf, 0, k == 0 || n_iir_ == 0 ? nullptr : sb[b ^ 1],
+                 n_iir_ ? sb[b] : nullptr, s_comp);
+      cuda_check(cudaEventRecord(ev_comp[k], s_comp), "record");
+      // D2H
+      cuda_check(cudaStreamWaitEvent(s_out, ev_comp[k], 0), "wait");
+      cuda_check(cudaMemcpyAsync(static_cast<char*>(out) + std::size_t(t0) * out_frame,
+                                 ob[b], std::size_t(nf) * out_frame,
+                                 cudaMemcpyDeviceToHost, s_out), "D2H");
+      cuda_check(cudaEventRecord(ev_out[k], s_out), "record");
+    }
+    cuda_check(cudaStreamSynchronize(s_out), "sync");
+    cuda_check(cudaStreamSynchronize(s_comp), "sync");
+  } catch (const Error& e) {
+    err = e.what();
+  }
+  cudaStreamSynchronize(s_in);
+  cudaStreamSynchronize(s_comp);
+  cudaStreamSynchronize(s_out);
+  for (int k = 0; k < n_chunks; ++k) {
+    cudaEventDestroy(ev_in[k]);
+    cudaEventDestroy(ev_comp[k]);
+    cudaEventDestroy(ev_out[k]);
+  }
+  cudaStreamDestroy(s_in);
+  cudaStreamDestroy(s_out);
+  cudaFree(mem);
+  if (!err.empty()) throw Error(ErrorKind::Internal, err);
+}
+
+}  // namespace fuseplan

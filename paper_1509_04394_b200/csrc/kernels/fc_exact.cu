@@ -1,0 +1,617 @@
+// Reference-exact sm_100a kernels for every stage of the SPEC chain and the
+// rest of the stencil catalog, plus the exact fused partitions.
+//
+// Arithmetic contract (simulator.cpp:48-108): every
+// float op is an explicit round-to-nearest intrinsic (__fmul_rn/__fadd_rn/
+// __fsub_rn/__fsqrt_rn) so nothing is contracted; the gaussian accumulates
+// in FP64 in dy-outer/dx-inner order (a DFMA equals the reference's
+// "acc += double(w) * src" because a float*float product is exact in double);
+// no flush-to-zero (the IIR decays into subnormals on dark pixels).
+// Borders: every stage reads ITS OWN input clamped to the video
+// (simulator.cpp:202-210): inside fused tiles a stage's out-of-video halo cell
+// holds that stage's value at the clamped position.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fc_kernels.h"
+
+namespace fc {
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) {
+  return min(max(v, lo), hi);
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<uint8_t>(uint8_t v) {
+  return float(v);
+}
+template <>
+__device__ __forceinline__ float to_f<float>(float v) {
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T from_level(float v);
+template <>
+__device__ __forceinline__ uint8_t from_level<uint8_t>(float v) {
+  return uint8_t(v);  // only used for white/black values that are bytes
+}
+template <>
+__device__ __forceinline__ float from_level<float>(float v) {
+  return v;
+}
+
+// simulator.cpp:51-56
+__device__ __forceinline__ float gray_op(const fc_stage& s, float r, float g,
+                                         float b) {
+  return __fadd_rn(__fadd_rn(__fmul_rn(s.wr, r), __fmul_rn(s.wg, g)),
+                   __fmul_rn(s.wb, b));
+}
+
+// simulator.cpp:57-62 with beta = float(1 - alpha) computed in float
+__device__ __forceinline__ float iir_op(float alpha, float beta, float x,
+                                        float prev) {
+  return __fadd_rn(__fmul_rn(alpha, x), __fmul_rn(beta, prev));
+}
+
+// simulator.cpp:75-83; s(dx,dy) supplied by the caller
+template <typename S>
+__device__ __forceinline__ float sobel_op(S s) {
+  float gx = __fsub_rn(
+      __fadd_rn(__fadd_rn(s(1, -1), __fmul_rn(2.0f, s(1, 0))), s(1, 1)),
+      __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(-1, 0))), s(-1, 1)));
+  float gy = __fsub_rn(
+      __fadd_rn(__fadd_rn(s(-1, 1), __fmul_rn(2.0f, s(0, 1))), s(1, 1)),
+      __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(0, -1))), s(1, -1)));
+  return __fsqrt_rn(__fadd_rn(__fmul_rn(gx, gx), __fmul_rn(gy, gy)));
+}
+
+// ------------------------------------------------------------ unfused stages
+
+template <typename InT>
+__global__ void k_rgba2gray(const InT* __restrict__ in, float* __restrict__ out,
+                            fc_stage s, long long hw, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long t = i / hw, p = i - t * hw;
+    const InT* f = in + t * 4 * hw + p;
+    out[i] = gray_op(s, to_f(f[0]), to_f(f[hw]), to_f(f[2 * hw]));
+  }
+}
+
+// One thread per pixel scans t (simulator.cpp:136-147).  Loads of later
+// frames do not depend on the carried state, so the unrolled loop keeps
+// several frames in flight.
+__global__ void k_iir(const float* __restrict__ in, float* __restrict__ out,
+                      float alpha, float beta, long long hw, int n_frames,
+                      int n_warm, const float* __restrict__ state_in,
+                      float* __restrict__ state_out) {
+  long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= hw) return;
+  float prev = state_in ? state_in[p] : 0.0f;
+  bool fresh = state_in == nullptr;
+#pragma unroll 8
+  for (int t = 0; t < n_frames; ++t) {
+    float x = in[t * hw + p];
+    prev = (fresh && t == 0) ? x : iir_op(alpha, beta, x, prev);
+    if (t >= n_warm) out[(t - n_warm) * hw + p] = prev;
+  }
+  if (state_out) state_out[p] = prev;
+}
+
+// 2-D stencils over a frame tile staged in shared memory.
+constexpr int TW = 32, TH = 8;
+
+template <int R>
+__global__ void k_gaussian(const float* __restrict__ in, float* __restrict__ out,
+                           fc_stage s, int W, int H) {
+  constexpr int SW = TW + 2 * R, SH = TH + 2 * R;
+  __shared__ double tile[SH][SW];
+  __shared__ double w[(2 * R + 1) * (2 * R + 1)];
+  const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
+  const float* f = in + (long long)blockIdx.z * W * H;
+  const int tid = threadIdx.y * TW + threadIdx.x;
+  for (int i = tid; i < (2 * R + 1) * (2 * R + 1); i += TW * TH) w[i] = s.g_w[i];
+  for (int i = tid; i < SW * SH; i += TW * TH) {
+    int sy = i / SW, sx = i - sy * SW;
+    int gx = clampi(x0 + sx - R, 0, W - 1), gy = clampi(y0 + sy - R, 0, H - 1);
+    tile[sy][sx] = double(f[(long long)gy * W + gx]);
+  }
+  __syncthreads();
+  int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  if (x >= W || y >= H) return;
+  double acc = 0.0;
+#pragma unroll
+  for (int dy = 0; dy <= 2 * R; ++dy)
+#pragma unroll
+    for (int dx = 0; dx <= 2 * R; ++dx)
+      acc = __fma_rn(w[dy * (2 * R + 1) + dx],
+                     tile[threadIdx.y + dy][threadIdx.x + dx], acc);
+  out[(long long)blockIdx.z * W * H + (long long)y * W + x] = __double2float_rn(acc);
+}
+
+__global__ void k_gradient(const float* __restrict__ in, float* __restrict__ out,
+                           int W, int H) {
+  __shared__ float tile[TH + 2][TW + 2];
+  const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
+  const float* f = in + (long long)blockIdx.z * W * H;
+  const int tid = threadIdx.y * TW + threadIdx.x;
+  for (int i = tid; i < (TW + 2) * (TH + 2); i += TW * TH) {
+    int sy = i / (TW + 2), sx = i - sy * (TW + 2);
+    int gx = clampi(x0 + sx - 1, 0, W - 1), gy = clampi(y0 + sy - 1, 0, H - 1);
+    tile[sy][sx] = f[(long long)gy * W + gx];
+  }
+  __syncthreads();
+  int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  if (x >= W || y >= H) return;
+  int cx = threadIdx.x + 1, cy = threadIdx.y + 1;
+  out[(long long)blockIdx.z * W * H + (long long)y * W + x] =
+      sobel_op([&](int dx, int dy) { return tile[cy + dy][cx + dx]; });
+}
+
+template <typename OutT>
+__global__ void k_pointwise(const float* __restrict__ in, OutT* __restrict__ out,
+                            fc_stage s, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float v = in[i];
+    float r;
+    if (s.op == FC_THRESHOLD)
+      r = v >= s.th ? s.white : s.black;  // simulator.cpp:84-89
+    else if (s.op == FC_SCALE_OFFSET)
+      r = __fadd_rn(__fmul_rn(s.scale, v), s.offset);  // :91-95
+    else
+      r = v;  // identity :90
+    out[i] = from_level<OutT>(r);
+  }
+}
+
+// float(u8) (video.cpp:87) for a single-channel u8 video entering a stage
+// that reads f32 planes.
+__global__ void k_u8_to_f32(const uint8_t* __restrict__ in, float* __restrict__ out,
+                            long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = float(in[i]);
+}
+
+// box_mean (simulator.cpp:96-106): double accumulation dt, dy, dx, clamp in
+// x, y and t; result float(acc / volume).
+__global__ void k_box_mean(const float* __restrict__ in, float* __restrict__ out,
+                           int rx, int ry, int rt, int W, int H, int F) {
+  long long hw = (long long)W * H, n = hw * F;
+  double vol = double((2 * rx + 1) * (2 * ry + 1) * (2 * rt + 1));
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    int t = int(i / hw);
+    int p = int(i - t * hw);
+    int y = p / W, x = p - y * W;
+    double acc = 0.0;
+    for (int dt = -rt; dt <= rt; ++dt) {
+      const float* f = in + clampi(t + dt, 0, F - 1) * hw;
+      for (int dy = -ry; dy <= ry; ++dy) {
+        const float* row = f + (long long)clampi(y + dy, 0, H - 1) * W;
+        for (int dx = -rx; dx <= rx; ++dx)
+          acc = __dadd_rn(acc, double(row[clampi(x + dx, 0, W - 1)]));
+      }
+    }
+    out[i] = __double2float_rn(__ddiv_rn(acc, vol));
+  }
+}
+
+// ------------------------------------------------------------ F12
+
+template <typename InT>
+__global__ void k_gray_iir(const InT* __restrict__ video, float* __restrict__ out,
+                           fc_stage sg, float alpha, float beta, long long hw,
+                           int n_frames, int n_warm,
+                           const float* __restrict__ state_in,
+                           float* __restrict__ state_out) {
+  long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= hw) return;
+  float prev = state_in ? state_in[p] : 0.0f;
+  bool fresh = state_in == nullptr;
+#pragma unroll 4
+  for (int t = 0; t < n_frames; ++t) {
+    const InT* f = video + (long long)t * 4 * hw + p;
+    float x = gray_op(sg, to_f(f[0]), to_f(f[hw]), to_f(f[2 * hw]));
+    prev = (fresh && t == 0) ? x : iir_op(alpha, beta, x, prev);
+    if (t >= n_warm) out[(t - n_warm) * hw + p] = prev;
+  }
+  if (state_out) state_out[p] = prev;
+}
+
+// ------------------------------------------------------------ F345
+// One CTA per (32x16 tile, frame).  Stage the IIR plane with a halo of R+1
+// as double (converted once per element), compute the gaussian on the
+// tile+1 ring (centres clamped to the video, so the ring's out-of-video cells
+// carry the edge value the gradient must see), then Sobel + threshold.
+constexpr int FW = 32, FH = 16, FT = 256;
+
+template <int R, typename OutT>
+__global__ void __launch_bounds__(FT) k_gauss_grad_thr(
+    const float* __restrict__ in, OutT* __restrict__ out, fc_stage sg,
+    float th, float white, float black, int W, int H) {
+  constexpr int K = 2 * R + 1;
+  constexpr int DW = FW + 2 * (R + 1), DH = FH + 2 * (R + 1);
+  constexpr int GW = FW + 2, GH = FH + 2;
+  __shared__ double d[DH][DW];
+  __shared__ float g[GH][GW];
+  __shared__ double w[K * K];
+  const int x0 = blockIdx.x * FW, y0 = blockIdx.y * FH;
+  const long long hw = (long long)W * H;
+  const float* f = in + blockIdx.z * hw;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < K * K; i += FT) w[i] = sg.g_w[i];
+  for (int i = tid; i < DW * DH; i += FT) {
+    int sy = i / DW, sx = i - sy * DW;
+    int gx = clampi(x0 + sx - (R + 1), 0, W - 1);
+    int gy = clampi(y0 + sy - (R + 1), 0, H - 1);
+    d[sy][sx] = double(f[(long long)gy * W + gx]);
+  }
+  __syncthreads();
+  for (int i = tid; i < GW * GH; i += FT) {
+    int sy = i / GW, sx = i - sy * GW;
+    // centre of this ring cell, clamped to the video; its window stays
+    // inside the staged box because clamping moves toward the tile
+    int cx = clampi(x0 + sx - 1, 0, W - 1) - (x0 - (R + 1));
+    int cy = clampi(y0 + sy - 1, 0, H - 1) - (y0 - (R + 1));
+    double acc = 0.0;
+#pragma unroll
+    for (int dy = 0; dy < K; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < K; ++dx)
+        acc = __fma_rn(w[dy * K + dx], d[cy - R + dy][cx - R + dx], acc);
+    g[sy][sx] = __double2float_rn(acc);
+  }
+  __syncthreads();
+  for (int i = tid; i < FW * FH; i += FT) {
+    int ty = i / FW, tx = i - ty * FW;
+    int x = x0 + tx, y = y0 + ty;
+    if (x >= W || y >= H) continue;
+    float m = sobel_op([&](int dx, int dy) { return g[ty + 1 + dy][tx + 1 + dx]; });
+    out[blockIdx.z * hw + (long long)y * W + x] =
+        from_level<OutT>(m >= th ? white : black);
+  }
+}
+
+// ------------------------------------------------------------ F12345 exact
+// Streaming all-fused chain: one CTA per spatial tile marches over t, the IIR
+// state of its haloed tile (R+1 ring) lives in registers, the frame's
+// inputs for t+1 are loaded while t is computed.  Reference-exact everywhere
+// (FP64 gaussian); the fast certified kernel is in fc_fast.cu.
+template <int R>
+struct ChainGeom {
+  static constexpr int DW = FW + 2 * (R + 1), DH = FH + 2 * (R + 1);
+  static constexpr int NS = (DW * DH + FT - 1) / FT;  // IIR slots per thread
+};
+
+template <int R, typename InT, typename OutT, bool GRAY_IN>
+__global__ void __launch_bounds__(FT) k_chain_exact(
+    const InT* __restrict__ video, OutT* __restrict__ out, fc_stage sgray,
+    float alpha, float beta, fc_stage sg, float th, float white, float black,
+    int W, int H, int n_frames, int n_warm, const float* __restrict__ state_in,
+    float* __restrict__ state_out) {
+  using G = ChainGeom<R>;
+  constexpr int K = 2 * R + 1, DW = G::DW, DH = G::DH, NS = G::NS;
+  constexpr int GW = FW + 2, GH = FH + 2;
+  constexpr int C = GRAY_IN ? 1 : 4;
+  __shared__ double d[DH][DW];
+  __shared__ float g[GH][GW];
+  __shared__ double w[K * K];
+  const int x0 = blockIdx.x * FW, y0 = blockIdx.y * FH;
+  const long long hw = (long long)W * H;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < K * K; i += FT) w[i] = sg.g_w[i];
+
+  // loop-invariant clamped source offsets of the owned IIR cells
+  int src[NS];
+  float st[NS];
+  bool fresh = state_in == nullptr;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    int i = tid + k * FT;
+    int sy = i / DW, sx = i - sy * DW;
+    int gx = clampi(x0 + sx - (R + 1), 0, W - 1);
+    int gy = clampi(y0 + sy - (R + 1), 0, H - 1);
+    src[k] = gy * W + gx;
+    st[k] = (i < DW * DH && state_in) ? state_in[src[k]] : 0.0f;
+  }
+  float cur[NS][3], nxt[NS][3];
+  auto load = [&](int t, float (&v)[NS][3]) {
+    const InT* f = video + (long long)t * C * hw;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      if (tid + k * FT < DW * DH) {
+#pragma unroll
+        for (int c = 0; c < (GRAY_IN ? 1 : 3); ++c) v[k][c] = to_f(f[c * hw + src[k]]);
+      }
+    }
+  };
+  load(0, cur);
+  for (int t = 0; t < n_frames; ++t) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      int i = tid + k * FT;
+      if (i < DW * DH) {
+        float x = GRAY_IN ? cur[k][0] : gray_op(sgray, cur[k][0], cur[k][1], cur[k][2]);
+        st[k] = (fresh && t == 0) ? x : iir_op(alpha, beta, x, st[k]);
+        int sy = i / DW, sx = i - sy * DW;
+        d[sy][sx] = double(st[k]);
+      }
+    }
+    if (t + 1 < n_frames) load(t + 1, nxt);
+    __syncthreads();
+    if (t >= n_warm) {
+      for (int i = tid; i < GW * GH; i += FT) {
+        int sy = i / GW, sx = i - sy * GW;
+        int cx = clampi(x0 + sx - 1, 0, W - 1) - (x0 - (R + 1));
+        int cy = clampi(y0 + sy - 1, 0, H - 1) - (y0 - (R + 1));
+        double acc = 0.0;
+#pragma unroll
+        for (int dy = 0; dy < K; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < K; ++dx)
+            acc = __fma_rn(w[dy * K + dx], d[cy - R + dy][cx - R + dx], acc);
+        g[sy][sx] = __double2float_rn(acc);
+      }
+    }
+    __syncthreads();
+    if (t >= n_warm) {
+      OutT* o = out + (long long)(t - n_warm) * hw;
+      for (int i = tid; i < FW * FH; i += FT) {
+        int ty = i / FW, tx = i - ty * FW;
+        int x = x0 + tx, y = y0 + ty;
+        if (x >= W || y >= H) continue;
+        float m =
+            sobel_op([&](int dx, int dy) { return g[ty + 1 + dy][tx + 1 + dx]; });
+        o[(long long)y * W + x] = from_level<OutT>(m >= th ? white : black);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) cur[k][c] = nxt[k][c];
+  }
+  if (state_out) {
+    // write back the state of the cells that are the tile's own pixels
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      int i = tid + k * FT;
+      int sy = i / DW, sx = i - sy * DW;
+      int x = x0 + sx - (R + 1), y = y0 + sy - (R + 1);
+      if (i < DW * DH && sx >= R + 1 && sx < R + 1 + FW && sy >= R + 1 &&
+          sy < R + 1 + FH && x < W && y < H)
+        state_out[(long long)y * W + x] = st[k];
+    }
+  }
+}
+
+// ------------------------------------------------------------ synthetic input
+
+__global__ void k_hash_video(uint8_t* __restrict__ out, long long n, int C, int H,
+                             int W, long long t0, unsigned long long seed_term) {
+  long long per_frame = (long long)C * H * W;
+  long long base = t0 * per_frame;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 16; i < n;
+       i += (long long)gridDim.x * blockDim.x * 16) {
+    if (i + 16 <= n) {
+      uint32_t words[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t wv = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          unsigned long long z = (unsigned long long)(base + i + q * 4 + b) + seed_term;
+          z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+          z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+          z ^= z >> 31;
+          wv |= uint32_t(z >> 56) << (8 * b);
+        }
+        words[q] = wv;
+      }
+      *reinterpret_cast<uint4*>(out + i) = make_uint4(words[0], words[1], words[2], words[3]);
+    } else {
+      for (long long j = i; j < n; ++j) {
+        unsigned long long z = (unsigned long long)(base + j) + seed_term;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        out[j] = uint8_t(z >> 56);
+      }
+    }
+  }
+}
+
+inline int grid_for(long long n, int block) {
+  long long g = (n + block - 1) / block;
+  return int(g > 148LL * 64 ? 148LL * 64 : (g < 1 ? 1 : g));
+}
+
+inline int status() { return int(cudaGetLastError()); }
+
+}  // namespace fc
+
+using namespace fc;
+
+extern "C" {
+
+const char* fc_error_string(int code) {
+  if (code == -1) return "unsupported kernel arguments";
+  return cudaGetErrorString(cudaError_t(code));
+}
+
+int fc_stage_spatial(const fc_stage* s, const void* in, int in_type, void* out,
+                     int out_type, fc_dims d, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  long long hw = (long long)d.width * d.height, n = hw * d.frames;
+  if (n == 0) return 0;
+  dim3 tiles((d.width + TW - 1) / TW, (d.height + TH - 1) / TH, d.frames);
+  switch (s->op) {
+    case FC_RGBA2GRAY:
+      if (out_type != FC_F32) return -1;
+      if (in_type == FC_U8)
+        k_rgba2gray<uint8_t><<<grid_for(n, 256), 256, 0, st>>>(
+            static_cast<const uint8_t*>(in), static_cast<float*>(out), *s, hw, n);
+      else
+        k_rgba2gray<float><<<grid_for(n, 256), 256, 0, st>>>(
+            static_cast<const float*>(in), static_cast<float*>(out), *s, hw, n);
+      return status();
+    case FC_GAUSSIAN: {
+      if (in_type != FC_F32 || out_type != FC_F32) return -1;
+      auto f = static_cast<const float*>(in);
+      auto o = static_cast<float*>(out);
+      dim3 b(TW, TH);
+      switch (s->g_radius) {
+        case 0: k_gaussian<0><<<tiles, b, 0, st>>>(f, o, *s, d.width, d.height); break;
+        case 1: k_gaussian<1><<<tiles, b, 0, st>>>(f, o, *s, d.width, d.height); break;
+        case 2: k_gaussian<2><<<tiles, b, 0, st>>>(f, o, *s, d.width, d.height); break;
+        case 3: k_gaussian<3><<<tiles, b, 0, st>>>(f, o, *s, d.width, d.height); break;
+        case 4: k_gaussian<4><<<tiles, b, 0, st>>>(f, o, *s, d.width, d.height); break;
+        default: return -1;
+      }
+      return status();
+    }
+    case FC_GRADIENT:
+      if (in_type != FC_F32 || out_type != FC_F32) return -1;
+      k_gradient<<<tiles, dim3(TW, TH), 0, st>>>(static_cast<const float*>(in),
+                                                 static_cast<float*>(out),
+                                                 d.width, d.height);
+      return status();
+    case FC_THRESHOLD:
+    case FC_IDENTITY:
+    case FC_SCALE_OFFSET:
+      if (s->op == FC_IDENTITY && in_type == FC_U8 && out_type == FC_F32) {
+        k_u8_to_f32<<<grid_for(n, 256), 256, 0, st>>>(
+            static_cast<const uint8_t*>(in), static_cast<float*>(out), n);
+        return status();
+      }
+      if (in_type != FC_F32) return -1;
+      if (out_type == FC_U8)
+        k_pointwise<uint8_t><<<grid_for(n, 256), 256, 0, st>>>(
+            static_cast<const float*>(in), static_cast<uint8_t*>(out), *s, n);
+      else
+        k_pointwise<float><<<grid_for(n, 256), 256, 0, st>>>(
+            static_cast<const float*>(in), static_cast<float*>(out), *s, n);
+      return status();
+    case FC_BOX_MEAN:
+      if (in_type != FC_F32 || out_type != FC_F32) return -1;
+      k_box_mean<<<grid_for(n, 256), 256, 0, st>>>(
+          static_cast<const float*>(in), static_cast<float*>(out), s->rx, s->ry,
+          s->rt, d.width, d.height, d.frames);
+      return status();
+    default:
+      return -1;
+  }
+}
+
+int fc_stage_iir(const fc_stage* s, const float* in, float* out, fc_dims d,
+                 int n_warm, const float* state_in, float* state_out,
+                 void* stream) {
+  long long hw = (long long)d.width * d.height;
+  if (hw == 0 || d.frames == 0) return 0;
+  float beta = 1.0f - s->alpha;  // host float arithmetic == reference's
+  k_iir<<<int((hw + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      in, out, s->alpha, beta, hw, d.frames, n_warm, state_in, state_out);
+  return status();
+}
+
+int fc_fused_gray_iir(const fc_stage* sg, const fc_stage* si, const void* video,
+                      int in_type, float* out, fc_dims d, int n_warm,
+                      const float* state_in, float* state_out, void* stream) {
+  long long hw = (long long)d.width * d.height;
+  if (hw == 0 || d.frames == 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float beta = 1.0f - si->alpha;
+  int grid = int((hw + 127) / 128);
+  if (in_type == FC_U8)
+    k_gray_iir<uint8_t><<<grid, 128, 0, st>>>(static_cast<const uint8_t*>(video),
+                                              out, *sg, si->alpha, beta, hw,
+                                              d.frames, n_warm, state_in, state_out);
+  else
+    k_gray_iir<float><<<grid, 128, 0, st>>>(static_cast<const float*>(video), out,
+                                            *sg, si->alpha, beta, hw, d.frames,
+                                            n_warm, state_in, state_out);
+  return status();
+}
+
+int fc_fused_gauss_grad_thr(const fc_stage* sg, const fc_stage* /*sgrad*/,
+                            const fc_stage* sthr, const float* in, void* out,
+                            int out_type, fc_dims d, void* stream) {
+  if ((long long)d.width * d.height * d.frames == 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  dim3 grid((d.width + FW - 1) / FW, (d.height + FH - 1) / FH, d.frames);
+#define FC_GGT(R, T)                                                              \
+  k_gauss_grad_thr<R, T><<<grid, FT, 0, st>>>(in, static_cast<T*>(out), *sg,     \
+                                              sthr->th, sthr->white, sthr->black, \
+                                              d.width, d.height)
+#define FC_GGT_R(T)            \
+  switch (sg->g_radius) {      \
+    case 0: FC_GGT(0, T); break; \
+    case 1: FC_GGT(1, T); break; \
+    case 2: FC_GGT(2, T); break; \
+    case 3: FC_GGT(3, T); break; \
+    case 4: FC_GGT(4, T); break; \
+    default: return -1;        \
+  }
+  if (out_type == FC_U8) {
+    FC_GGT_R(uint8_t)
+  } else {
+    FC_GGT_R(float)
+  }
+#undef FC_GGT_R
+#undef FC_GGT
+  return status();
+}
+
+// Exact streaming chain; the certified fast variant lives in fc_fast.cu and
+// is dispatched from there (fc_fused_chain).
+int fc_chain_exact(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                   const fc_stage* sthr, const void* video, int in_type,
+                   int gray_in, void* out, int out_type, fc_dims d, int n_warm,
+                   const float* state_in, float* state_out, void* stream) {
+  if ((long long)d.width * d.height * d.frames == 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  dim3 grid((d.width + FW - 1) / FW, (d.height + FH - 1) / FH);
+  float beta = 1.0f - si->alpha;
+  fc_stage gdummy = {};
+  const fc_stage& sgr = sgray ? *sgray : gdummy;
+#define FC_CH(R, IT, OT, GI)                                                     \
+  k_chain_exact<R, IT, OT, GI><<<grid, FT, 0, st>>>(                            \
+      static_cast<const IT*>(video), static_cast<OT*>(out), sgr, si->alpha,     \
+      beta, *sg, sthr->th, sthr->white, sthr->black, d.width, d.height,         \
+      d.frames, n_warm, state_in, state_out)
+#define FC_CH_GI(R, IT, OT) \
+  if (gray_in) FC_CH(R, IT, OT, true); else FC_CH(R, IT, OT, false);
+#define FC_CH_OT(R, IT) \
+  if (out_type == FC_U8) { FC_CH_GI(R, IT, uint8_t) } else { FC_CH_GI(R, IT, float) }
+#define FC_CH_IT(R) \
+  if (in_type == FC_U8) { FC_CH_OT(R, uint8_t) } else { FC_CH_OT(R, float) }
+  switch (sg->g_radius) {
+    case 1: FC_CH_IT(1) break;
+    case 2: FC_CH_IT(2) break;
+    case 3: FC_CH_IT(3) break;
+    default: return -1;
+  }
+#undef FC_CH_IT
+#undef FC_CH_OT
+#undef FC_CH_GI
+#undef FC_CH
+  return status();
+}
+
+int fc_hash_video_u8(uint8_t* out, fc_dims d, int channels, int t0,
+                     uint64_t seed, void* stream) {
+  long long n = (long long)d.width * d.height * d.frames * channels;
+  if (n == 0) return 0;
+  unsigned long long seed_term = (unsigned long long)seed * 0x9E3779B97F4A7C15ull;
+  k_hash_video<<<grid_for((n + 15) / 16, 256), 256, 0,
+                 static_cast<cudaStream_t>(stream)>>>(out, n, channels, d.height,
+                                                      d.width, t0, seed_term);
+  return status();
+}
+
+}  // extern "C"

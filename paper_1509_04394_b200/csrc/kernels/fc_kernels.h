@@ -1,0 +1,112 @@
+/* Thin C ABI between the C++ host (executor.cpp) and the sm_100a kernels.
+ * Raw device pointers, plain sizes, a cudaStream_t passed as void*, int
+ * status (0 = ok, else a cudaError_t value; -1 = unsupported arguments).
+ *
+ * Layouts (HBM):
+ *   video  : planar u8 or f32, [t][c][y][x]   (the FPVD payload order,
+ *            /root/reference/proj/include/fuseplan/video.hpp:24-28)
+ *   planes : f32 [t][y][x] for every intermediate stage
+ *   mask   : u8  [t][y][x] (threshold output when white/black are bytes)
+ */
+#ifndef FC_KERNELS_H
+#define FC_KERNELS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum fc_op {
+  FC_RGBA2GRAY = 0,
+  FC_IIR_TEMPORAL = 1,
+  FC_GAUSSIAN = 2,
+  FC_GRADIENT = 3,
+  FC_THRESHOLD = 4,
+  FC_IDENTITY = 5,
+  FC_SCALE_OFFSET = 6,
+  FC_BOX_MEAN = 7
+};
+
+#define FC_MAX_GAUSS_RADIUS 4
+
+/* Parameters of one stencil stage, already converted the way the reference
+ * converts them (float(param) for float ops, simulator.cpp:51-106; gaussian
+ * taps from simulator.cpp:27-44 computed on the host with std::exp). */
+typedef struct {
+  int op;
+  float wr, wg, wb;          /* rgba2gray */
+  float alpha;               /* iir_temporal */
+  int g_radius;              /* gaussian */
+  float g_w[(2 * FC_MAX_GAUSS_RADIUS + 1) * (2 * FC_MAX_GAUSS_RADIUS + 1)];
+  float th, white, black;    /* threshold */
+  float scale, offset;       /* scale_offset */
+  int rx, ry, rt;            /* box_mean */
+} fc_stage;
+
+typedef struct {
+  int width, height, frames;
+} fc_dims;
+
+/* Element type codes. */
+enum { FC_U8 = 0, FC_F32 = 1 };
+
+/* ---- unfused stages (the paper's sequential baseline) -------------------
+ * One launch per stage over the whole volume; input/output f32 planes except
+ * rgba2gray (video in, 4 channels, u8 or f32) and threshold (u8 or f32 out).
+ * IIR stages take the streaming-range arguments described below. */
+int fc_stage_spatial(const fc_stage* st, const void* in, int in_type,
+                     void* out, int out_type, fc_dims d, void* stream);
+
+/* Streaming range for anything containing the causal IIR:
+ *   in/out point at the first processed frame; n_frames are processed; the
+ *   first n_warm are warm-up frames (state only, no output written; out
+ *   then points at the first OUTPUT frame).  state_in (nullable): IIR plane
+ *   to resume from; NULL restarts the recurrence at the first processed
+ *   frame (y = x, simulator.cpp:57-62).  state_out (nullable): IIR plane after
+ *   the last processed frame. */
+int fc_stage_iir(const fc_stage* st, const float* in, float* out, fc_dims d,
+                 int n_warm, const float* state_in, float* state_out,
+                 void* stream);
+
+/* ---- fused partitions ----------------------------------------------------
+ * F12   : rgba2gray + iir                 video -> f32 planes  (time scan)
+ * F345  : gaussian + gradient + threshold f32 planes -> mask   (per frame)
+ * F12345: the whole SPEC chain            video -> mask        (streaming)
+ * `gray_in` for F12345 = 1 when the video is already single-channel (the
+ * chain then starts at the IIR; s_gray is ignored). */
+int fc_fused_gray_iir(const fc_stage* s_gray, const fc_stage* s_iir,
+                      const void* video, int in_type, float* out, fc_dims d,
+                      int n_warm, const float* state_in, float* state_out,
+                      void* stream);
+
+int fc_fused_gauss_grad_thr(const fc_stage* s_gauss, const fc_stage* s_grad,
+                            const fc_stage* s_thr, const float* in, void* out,
+                            int out_type, fc_dims d, void* stream);
+
+/* variant: 0 = auto, 1 = exact (FP64 gaussian everywhere),
+ *          2 = certified FP32 fast path with exact recheck */
+int fc_fused_chain(const fc_stage* s_gray, const fc_stage* s_iir,
+                   const fc_stage* s_gauss, const fc_stage* s_grad,
+                   const fc_stage* s_thr, const void* video, int in_type,
+                   int gray_in, void* out, int out_type, fc_dims d, int n_warm,
+                   const float* state_in, float* state_out, int variant,
+                   void* stream);
+
+/* Deterministic counter-hash u8 video (splitmix64 finaliser of
+ * index + seed * 0x9E3779B97F4A7C15, top byte), [t][c][y][x]; frames
+ * [t0, t0 + d.frames).  Mirrors tests/golden/make_golden.py:hash_video. */
+int fc_hash_video_u8(uint8_t* out, fc_dims d, int channels, int t0,
+                     uint64_t seed, void* stream);
+
+/* Count of pixels that took the exact recheck path in the last certified
+ * launch on this stream's device (diagnostic; 0 if unavailable). */
+long long fc_last_recheck_count(void);
+
+const char* fc_error_string(int code);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

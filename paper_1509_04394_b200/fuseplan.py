@@ -1,0 +1,373 @@
+"""Python binding of the fuseplan C ABI (include/fuseplan.h) -- the
+reference-facing surface of this build, loaded from the in-tree
+libfuseplan_b200.so.
+
+Mirrors the reference's handles and status taxonomy
+(/root/reference/proj/include/fuseplan.h:14-93): ``Pipeline`` / ``Device`` /
+``Plan`` wrap the opaque handles, failures raise ``FuseplanError`` subclasses
+carrying the fp_status code (Input -> 2, Infeasible -> 1, Internal -> 3) and
+the thread-local fp_last_error() text.  ``Executor`` is the new device
+executor (fp_exec_*): it takes torch CUDA tensors (zero-copy, asynchronous on
+the current torch stream) or host numpy / torch CPU arrays (streamed through
+the device, synchronous).
+
+There is no CPU execution path: without the .so or without a CUDA device the
+executor raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from typing import Optional, Union
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libfuseplan_b200.so")
+DATA_DIR = os.path.join(PKG, "data")
+
+FP_OK, FP_ERR_INFEASIBLE, FP_ERR_INPUT, FP_ERR_INTERNAL = 0, 1, 2, 3
+FP_ELEM_U8, FP_ELEM_F32 = 0, 1
+FP_EXEC_HOST_PTRS, FP_EXEC_DEVICE_PTRS = 0, 1
+
+
+class FuseplanError(RuntimeError):
+    status = FP_ERR_INTERNAL
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+
+
+class InfeasibleError(FuseplanError):
+    status = FP_ERR_INFEASIBLE
+
+
+class InputError(FuseplanError):
+    status = FP_ERR_INPUT
+
+
+class InternalError(FuseplanError):
+    status = FP_ERR_INTERNAL
+
+
+_ERRORS = {FP_ERR_INFEASIBLE: InfeasibleError, FP_ERR_INPUT: InputError,
+           FP_ERR_INTERNAL: InternalError}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded C ABI.  Raises if the extension has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: run `python -m paper_1509_04394_b200.build` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I, S, V = ctypes.c_void_p, ctypes.c_int, ctypes.c_char_p, None
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    PS = ctypes.POINTER(ctypes.c_char_p)
+    sig = {
+        "fp_last_error": ([], ctypes.c_char_p),
+        "fp_string_free": ([P], V),
+        "fp_pipeline_parse": ([S, PP], I),
+        "fp_pipeline_load": ([S, PP], I),
+        "fp_pipeline_free": ([P], V),
+        "fp_device_parse": ([S, PP], I),
+        "fp_device_load": ([S, PP], I),
+        "fp_device_free": ([P], V),
+        "fp_plan_create": ([P, P, S, PP], I),
+        "fp_plan_free": ([P], V),
+        "fp_plan_render_json": ([P, PP], I),
+        "fp_analyze_report": ([P, S, I, PP], I),
+        "fp_plan_report": ([P, S, I, PP], I),
+        "fp_tile_sweep": ([P, ctypes.POINTER(ctypes.c_int), I, I, S, PP], I),
+        "fp_codegen": ([P, P, S, S, S, PP], I),
+        "fp_simulate": ([P, P, S, S, S, S, S, I, PP], I),
+        "fp_calibrate_csv": ([S, PP], I),
+        "fp_device_render_with_cost": ([P, S, PP], I),
+        "fp_exec_create": ([P, P, I, S, PP], I),
+        "fp_exec_free": ([P], V),
+        "fp_exec_output_type": ([P, ctypes.POINTER(ctypes.c_int)], I),
+        "fp_exec_state_planes": ([P, ctypes.POINTER(ctypes.c_int)], I),
+        "fp_exec_run": ([P, P, I, P, I, P], I),
+        "fp_exec_run_range": ([P, P, I, P, I, I, P, P, P], I),
+        "fp_exec_describe": ([P, PP], I),
+        "fp_synth_hash_u8": ([P, I, I, I, I, I, ctypes.c_uint64, P], I),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def _check(status: int) -> None:
+    if status != FP_OK:
+        msg = lib().fp_last_error().decode(errors="replace")
+        raise _ERRORS.get(status, InternalError)(msg)
+
+
+def _take_string(ptr: ctypes.c_void_p) -> str:
+    s = ctypes.cast(ptr, ctypes.c_char_p).value.decode()
+    lib().fp_string_free(ptr)
+    return s
+
+
+def _enc(s: Optional[str]):
+    return None if s is None else s.encode()
+
+
+def _opts(options: Union[None, str, dict]) -> Optional[bytes]:
+    if options is None:
+        return None
+    return (options if isinstance(options, str) else json.dumps(options)).encode()
+
+
+class _Handle:
+    _free = ""
+
+    def __init__(self, ptr):
+        self._ptr = ptr
+
+    def __del__(self):
+        p = getattr(self, "_ptr", None)
+        if p and _lib is not None:
+            getattr(_lib, self._free)(p)
+            self._ptr = None
+
+    @property
+    def ptr(self):
+        return self._ptr
+
+
+class Pipeline(_Handle):
+    """fp_pipeline: a validated kernel chain (parse_pipeline, config.cpp:98-159)."""
+    _free = "fp_pipeline_free"
+
+    def __init__(self, json_text: str):
+        out = ctypes.c_void_p()
+        _check(lib().fp_pipeline_parse(json_text.encode(), ctypes.byref(out)))
+        super().__init__(out)
+        self.json = json_text
+        self.spec = json.loads(json_text)
+
+    @classmethod
+    def load(cls, path: str) -> "Pipeline":
+        with open(path) as fh:
+            return cls(fh.read())
+
+    @property
+    def dims(self):
+        v = self.spec["video"]
+        return v["width"], v["height"], v["frames"], v.get("channels", 1)
+
+    def analyze(self, fmt: str = "text", timestamp: bool = False) -> str:
+        out = ctypes.c_void_p()
+        _check(lib().fp_analyze_report(self.ptr, fmt.encode(), int(timestamp),
+                                       ctypes.byref(out)))
+        return _take_string(out)
+
+
+class Device(_Handle):
+    """fp_device: a device profile (parse_device, config.cpp:161-190)."""
+    _free = "fp_device_free"
+
+    def __init__(self, json_text: str):
+        out = ctypes.c_void_p()
+        _check(lib().fp_device_parse(json_text.encode(), ctypes.byref(out)))
+        super().__init__(out)
+        self.json = json_text
+
+    @classmethod
+    def load(cls, path_or_name: str) -> "Device":
+        path = path_or_name
+        if not os.path.exists(path):
+            bundled = os.path.join(DATA_DIR, path_or_name + ".json")
+            if os.path.exists(bundled):
+                path = bundled
+        with open(path) as fh:
+            return cls(fh.read())
+
+    def tile_sweep(self, halo, max_x: int, max_t: int, fmt: str = "csv") -> str:
+        arr = (ctypes.c_int * 6)(*halo)
+        out = ctypes.c_void_p()
+        _check(lib().fp_tile_sweep(self.ptr, arr, max_x, max_t, fmt.encode(),
+                                   ctypes.byref(out)))
+        return _take_string(out)
+
+
+class Plan(_Handle):
+    """fp_plan: the optimizer's fusion plan (plan(), planner.cpp:342-393)."""
+    _free = "fp_plan_free"
+
+    def __init__(self, pipeline: Pipeline, device: Device,
+                 options: Union[None, str, dict] = None):
+        out = ctypes.c_void_p()
+        _check(lib().fp_plan_create(pipeline.ptr, device.ptr, _opts(options),
+                                    ctypes.byref(out)))
+        super().__init__(out)
+        self.pipeline = pipeline
+
+    def render_json(self) -> str:
+        out = ctypes.c_void_p()
+        _check(lib().fp_plan_render_json(self.ptr, ctypes.byref(out)))
+        return _take_string(out)
+
+    def report(self, fmt: str = "text", timestamp: bool = False) -> str:
+        out = ctypes.c_void_p()
+        _check(lib().fp_plan_report(self.ptr, fmt.encode(), int(timestamp),
+                                    ctypes.byref(out)))
+        return _take_string(out)
+
+    @property
+    def partition(self):
+        return [(g["interval"]["first"], g["interval"]["last"])
+                for g in json.loads(self.render_json())["groups"]]
+
+
+def simulate(pipeline: Pipeline, device: Device, options=None, video_path=None,
+             synth: Union[None, str, dict] = None, fmt: str = "text",
+             timestamp: bool = False) -> str:
+    out = ctypes.c_void_p()
+    _check(lib().fp_simulate(pipeline.ptr, device.ptr, _opts(options),
+                             _enc(video_path), _opts(synth), None, fmt.encode(),
+                             int(timestamp), ctypes.byref(out)))
+    return _take_string(out)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class Executor(_Handle):
+    """fp_exec: runs a plan's partitions as sm_100a kernels on one GPU."""
+    _free = "fp_exec_free"
+
+    def __init__(self, pipeline: Pipeline, plan: Plan, device: int = 0,
+                 variant: str = "auto", host_chunk_frames: int = 0):
+        out = ctypes.c_void_p()
+        opts = json.dumps({"variant": variant, "host_chunk_frames": host_chunk_frames})
+        _check(lib().fp_exec_create(pipeline.ptr, plan.ptr, device, opts.encode(),
+                                    ctypes.byref(out)))
+        super().__init__(out)
+        self.pipeline = pipeline
+        self.device = device
+        t = ctypes.c_int()
+        _check(lib().fp_exec_output_type(self.ptr, ctypes.byref(t)))
+        self.out_elem = t.value
+        _check(lib().fp_exec_state_planes(self.ptr, ctypes.byref(t)))
+        self.state_planes = t.value
+
+    def describe(self) -> dict:
+        out = ctypes.c_void_p()
+        _check(lib().fp_exec_describe(self.ptr, ctypes.byref(out)))
+        return json.loads(_take_string(out))
+
+    @property
+    def out_dtype(self):
+        return np.uint8 if self.out_elem == FP_ELEM_U8 else np.float32
+
+    def _elem(self, dtype) -> int:
+        if dtype in (np.uint8,) or str(dtype) in ("torch.uint8", "uint8"):
+            return FP_ELEM_U8
+        if dtype in (np.float32,) or str(dtype) in ("torch.float32", "float32"):
+            return FP_ELEM_F32
+        raise InputError(f"video dtype must be uint8 or float32, got {dtype}")
+
+    def run(self, video, out=None, stream=None):
+        """video: planar [F, C, H, W].  CUDA tensor -> CUDA tensor (async on the
+        current torch stream); numpy / CPU tensor -> numpy (synchronous)."""
+        W, H, F, C = self.pipeline.dims
+        if tuple(video.shape) != (F, C, H, W):
+            raise InputError(f"video shape {tuple(video.shape)} != {(F, C, H, W)}")
+        is_torch = type(video).__module__.startswith("torch")
+        if is_torch and video.is_cuda:
+            torch = _torch()
+            video = video.contiguous()
+            if out is None:
+                out = torch.empty((F, H, W), device=video.device,
+                                  dtype=torch.uint8 if self.out_elem == FP_ELEM_U8
+                                  else torch.float32)
+            if stream is None:
+                stream = torch.cuda.current_stream(video.device).cuda_stream
+            _check(lib().fp_exec_run(self.ptr, video.data_ptr(), self._elem(video.dtype),
+                                     out.data_ptr(), FP_EXEC_DEVICE_PTRS, stream))
+            return out
+        arr = video.numpy() if is_torch else np.asarray(video)
+        arr = np.ascontiguousarray(arr)
+        if out is None:
+            out = np.empty((F, H, W), self.out_dtype)
+        _check(lib().fp_exec_run(self.ptr, arr.ctypes.data, self._elem(arr.dtype),
+                                 out.ctypes.data, FP_EXEC_HOST_PTRS, None))
+        return out
+
+    def run_range(self, video, n_warm: int = 0, state_in=None, state_out=None,
+                  out=None, stream=None):
+        """T-shard run on CUDA tensors: video [n, C, H, W] starting at the first
+        processed frame; returns [n - n_warm, H, W]."""
+        torch = _torch()
+        n = int(video.shape[0])
+        W, H = int(video.shape[3]), int(video.shape[2])
+        video = video.contiguous()
+        if out is None:
+            out = torch.empty((n - n_warm, H, W), device=video.device,
+                              dtype=torch.uint8 if self.out_elem == FP_ELEM_U8
+                              else torch.float32)
+        if stream is None:
+            stream = torch.cuda.current_stream(video.device).cuda_stream
+        _check(lib().fp_exec_run_range(
+            self.ptr, video.data_ptr(), self._elem(video.dtype), out.data_ptr(), n,
+            n_warm, None if state_in is None else state_in.data_ptr(),
+            None if state_out is None else state_out.data_ptr(), stream))
+        return out
+
+
+def synth_hash_u8(out, t0: int = 0, seed: int = 1234, stream=None):
+    """Fill a CUDA uint8 tensor [F, C, H, W] with the counter-hash test video."""
+    torch = _torch()
+    F, C, H, W = out.shape
+    if stream is None:
+        stream = torch.cuda.current_stream(out.device).cuda_stream
+    _check(lib().fp_synth_hash_u8(out.data_ptr(), W, H, F, C, t0, seed, stream))
+    return out
+
+
+def hash_video_u8(frames: int, channels: int, height: int, width: int, seed: int,
+                  t0: int = 0) -> np.ndarray:
+    """Host copy of the counter-hash video (same values as synth_hash_u8)."""
+    t = np.arange(t0, t0 + frames, dtype=np.uint64)[:, None, None, None]
+    c = np.arange(channels, dtype=np.uint64)[None, :, None, None]
+    y = np.arange(height, dtype=np.uint64)[None, None, :, None]
+    x = np.arange(width, dtype=np.uint64)[None, None, None, :]
+    with np.errstate(over="ignore"):
+        idx = ((t * np.uint64(channels) + c) * np.uint64(height) + y) * np.uint64(width) + x
+        z = idx + np.uint64((seed * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(56)).astype(np.uint8)
+
+
+def spec_chain(width: int, height: int, frames: int, alpha: float = 0.5,
+               radius: int = 2, sigma: float = 1.0, th: float = 128.0,
+               kalman: bool = False, channels: int = 4) -> dict:
+    """The SPEC chain (proj/data/vision_pipeline.json:4-8) at a given size."""
+    ks = []
+    if channels == 4:
+        ks.append({"name": "rgba_to_gray", "stencil_op": "rgba2gray"})
+    ks += [{"name": "temporal_denoise", "stencil_op": "iir_temporal",
+            "params": {"alpha": alpha}},
+           {"name": "gaussian_smooth", "stencil_op": "gaussian",
+            "params": {"radius": radius, "sigma": sigma}},
+           {"name": "gradient_magnitude", "stencil_op": "gradient"},
+           {"name": "binarize", "stencil_op": "threshold", "params": {"th": th}}]
+    if kalman:
+        ks.append({"name": "kalman_tracking", "stencil_op": "kalman_track"})
+    return {"video": {"width": width, "height": height, "frames": frames, "fps": 1,
+                      "channels": channels}, "kernels": ks}

@@ -1,0 +1,94 @@
+"""The C-ABI library loads and exports every entry point include/fuseplan.h
+declares; handle / status / ownership conventions match the reference's
+tests/test_capi.cpp (no GPU needed for these)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "fuseplan.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_reference_abi():
+    names = declared_functions()
+    reference = ["fp_last_error", "fp_string_free", "fp_pipeline_parse",
+                 "fp_pipeline_load", "fp_pipeline_free", "fp_device_parse",
+                 "fp_device_load", "fp_device_free", "fp_plan_create", "fp_plan_free",
+                 "fp_plan_render_json", "fp_analyze_report", "fp_plan_report",
+                 "fp_tile_sweep", "fp_codegen", "fp_simulate", "fp_calibrate_csv",
+                 "fp_device_render_with_cost"]
+    for n in reference:
+        assert n in names, n
+
+
+def test_library_exports_every_declared_symbol(fp):
+    L = fp.lib()
+    for name in declared_functions():
+        assert hasattr(L, name), f"{name} not exported"
+
+
+def test_null_arguments_are_input_errors(fp):
+    L = fp.lib()
+    out = ctypes.c_void_p()
+    assert L.fp_plan_create(None, None, None, ctypes.byref(out)) == fp.FP_ERR_INPUT
+    assert b"null" in L.fp_last_error()
+    assert L.fp_pipeline_parse(None, ctypes.byref(out)) == fp.FP_ERR_INPUT
+
+
+def test_device_load_errors(fp):
+    L = fp.lib()
+    out = ctypes.c_void_p()
+    assert L.fp_device_load(b"/nonexistent/device.json", ctypes.byref(out)) == \
+        fp.FP_ERR_INPUT
+    os.environ["FUSEPLAN_DEVICE_DIR"] = fp.DATA_DIR
+    assert L.fp_device_load(b"k20_like", ctypes.byref(out)) == fp.FP_OK
+    L.fp_device_free(out)
+
+
+def test_render_json_owned_string(fp):
+    p = fp.Pipeline.load(os.path.join(fp.DATA_DIR, "vision_pipeline.json"))
+    plan = fp.Plan(p, fp.Device.load("k20_like"))
+    js = plan.render_json()
+    assert '"schema_version": 1' in js
+
+
+def test_pipeline_validation_errors(fp):
+    bad = [
+        '{"video": {"width": 8, "height": 8, "frames": 2, "channels": 1},'
+        ' "kernels": [{"stencil_op": "rgba2gray"}]}',                       # channels
+        '{"video": {"width": 8, "height": 8, "frames": 2, "channels": 1},'
+        ' "kernels": [{"stencil_op": "warp"}]}',                            # unknown op
+        '{"video": {"width": 8, "height": 8, "frames": 2, "channels": 1},'
+        ' "kernels": [{"stencil_op": "gaussian", "halo": {"x_lo": -1}}]}',  # negative
+        '{"video": {"width": 0, "height": 8, "frames": 2},'
+        ' "kernels": [{"stencil_op": "identity"}]}',                        # width
+        '{"video": {"width": 8, "height": 8}, "kernels": []}',             # frames
+    ]
+    for text in bad:
+        with pytest.raises(fp.InputError):
+            fp.Pipeline(text)
+
+
+def test_executor_without_gpu_fails_loudly(fp):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    p = fp.Pipeline.load(os.path.join(fp.DATA_DIR, "vision_pipeline.json"))
+    plan = fp.Plan(p, fp.Device.load("k20_like"))
+    with pytest.raises(fp.InternalError):
+        fp.Executor(p, plan)
+
+
+def test_out_of_scope_entry_points_report_input_error(fp):
+    L = fp.lib()
+    out = ctypes.c_void_p()
+    assert L.fp_calibrate_csv(b"n_kernels\n", ctypes.byref(out)) == fp.FP_ERR_INPUT

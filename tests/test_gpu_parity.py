@@ -1,0 +1,186 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI, against the
+reference's golden vectors and the oracle -- bit-exact for every element
+(masks and float planes alike; the reference semantics are reproduced
+operation for operation)."""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CHAINS, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def partitions(pipe):
+    """No / Two / Full fusion + the optimizer's choice (capi.cpp:149-168)."""
+    ks = pipe["kernels"]
+    n = len(ks)
+    agg = [i + 1 for i, k in enumerate(ks) if k["stencil_op"] == "kalman_track"]
+    last = n - len(agg)
+    tail = ",".join(str(a) for a in agg)
+    none = ",".join(str(i) for i in range(1, last + 1))
+    full = f"1-{last}" if last > 1 else "1"
+    two = f"1-2,3-{last}" if last >= 3 else full
+    out = {"none": none, "two": two, "full": full}
+    return {k: (v + ("," + tail if tail else "")) for k, v in out.items()}
+
+
+def run(fp, pipe, video, options=None, variant="auto", device="b200", torch_dev=None,
+        chunk=0):
+    p = fp.Pipeline(json.dumps(pipe))
+    plan = fp.Plan(p, fp.Device.load(device), options)
+    ex = fp.Executor(p, plan, variant=variant, host_chunk_frames=chunk)
+    if torch_dev is not None:
+        import torch
+        v = torch.from_numpy(np.ascontiguousarray(video)).to(torch_dev)
+        out = ex.run(v)
+        torch.cuda.synchronize()
+        return out.cpu().numpy().astype(np.float32), ex
+    return ex.run(video).astype(np.float32), ex
+
+
+@pytest.mark.parametrize("name", GOLDEN_CHAINS)
+@pytest.mark.parametrize("part", ["default", "none", "two", "full"])
+def test_golden_partitions(fp, cuda, name, part):
+    g = load_golden(name)
+    pipe = json.loads(str(g["pipeline"]))
+    opts = None if part == "default" else {"force_partition": partitions(pipe)[part]}
+    try:
+        out, ex = run(fp, pipe, g["video"], opts, torch_dev=cuda)
+    except fp.InfeasibleError:
+        pytest.skip("partition infeasible under the device profile")
+    np.testing.assert_array_equal(out, g["final"])
+
+
+@pytest.mark.parametrize("name", GOLDEN_CHAINS)
+@pytest.mark.parametrize("variant", ["exact", "auto"])
+def test_golden_host_pointers_chunked(fp, cuda, name, variant):
+    g = load_golden(name)
+    pipe = json.loads(str(g["pipeline"]))
+    out, _ = run(fp, pipe, g["video"], {"force_partition": partitions(pipe)["full"]},
+                 variant=variant, chunk=3)
+    np.testing.assert_array_equal(out, g["final"])
+
+
+@pytest.mark.parametrize("name", [n for n in GOLDEN_CHAINS if "stages" in load_golden(n)])
+def test_golden_every_stage_plane(fp, cuda, name):
+    """Truncated chains expose every intermediate plane: each must equal the
+    reference's stage_outputs[k] (simulator.hpp:37-42) bit for bit."""
+    g = load_golden(name)
+    pipe = json.loads(str(g["pipeline"]))
+    for k in range(1, len(pipe["kernels"]) + 1):
+        sub = dict(pipe, kernels=pipe["kernels"][:k])
+        for part in ("none", "full"):
+            opts = {"force_partition": partitions(sub)[part]}
+            out, _ = run(fp, sub, g["video"], opts, torch_dev=cuda)
+            np.testing.assert_array_equal(out, g["stages"][k - 1],
+                                          err_msg=f"stage {k} {part}")
+
+
+def test_f32_video_input(fp, cuda, oracle):
+    g = load_golden("synth_64x48x20")
+    pipe = json.loads(str(g["pipeline"]))
+    rng = np.random.default_rng(3)
+    v = (g["video"].astype(np.float32) + rng.uniform(-0.49, 0.49, g["video"].shape)
+         ).clip(0, 255).astype(np.float32)
+    want = oracle.orc_chain(pipe, v)
+    for part in ("none", "two", "full"):
+        out, _ = run(fp, pipe, v, {"force_partition": partitions(pipe)[part]},
+                     torch_dev=cuda)
+        np.testing.assert_array_equal(out, want, err_msg=part)
+
+
+def test_larger_hash_video_dense_mask(fp, cuda, oracle):
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    pipe = spec_chain(200, 150, 24, th=24.0)
+    v = hash_video_u8(24, 4, 150, 200, 77)
+    want = oracle.orc_chain(pipe, v)
+    assert 0.05 < (want == 255).mean() < 0.95
+    for part in ("none", "two", "full"):
+        for variant in ("exact", "auto"):
+            out, _ = run(fp, pipe, v, {"force_partition": partitions(pipe)[part]},
+                         variant=variant, torch_dev=cuda)
+            np.testing.assert_array_equal(out, want, err_msg=f"{part} {variant}")
+
+
+def test_state_carry_and_warm_restart(fp, cuda, oracle):
+    """run_range: resuming from the carried state is exact; a warm-up restart
+    equals the oracle's restart semantics at the same frame."""
+    import torch
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    F = 30
+    pipe = spec_chain(96, 64, F, th=24.0)
+    v = hash_video_u8(F, 4, 64, 96, 5)
+    full = oracle.orc_chain(pipe, v)
+    p = fp.Pipeline(json.dumps(pipe))
+    for part in ("1-5", "1-2,3-5", "1,2,3,4,5"):
+        plan = fp.Plan(p, fp.Device.load("b200"), {"force_partition": part})
+        ex = fp.Executor(p, plan)
+        vt = torch.from_numpy(v).to(cuda)
+        st = torch.empty((1, 64, 96), device=cuda)
+        a = ex.run_range(vt[:13], state_out=st)
+        b = ex.run_range(vt[13:], state_in=st)
+        torch.cuda.synchronize()
+        got = torch.cat([a, b]).cpu().numpy().astype(np.float32)
+        np.testing.assert_array_equal(got, full, err_msg=part)
+        # warm restart at frame 20 - 8
+        w = ex.run_range(vt[12:], n_warm=8)
+        torch.cuda.synchronize()
+        want = oracle.orc_chain(pipe, v, t_begin=12, t_out=20)
+        np.testing.assert_array_equal(w.cpu().numpy().astype(np.float32), want,
+                                      err_msg=part)
+
+
+def test_device_hash_generator_matches_host(fp, cuda):
+    import torch
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, synth_hash_u8
+    out = torch.empty((5, 4, 33, 47), dtype=torch.uint8, device=cuda)
+    synth_hash_u8(out, t0=7, seed=1234)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy(), hash_video_u8(5, 4, 33, 47, 1234, 7))
+
+
+def test_random_catalog_chains(fp, cuda, oracle):
+    """The reference's randomized suites (test_simulator.cpp:228-243,
+    acceptance.cpp:276-320) over the whole catalog, on the GPU executor."""
+    rng = np.random.default_rng(2024)
+    pool = [("identity", {}), ("scale_offset", {"scale": 1.5, "offset": 3.0}),
+            ("gaussian", {"radius": 1, "sigma": 1.0}), ("gradient", {}),
+            ("threshold", {"th": 32.0}),
+            ("box_mean", {"radius_x": 1, "radius_y": 1, "radius_t": 1}),
+            ("iir_temporal", {"alpha": 0.25})]
+    for trial in range(30):
+        w, h, f = (int(rng.choice([8, 16, 24, 32])), int(rng.choice([8, 16, 24, 32])),
+                   int(rng.choice([8, 16, 24, 32])) // 2)
+        ks = []
+        for i in range(int(rng.integers(2, 6))):
+            op, params = pool[int(rng.integers(0, len(pool)))]
+            ks.append({"name": f"k{i}", "stencil_op": op, "params": params})
+        pipe = {"video": {"width": w, "height": h, "frames": f, "channels": 1},
+                "kernels": ks}
+        vid = rng.uniform(0, 255, (f, 1, h, w)).astype(np.float32)
+        want = oracle.orc_run_sequential(pipe, vid)[-1]
+        for opts in (None, {"force_partition": ",".join(str(i + 1) for i in range(len(ks)))}):
+            out, _ = run(fp, pipe, vid, opts, device="k20_like", torch_dev=cuda)
+            np.testing.assert_array_equal(out, want, err_msg=f"trial {trial} {opts}")
+
+
+def test_simulate_reports_identical_outputs(fp, cuda):
+    """test_capi.cpp:136-160 through the GPU-backed fp_simulate."""
+    pipe = fp.Pipeline(json.dumps({
+        "video": {"width": 32, "height": 32, "frames": 6, "channels": 1},
+        "kernels": [{"name": "smooth", "stencil_op": "gaussian",
+                     "params": {"radius": 1, "sigma": 1.0}},
+                    {"name": "bin", "stencil_op": "threshold", "params": {"th": 100}}]}))
+    dev = fp.Device.load("k20_like")
+    rep = fp.simulate(pipe, dev, synth={"width": 32, "height": 32, "frames": 6,
+                                        "channels": 1,
+                                        "markers": [{"x": 16, "y": 16, "radius": 4}]})
+    assert "outputs identical: true" in rep
+    assert "Full Fusion" in rep
+    bundled = fp.Pipeline.load(fp.DATA_DIR + "/vision_pipeline.json")
+    rep = fp.simulate(bundled, dev, synth={"width": 64, "height": 64, "frames": 32,
+                                           "channels": 4, "noise_sigma": 8, "seed": 1234,
+                                           "markers": [{"x": 20, "y": 20, "vx": 1}]})
+    assert "outputs identical: true" in rep
