@@ -230,7 +230,8 @@ void Executor::run_device(const void* video, int in_type, void* out, int n_frame
   if (n_frames == 0) return;
 
   // two f32 ping-pong planes of the largest frame count in flight
-  std::size_t plane_bytes = std::size_t(hw) * n_frames * sizeof(float);
+  std::size_t plane_bytes =
+      (std::size_t(hw) * n_frames * sizeof(float) + 255) & ~std::size_t(255);
   bool need_scratch = in_type == FC_U8 && dims_.channels == 1 &&
                       groups_.front().kind != LaunchGroup::Chain;
   for (const auto& g : groups_)
@@ -366,9 +367,10 @@ void Executor::run_host(const void* video, int in_type, void* out) {
   const int n_chunks = (F + chunk - 1) / chunk;
 
   // device staging: 2 video chunks, 2 output chunks, 2 state sets
-  std::size_t vbytes = std::size_t(chunk) * in_frame;
-  std::size_t obytes = std::size_t(chunk) * out_frame;
-  std::size_t sbytes = std::size_t(std::max(n_iir_, 1)) * hw * sizeof(float);
+  auto align = [](std::size_t b) { return (b + 255) & ~std::size_t(255); };
+  std::size_t vbytes = align(std::size_t(chunk) * in_frame);
+  std::size_t obytes = align(std::size_t(chunk) * out_frame);
+  std::size_t sbytes = align(std::size_t(std::max(n_iir_, 1)) * hw * sizeof(float));
   char* mem = nullptr;
   cuda_check(cudaMalloc(&mem, 2 * (vbytes + obytes + sbytes)), "cudaMalloc(stream)");
   char* vb[2] = {mem, mem + vbytes};

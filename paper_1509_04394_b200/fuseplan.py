@@ -245,6 +245,17 @@ def _torch():
     return torch
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+
+def _stream_handle(stream) -> int:
+    """cudaStream_t of a torch stream.  torch's default stream has handle 0,
+    which the C ABI reads as "the executor's own stream"; map it to the legacy
+    default stream so work stays ordered with torch's."""
+    h = int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream or 0)
+    return h if h != 0 else CUDA_STREAM_LEGACY
+
+
 class Executor(_Handle):
     """fp_exec: runs a plan's partitions as sm_100a kernels on one GPU."""
     _free = "fp_exec_free"
@@ -294,8 +305,8 @@ class Executor(_Handle):
                 out = torch.empty((F, H, W), device=video.device,
                                   dtype=torch.uint8 if self.out_elem == FP_ELEM_U8
                                   else torch.float32)
-            if stream is None:
-                stream = torch.cuda.current_stream(video.device).cuda_stream
+            stream = _stream_handle(torch.cuda.current_stream(video.device)
+                                    if stream is None else stream)
             _check(lib().fp_exec_run(self.ptr, video.data_ptr(), self._elem(video.dtype),
                                      out.data_ptr(), FP_EXEC_DEVICE_PTRS, stream))
             return out
@@ -319,8 +330,8 @@ class Executor(_Handle):
             out = torch.empty((n - n_warm, H, W), device=video.device,
                               dtype=torch.uint8 if self.out_elem == FP_ELEM_U8
                               else torch.float32)
-        if stream is None:
-            stream = torch.cuda.current_stream(video.device).cuda_stream
+        stream = _stream_handle(torch.cuda.current_stream(video.device)
+                                if stream is None else stream)
         _check(lib().fp_exec_run_range(
             self.ptr, video.data_ptr(), self._elem(video.dtype), out.data_ptr(), n,
             n_warm, None if state_in is None else state_in.data_ptr(),
@@ -332,8 +343,8 @@ def synth_hash_u8(out, t0: int = 0, seed: int = 1234, stream=None):
     """Fill a CUDA uint8 tensor [F, C, H, W] with the counter-hash test video."""
     torch = _torch()
     F, C, H, W = out.shape
-    if stream is None:
-        stream = torch.cuda.current_stream(out.device).cuda_stream
+    stream = _stream_handle(torch.cuda.current_stream(out.device)
+                            if stream is None else stream)
     _check(lib().fp_synth_hash_u8(out.data_ptr(), W, H, F, C, t0, seed, stream))
     return out
 
