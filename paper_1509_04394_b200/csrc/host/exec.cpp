@@ -196,7 +196,8 @@ std::string Executor::describe() const {
   std::ostringstream ss;
   ss << "{\"device\": " << device_ << ", \"variant\": " << int(opt_.variant)
      << ", \"output\": \"" << (out_type_ == FC_U8 ? "u8" : "f32")
-     << "\", \"launches_per_run\": " << launches_per_run() << ", \"groups\": [";
+     << "\", \"launches_per_run\": " << launches_per_run()
+     << ", \"exact_rechecks_total\": " << fc_last_recheck_count() << ", \"groups\": [";
   for (std::size_t i = 0; i < groups_.size(); ++i) {
     const auto& g = groups_[i];
     ss << (i ? ", " : "") << "{\"first\": " << g.first << ", \"last\": " << g.last

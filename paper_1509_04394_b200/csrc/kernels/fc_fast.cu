@@ -1,12 +1,739 @@
-// Certified FP32 fast path for the all-fused chain (placeholder until the
-// register-column kernel lands): reports "not covered" so dispatch falls
-// back to the exact kernel.
+// F12345 fast path: the whole SPEC chain in one streaming sm_100a kernel with
+// a CERTIFIED FP32 stencil path and an exact FP64 recheck, so the u8 mask is
+// bit-identical to the reference (simulator.cpp:48-108) while the hot loop
+// runs at packed-FP32 rate.
+//
+// Work decomposition
+//   * one CTA (1024 threads) per spatial tile of TW x th output pixels (TW a
+//     compile-time width, th chosen at launch); the CTA marches over all
+//     frames carrying the exact IIR state of its haloed tile in registers --
+//     the recurrence is never split (SURVEY finding 5);
+//   * the host picks (TW, th) so every tile is resident and SM work balanced;
+//   * frames are processed in PAIRS (t, t+1): every stencil value is a float2
+//     (frame t, frame t+1), so each spatial op is one f32x2 instruction
+//     (FFMA2 / FADD2 / FMUL2) with no lane shuffling;
+//   * input: a TMA ring of NS frames; one 3-D tensor copy per frame brings the
+//     R, G, B planes of the haloed box (alpha never leaves HBM).  Out-of-video
+//     cells arrive zero-filled and are never read: every stage reads its input
+//     at clamped coordinates (simulator.cpp:202-210).
+//
+// Per frame pair (4 CTA barriers):
+//   A  S1+S2 exact.  gray = fl(fl(fl(wr R)+fl(wg G))+fl(wb B)) with each
+//      product from one FFMA on a byte->float magic number (exact rounding of
+//      w*c), alpha = 0.5 folded into the weights (a power-of-two scale
+//      commutes with rounding for these normal values), and the IIR
+//      fl(fl(a x) + fl(b y)) evaluated as FMA(0.5, y, a x): identical, because
+//      a x is either 0 or >= 0.057 and 0.5 y is exact unless y is subnormal, in
+//      which case both forms round to a x.  P2 <- (y_t, y_t+1).
+//   B  horizontal 5-tap FP32 gaussian pass (separable taps)        -> H2
+//   C  vertical 5-tap FP32 pass -> approximate S3                  -> G2
+//   D  Sobel, m = gx^2 + gy^2; the mask bit is sqrtf(m) >= th <=> m >= M*
+//      (M* = min{m : sqrtf(m) >= th}, found on the host).  Pixels with
+//      |m - M*| inside the certified error band (certify_band) are recomputed
+//      EXACTLY from the exact IIR plane: FP64 gaussian in the reference's tap
+//      order, reference Sobel, IEEE sqrt.  Everything else is decided by m.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
 #include "fc_kernels.h"
 
-extern "C" int fc_chain_fast(const fc_stage*, const fc_stage*, const fc_stage*,
-                             const fc_stage*, const void*, int, int, void*, int,
-                             fc_dims, int, const float*, float*, void*) {
-  return -1;
+namespace fcfast {
+
+constexpr int NT = 256;   // threads per CTA
+constexpr int MAXB = 2;   // CTAs per SM (2 x 256 threads x 128 registers)
+constexpr int NS = 4;     // TMA frame slots (even: a pair never straddles a wrap)
+constexpr int KA = 4;     // max 4-cell IIR groups per thread
+
+struct Args {
+  uint8_t* out;
+  int W, H, n_frames, n_warm;
+  int th, tiles_x;
+  int RH, BWB;                // haloed region rows, TMA box row bytes
+  unsigned slot_bytes;        // TMA bytes per frame: 3 * RH * BWB
+  unsigned slot_stride;       // slot_bytes rounded up to 128
+  unsigned off_p2, off_h2, off_g2, off_bar, off_taps, off_queue;
+  const float* state_in;
+  float* state_out;
+  float wr, wg, wb, wrm, wgm, wbm;  // gray weights (x alpha when folded), -w*2^23
+  float alpha, beta;
+  int alpha_half;
+  float h0, h1, h2;                 // separable fast taps: |d|=2, |d|=1, centre
+  float taps[25];                   // reference taps for the exact recheck
+  float mstar, band, th_val;
+};
+
+__device__ unsigned long long g_rechecks;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-extern "C" long long fc_last_recheck_count(void) { return 0; }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// x (innermost, bytes) must be a multiple of 16 (measured on B200: other
+// offsets raise an illegal-instruction fault; scripts/tma_probe.cu).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// float(byte k of w) + 2^23 in one PRMT: bytes {w.k, 0, 0, 0x4B}
+template <int K>
+__device__ __forceinline__ float magic(uint32_t w) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(0x4B000000u), "n"(0x7440 + K));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 splat(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
+
+// fl(w * c), c in [0,255] held as c + 2^23: FMA(w, c + 2^23, -w 2^23)
+// rounds the exact product w*c once (w 2^23 is exact).
+__device__ __forceinline__ float2 wprod(float2 m, float w, float wm) {
+  return __ffma2_rn(splat(w), m, splat(wm));
+}
+
+__device__ __forceinline__ float2 tap5(float2 a, float2 b, float2 c, float2 d, float2 e,
+                                       float h0, float h1, float h2) {
+  float2 acc = __fmul2_rn(splat(h0), __fadd2_rn(a, e));
+  acc = __ffma2_rn(splat(h1), __fadd2_rn(b, d), acc);
+  return __ffma2_rn(splat(h2), c, acc);
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
+
+// Exact reference threshold decision at (x, y), frame component f, from the
+// exact IIR plane (simulator.cpp:63-89): FP64 gaussian in dy/dx order at the
+// 3x3 clamped centres, Sobel in the reference's float order, IEEE sqrt.
+// P2 region cell (c, r) <-> global (bx + c, by + r), stored at r*PW + c + 1.
+__device__ __noinline__ bool exact_white(const Args& a, const float2* P2, const double* taps,
+                                         int PW, int bx, int by, int x, int y, int f) {
+  float g[3][3];
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < 3; ++i) {
+      int cx = clampi(x + i - 1, 0, a.W - 1), cy = clampi(y + j - 1, 0, a.H - 1);
+      double acc = 0.0;
+      for (int dy = -2; dy <= 2; ++dy) {
+        int ry = clampi(cy + dy, 0, a.H - 1) - by;
+        for (int dx = -2; dx <= 2; ++dx) {
+          int rx = clampi(cx + dx, 0, a.W - 1) - bx;
+          float2 v = P2[ry * PW + rx + 1];
+          acc = __fma_rn(taps[(dy + 2) * 5 + dx + 2], double(f ? v.y : v.x), acc);
+        }
+      }
+      g[j][i] = __double2float_rn(acc);
+    }
+  auto s = [&](int dx, int dy) { return g[dy + 1][dx + 1]; };
+  float gx = __fsub_rn(__fadd_rn(__fadd_rn(s(1, -1), __fmul_rn(2.0f, s(1, 0))), s(1, 1)),
+                       __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(-1, 0))), s(-1, 1)));
+  float gy = __fsub_rn(__fadd_rn(__fadd_rn(s(-1, 1), __fmul_rn(2.0f, s(0, 1))), s(1, 1)),
+                       __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(0, -1))), s(1, -1)));
+  return __fsqrt_rn(__fadd_rn(__fmul_rn(gx, gx), __fmul_rn(gy, gy))) >= a.th_val;
+}
+
+// Fast Sobel for output pixels (x, x+1) of tile row i from G2 (cols 2q..2q+3
+// hold x-1 .. x+2, rows i..i+2 hold y-1..y+1): dm[k] = m - M* for pixel
+// x + k, both frames.  gx = v(x+1) - v(x-1) with v the [1 2 1] column sum,
+// gy = d(x-1) + 2 d(x) + d(x+1) with d = g(y+1) - g(y-1).
+template <int HP>
+__device__ __forceinline__ void sobel_dm(const float2* G2, int i, int q, float mstar,
+                                         float2 (&dm)[2]) {
+  float2 v[4], dd[4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float4 t0 = *reinterpret_cast<const float4*>(G2 + i * HP + 2 * q + 2 * h);
+    float4 t1 = *reinterpret_cast<const float4*>(G2 + (i + 1) * HP + 2 * q + 2 * h);
+    float4 t2 = *reinterpret_cast<const float4*>(G2 + (i + 2) * HP + 2 * q + 2 * h);
+    v[2 * h] = __fadd2_rn(__ffma2_rn(splat(2.0f), lo2(t1), lo2(t0)), lo2(t2));
+    v[2 * h + 1] = __fadd2_rn(__ffma2_rn(splat(2.0f), hi2(t1), hi2(t0)), hi2(t2));
+    dd[2 * h] = __ffma2_rn(splat(-1.0f), lo2(t0), lo2(t2));
+    dd[2 * h + 1] = __ffma2_rn(splat(-1.0f), hi2(t0), hi2(t2));
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    float2 gx = __ffma2_rn(splat(-1.0f), v[k], v[k + 2]);
+    float2 gy = __fadd2_rn(__ffma2_rn(splat(2.0f), dd[k + 1], dd[k]), dd[k + 2]);
+    float2 m = __ffma2_rn(gx, gx, __fmul2_rn(gy, gy));
+    dm[k] = __fadd2_rn(m, splat(-mstar));
+  }
+}
+
+constexpr int QCAP = 2048;  // queued uncertain pixels per frame pair
+
+template <int TW>
+struct Geom {
+  static constexpr int RW = TW + 8;       // region cells per row: x0-4 .. x0+TW+3
+  static constexpr int GPR = RW / 4;      // 4-cell groups per region row
+  static constexpr int PW = RW + 4;       // P2 pitch (float2), col c at c + 1
+  static constexpr int HC = TW + 2;       // H2 / G2 columns: x0-1 .. x0+TW
+  static constexpr int HP = TW + 4;       // H2 / G2 pitch (float2)
+  static constexpr int BPAIRS = HC / 2;   // phase-B items per row
+  static constexpr int DQ = TW / 2;       // phase-D items per row (2 px each)
+};
+
+template <int TW>
+__global__ void __launch_bounds__(NT, MAXB)
+    k_chain_fast(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
+  using G = Geom<TW>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* rgb = smem;
+  float2* P2 = reinterpret_cast<float2*>(smem + a.off_p2);
+  float2* H2 = reinterpret_cast<float2*>(smem + a.off_h2);
+  float2* G2 = reinterpret_cast<float2*>(smem + a.off_g2);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.off_bar);
+  double* taps = reinterpret_cast<double*>(smem + a.off_taps);
+  unsigned* queue = reinterpret_cast<unsigned*>(smem + a.off_queue);
+  unsigned* qcount = queue + QCAP;
+
+  const int tid = threadIdx.x;
+  const int tile_x = blockIdx.x % a.tiles_x, tile_y = blockIdx.x / a.tiles_x;
+  const int x0 = tile_x * TW, y0 = tile_y * a.th;
+  const int W = a.W, H = a.H, n = a.n_frames, th = a.th, RH = a.RH;
+  // region cell (0,0) = global (x0-4, y0-3); TMA box starts at the 16-byte
+  // aligned column tx0 <= bx
+  const int bx = x0 - 4, by = y0 - 3;
+  const int tx0 = bx >= 0 ? (bx & ~15) : -((-bx + 15) & ~15);
+  const int xoff = bx - tx0;
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+    *qcount = 0;
+  }
+  if (tid < 25) taps[tid] = double(a.taps[tid]);
+  __syncthreads();
+  if (tid == 0)
+    for (int t = 0; t < NS && t < n; ++t) {
+      mbar_expect_tx(&bar[t], a.slot_bytes);
+      tma_load_3d(rgb + t * a.slot_stride, &tmap, &bar[t], tx0, by, 4 * t);
+    }
+
+  // ---- loop-invariant ownership of IIR cells: groups of 4 region cells
+  const int n_groups = G::GPR * RH;
+  int g_src[KA], g_dst[KA];  // RGB byte offset in a slot plane; P2 float2 index
+  bool g_border[KA];
+  // The IIR state of a cell is the .y (frame t+1) component of its P2 entry:
+  // phase A reads it back from shared memory instead of pinning 4*KA
+  // registers for the whole march.
+  const bool fresh = a.state_in == nullptr;
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {
+    int g = tid + k * NT;
+    int r = g / G::GPR, c = (g - r * G::GPR) * 4;
+    int gy = clampi(by + r, 0, H - 1);
+    g_src[k] = (gy - by) * a.BWB + xoff + c;
+    g_dst[k] = r * G::PW + c + 1;
+    g_border[k] = (bx + c < 0) || (bx + c + 3 > W - 1);
+    if (g < n_groups && !fresh) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int gx = clampi(bx + c + i, 0, W - 1);
+        P2[g_dst[k] + i] = make_float2(0.0f, a.state_in[(long long)gy * W + gx]);
+      }
+    }
+  }
+  const bool border_x = (x0 - 1 < 0) || (x0 + TW > W - 1);
+  const bool border_y = (y0 - 1 < 0) || (y0 + th > H - 1);
+  const long long hw = (long long)W * H;
+  const int plane = RH * a.BWB;
+  const float h0 = a.h0, h1 = a.h1, h2 = a.h2;
+
+  for (int t = 0; t < n; t += 2) {
+    const bool has1 = t + 1 < n;
+    const int s0 = t % NS, s1 = (t + 1) % NS;
+    mbar_wait(&bar[s0], (t / NS) & 1);
+    if (has1) mbar_wait(&bar[s1], ((t + 1) / NS) & 1);
+    const unsigned char* f0 = rgb + s0 * a.slot_stride;
+    const unsigned char* f1 = rgb + s1 * a.slot_stride;
+
+    // ---------------- A: gray + IIR (exact) -> P2
+    // one group at a time (descriptors recomputed: GPR is a compile-time
+    // constant, so this is a few integer ops and keeps register use low)
+#pragma unroll 1
+    for (int g = tid; g < n_groups; g += NT) {
+      const int r = g / G::GPR, cbase = (g - r * G::GPR) * 4;
+      const int src = (clampi(by + r, 0, H - 1) - by) * a.BWB + xoff + cbase;
+      const int dst = r * G::PW + cbase + 1;
+      uint32_t w0[3], w1[3];
+      if (bx + cbase >= 0 && bx + cbase + 3 <= W - 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          w0[c] = *reinterpret_cast<const uint32_t*>(f0 + c * plane + src);
+          w1[c] = *reinterpret_cast<const uint32_t*>(f1 + c * plane + src);
+        }
+      } else {  // clamped per-cell gathers at the left / right video border
+        int rowb = src - xoff - cbase;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          uint32_t v0 = 0, v1 = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            int col = clampi(bx + cbase + i, 0, W - 1) - bx + xoff;
+            v0 |= uint32_t(f0[c * plane + rowb + col]) << (8 * i);
+            v1 |= uint32_t(f1[c * plane + rowb + col]) << (8 * i);
+          }
+          w0[c] = v0;
+          w1[c] = v1;
+        }
+      }
+      float2* d = P2 + dst;  // dst odd: d + 1 is 16-byte aligned
+      float st[4];
+      {
+        float2 q0 = d[0], q3 = d[3];
+        float4 q12 = *reinterpret_cast<const float4*>(d + 1);
+        st[0] = q0.y;
+        st[1] = q12.y;
+        st[2] = q12.w;
+        st[3] = q3.y;
+      }
+      float2 y2[4];
+#define FC_CELL(I)                                                                   \
+  {                                                                                    \
+    float2 pr = wprod(f2(magic<I>(w0[0]), magic<I>(w1[0])), a.wr, a.wrm);              \
+    float2 pg = wprod(f2(magic<I>(w0[1]), magic<I>(w1[1])), a.wg, a.wgm);              \
+    float2 pb = wprod(f2(magic<I>(w0[2]), magic<I>(w1[2])), a.wb, a.wbm);              \
+    float2 gq = __fadd2_rn(__fadd2_rn(pr, pg), pb);                                    \
+    float ya, yb;                                                                      \
+    if (a.alpha_half) {                                                                \
+      ya = (fresh && t == 0) ? __fadd_rn(gq.x, gq.x) : __fmaf_rn(0.5f, st[I], gq.x);    \
+      yb = has1 ? __fmaf_rn(0.5f, ya, gq.y) : ya;                                      \
+    } else {                                                                           \
+      ya = (fresh && t == 0)                                                           \
+               ? gq.x                                                                  \
+               : __fadd_rn(__fmul_rn(a.alpha, gq.x), __fmul_rn(a.beta, st[I]));        \
+      yb = has1 ? __fadd_rn(__fmul_rn(a.alpha, gq.y), __fmul_rn(a.beta, ya)) : ya;     \
+    }                                                                                  \
+    y2[I] = f2(ya, yb);                                                                \
+  }
+      FC_CELL(0) FC_CELL(1) FC_CELL(2) FC_CELL(3)
+#undef FC_CELL
+      d[0] = y2[0];
+      *reinterpret_cast<float4*>(d + 1) = make_float4(y2[1].x, y2[1].y, y2[2].x, y2[2].y);
+      d[3] = y2[3];
+    }
+    __syncthreads();  // P2 complete; RGB slots of t, t+1 consumed
+
+    if (tid == 0) {  // refill the two slots with frames t+NS, t+NS+1
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int q = 0; q < 2; ++q) {
+        int tf = t + q + NS;
+        if (tf < n) {
+          int s = tf % NS;
+          mbar_expect_tx(&bar[s], a.slot_bytes);
+          tma_load_3d(rgb + s * a.slot_stride, &tmap, &bar[s], tx0, by, 4 * tf);
+        }
+      }
+    }
+    const bool out0 = t >= a.n_warm, out1 = has1 && t + 1 >= a.n_warm;
+    if (!out0 && !out1) continue;  // warm-up pair: state only
+
+    // ---------------- B: horizontal pass, H2[r][j] centred at x0-1+j (clamped)
+    if (!border_x) {
+      // centre region col = j + 3, window cols j+1..j+6 -> P2 float2 j+2..j+7
+      for (int it = tid; it < RH * G::BPAIRS; it += NT) {
+        int r = it / G::BPAIRS, j0 = (it - r * G::BPAIRS) * 2;
+        const float4* p = reinterpret_cast<const float4*>(P2 + r * G::PW + j0 + 2);
+        float4 u0 = p[0], u1 = p[1], u2 = p[2];
+        float2 o0 = tap5(lo2(u0), hi2(u0), lo2(u1), hi2(u1), lo2(u2), h0, h1, h2);
+        float2 o1 = tap5(hi2(u0), lo2(u1), hi2(u1), lo2(u2), hi2(u2), h0, h1, h2);
+        *reinterpret_cast<float4*>(H2 + r * G::HP + j0) = make_float4(o0.x, o0.y, o1.x, o1.y);
+      }
+    } else {
+      for (int it = tid; it < RH * G::BPAIRS; it += NT) {
+        int r = it / G::BPAIRS, j0 = (it - r * G::BPAIRS) * 2;
+        int c0 = clampi(x0 - 1 + j0, 0, W - 1) - bx;
+        int c1 = clampi(x0 + j0, 0, W - 1) - bx;
+        const float2* p = P2 + r * G::PW + c0 - 1;
+        float2 o0 = tap5(p[0], p[1], p[2], p[3], p[4], h0, h1, h2);
+        float2 o1 = o0;
+        if (c1 != c0) o1 = tap5(p[1], p[2], p[3], p[4], p[5], h0, h1, h2);
+        *reinterpret_cast<float4*>(H2 + r * G::HP + j0) = make_float4(o0.x, o0.y, o1.x, o1.y);
+      }
+    }
+    __syncthreads();
+    // ---------------- C: vertical pass, G2[i][j] centred at y0-1+i (clamped)
+    {
+      const int ipairs = (th + 3) >> 1;
+      for (int it = tid; it < ipairs * G::HC; it += NT) {
+        int ip = it / G::HC, j = it - ip * G::HC;
+        int i0 = ip * 2;
+        int r0 = border_y ? clampi(y0 - 1 + i0, 0, H - 1) - by : i0 + 2;
+        const float2* p = H2 + (r0 - 2) * G::HP + j;
+        float2 v0 = p[0], v1 = p[G::HP], v2 = p[2 * G::HP], v3 = p[3 * G::HP],
+               v4 = p[4 * G::HP];
+        float2 o0 = tap5(v0, v1, v2, v3, v4, h0, h1, h2);
+        G2[i0 * G::HP + j] = o0;
+        if (i0 + 1 < th + 2) {
+          int r1 = border_y ? clampi(y0 + i0, 0, H - 1) - by : r0 + 1;
+          float2 o1 = o0;
+          if (r1 != r0) o1 = tap5(v1, v2, v3, v4, p[5 * G::HP], h0, h1, h2);
+          G2[(i0 + 1) * G::HP + j] = o1;
+        }
+      }
+    }
+    __syncthreads();
+    // ---------------- D: Sobel + certified threshold, 2 pixels x 2 frames.
+    // Uncertain pixels are queued and resolved exactly in phase E, so the
+    // FP64 recheck code never holds registers in this loop.
+    unsigned char* o0p = a.out + (long long)(t - a.n_warm) * hw;
+    for (int it = tid; it < th * G::DQ; it += NT) {
+      int i = it / G::DQ, q = it - i * G::DQ;
+      int x = x0 + 2 * q, y = y0 + i;
+      if (x >= W || y >= H) continue;
+      float2 dm[2];
+      sobel_dm<G::HP>(G2, i, q, a.mstar, dm);
+      uint32_t b0 = (dm[0].x >= 0.0f ? 0xFFu : 0u) | (dm[1].x >= 0.0f ? 0xFF00u : 0u);
+      uint32_t b1 = (dm[0].y >= 0.0f ? 0xFFu : 0u) | (dm[1].y >= 0.0f ? 0xFF00u : 0u);
+      long long o = (long long)y * W + x;
+      if (out0) *reinterpret_cast<uint16_t*>(o0p + o) = uint16_t(b0);
+      if (out1) *reinterpret_cast<uint16_t*>(o0p + hw + o) = uint16_t(b1);
+      // branch-free uncertainty mask; the (rare) queue push is one branch
+      const float band = a.band;
+      unsigned amb = (fabsf(dm[0].x) <= band ? 1u : 0u) | (fabsf(dm[1].x) <= band ? 2u : 0u) |
+                     (has1 && fabsf(dm[0].y) <= band ? 4u : 0u) |
+                     (has1 && fabsf(dm[1].y) <= band ? 8u : 0u);
+      if (amb) {
+        unsigned pos = atomicAdd(qcount, unsigned(__popc(amb)));
+        for (int k = 0; k < 4; ++k)
+          if (amb & (1u << k)) {
+            if (pos < QCAP)
+              queue[pos] = (unsigned(k >> 1) << 31) | (unsigned(i) << 16) |
+                           unsigned(2 * q + (k & 1));
+            ++pos;
+          }
+      }
+    }
+    __syncthreads();
+    // ---------------- E: exact recheck of the queued pixels (rare)
+    const unsigned n_amb = *qcount;
+    if (n_amb) {
+      for (unsigned e = tid; e < min(n_amb, unsigned(QCAP)); e += NT) {
+        unsigned code = queue[e];
+        int f = int(code >> 31), i = int((code >> 16) & 0x7FFF), xl = int(code & 0xFFFF);
+        int x = x0 + xl, y = y0 + i;
+        bool wv = exact_white(a, P2, taps, G::PW, bx, by, x, y, f);
+        if (f ? out1 : out0)
+          o0p[(f ? hw : 0) + (long long)y * W + x] = wv ? 0xFF : 0x00;
+      }
+      if (n_amb > unsigned(QCAP)) {  // queue overflow: sweep the tile again
+        for (int it = tid; it < th * G::DQ; it += NT) {
+          int i = it / G::DQ, q = it - i * G::DQ;
+          int x = x0 + 2 * q, y = y0 + i;
+          if (x >= W || y >= H) continue;
+          float2 dm[2];
+          sobel_dm<G::HP>(G2, i, q, a.mstar, dm);
+          for (int k = 0; k < 4; ++k) {
+            float v = (k & 2) ? dm[k & 1].y : dm[k & 1].x;
+            int f = k >> 1;
+            if (!(fabsf(v) <= a.band) || (f == 1 && !has1) || !(f ? out1 : out0)) continue;
+            bool wv = exact_white(a, P2, taps, G::PW, bx, by, x + (k & 1), y, f);
+            o0p[(f ? hw : 0) + (long long)y * W + x + (k & 1)] = wv ? 0xFF : 0x00;
+          }
+        }
+      }
+      if (tid == 0) atomicAdd(&g_rechecks, (unsigned long long)n_amb);
+    }
+    __syncthreads();  // E (reads P2, queue) done before the next A
+    if (tid == 0) *qcount = 0;
+  }
+
+  if (a.state_out) {
+#pragma unroll
+    for (int k = 0; k < KA; ++k) {
+      int g = tid + k * NT;
+      if (g >= n_groups) break;
+      int r = g / G::GPR, c = (g - r * G::GPR) * 4;
+      int gy = by + r;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int gx = bx + c + i;
+        bool own = gx >= x0 && gx < x0 + TW && gy >= y0 && gy < y0 + th && gx < W && gy < H;
+        if (own) a.state_out[(long long)gy * W + gx] = P2[g_dst[k] + i].y;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host
+
+constexpr int kWidths[] = {32, 48, 64, 80, 96, 128, 160};
+
+struct TilePlan {
+  int tw = 0, th = 0, tiles_x = 0, tiles_y = 0;
+  size_t smem = 0;
+};
+
+// Dynamic shared-memory layout; fills the offsets of `a` when given.
+size_t layout(int tw, int th, Args* a) {
+  const int RW = tw + 8, RH = th + 6, PW = RW + 4, HP = tw + 4;
+  const int BWB = (RW + 12 + 15) / 16 * 16;  // + worst-case alignment slack
+  size_t slot = size_t(3) * RH * BWB, stride = (slot + 127) / 128 * 128;
+  size_t off = NS * stride;
+  size_t off_p2 = off;
+  off += size_t(RH) * PW * 8;
+  size_t off_h2 = (off + 15) / 16 * 16;
+  off = off_h2 + size_t(RH) * HP * 8;
+  size_t off_g2 = (off + 15) / 16 * 16;
+  off = off_g2 + size_t(th + 3) * HP * 8;
+  size_t off_bar = (off + 7) / 8 * 8;
+  off = off_bar + NS * 8;
+  size_t off_taps = (off + 7) / 8 * 8;
+  off = off_taps + 25 * 8;
+  size_t off_queue = (off + 15) / 16 * 16;
+  off = off_queue + (QCAP + 4) * 4;
+  if (a) {
+    a->off_queue = unsigned(off_queue);
+    a->RH = RH;
+    a->BWB = BWB;
+    a->slot_bytes = unsigned(slot);
+    a->slot_stride = unsigned(stride);
+    a->off_p2 = unsigned(off_p2);
+    a->off_h2 = unsigned(off_h2);
+    a->off_g2 = unsigned(off_g2);
+    a->off_bar = unsigned(off_bar);
+    a->off_taps = unsigned(off_taps);
+  }
+  return off;
+}
+
+// Every tile runs every frame, so a tile's cost is its per-frame work; the
+// kernel time is (waves) x (largest tile work).  Work model in lane-ops per
+// frame: ~8 per IIR cell, ~3 per H2 / G2 value, ~10 per output pixel.
+// An SM runs ceil(tiles / SMs) tiles over the whole march; two co-resident
+// CTAs hide each other's barrier waits, so single-CTA tilings pay a penalty.
+// FUSEPLAN_FAST_TILE="tw,th" overrides the choice (tuning).
+bool choose_tiles(int W, int H, int sms, size_t smem_cap, TilePlan* best) {
+  const size_t smem_per_sm = 233472;  // 228 KB per SM, 1 KB reserved per CTA
+  double best_cost = 1e300;
+  int force_tw = 0, force_th = 0;
+  if (const char* env = std::getenv("FUSEPLAN_FAST_TILE"))
+    std::sscanf(env, "%d,%d", &force_tw, &force_th);
+  for (int tw : kWidths) {
+    if (force_tw && tw != force_tw) continue;
+    int tx = (W + tw - 1) / tw;
+    for (int th = 2; th + 6 <= 256; ++th) {  // TMA box rows <= 256
+      if (force_th && th != force_th) continue;
+      int ty = (H + th - 1) / th;
+      if (!force_th && ty > 1 && (ty - 1) * th >= H) continue;
+      size_t sm = layout(tw, th, nullptr);
+      if (sm > smem_cap) break;
+      int per_sm = int(std::min<size_t>(MAXB, smem_per_sm / (sm + 1024)));
+      long long tiles = (long long)tx * ty;
+      long long load = (tiles + sms - 1) / sms;
+      double work = 8.0 * (tw + 8) * (th + 6) + 3.0 * (tw + 2) * (th + 6) +
+                    3.0 * (tw + 2) * (th + 2) + 10.0 * tw * th;
+      double cost = double(load) * work * (per_sm >= 2 ? 1.0 : 1.3);
+      if (cost < best_cost) {
+        best_cost = cost;
+        *best = TilePlan{tw, th, tx, ty, sm};
+      }
+    }
+  }
+  return best_cost < 1e300;
+}
+
+// Certified error band on m = gx^2 + gy^2 (u = 2^-24, all stencil inputs >= 0):
+//   kappa : relative error of the FP32 separable gaussian vs the reference's
+//           FP64-accumulated, float-rounded value: <= 8.1u (two passes of at
+//           most 4 roundings per term) + dw (separable vs reference taps) + u
+//           (the reference's final rounding) + 25 * 2^-53 (its double sums);
+//   E     : |gx_f - gx_ref| <= (kappa + 6.1u) * S, S = sum of the six taps'
+//           |values| <= 8 gmax (3 roundings on each side);
+//   Em(m) <= 4 E sqrt(m) + 2 E^2 + 4.1 u m   (|g.| <= sqrt(m), 2 roundings
+//           in each of m_f and m_ref);
+//   B solves B >= Em(M* + B); m_f >= M* + B certifies white, m_f < M* - B
+//   black.  The returned band is 2B (margin).
+float certify_band(float mstar, double gmax, double dw) {
+  const double u = std::ldexp(1.0, -24);
+  double kappa = 8.1 * u + dw + u + 25.0 * std::ldexp(1.0, -53);
+  double E = (kappa + 6.1 * u) * 8.0 * gmax;
+  double B = 1.0;
+  for (int it = 0; it < 60; ++it)
+    B = 4.0 * E * std::sqrt(double(mstar) + B) + 2.0 * E * E + 4.1 * u * (double(mstar) + B);
+  return float(2.0 * B + 1e-3);
+}
+
+template <int TW>
+int launch(const CUtensorMap& map, const Args& a, int grid, size_t smem, cudaStream_t st) {
+  static size_t configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_chain_fast<TW>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return int(e);
+    configured = smem;
+  }
+  k_chain_fast<TW><<<grid, NT, smem, st>>>(map, a);
+  return int(cudaGetLastError());
+}
+
+}  // namespace fcfast
+
+using namespace fcfast;
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+struct PlanCache {
+  int W = -1, H = -1, dev = -1;
+  TilePlan tp;
+};
+
+}  // namespace
+
+extern "C" int fc_chain_fast(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                             const fc_stage* sthr, const void* video, int in_type,
+                             int gray_in, void* out, int out_type, fc_dims d, int n_warm,
+                             const float* state_in, float* state_out, void* stream) {
+  // Coverage of the certified path: u8 RGBA video, {0,255} u8 mask, gaussian
+  // r = 2 with separable taps, threshold > 0, width a multiple of 16 (TMA
+  // strides), 16-byte aligned base.  Anything else -> the exact kernel.
+  if (in_type != FC_U8 || out_type != FC_U8 || gray_in || sgray == nullptr) return -1;
+  if (sg->g_radius != 2 || !(sthr->th > 0.0f)) return -1;
+  if (sthr->white != 255.0f || sthr->black != 0.0f) return -1;
+  if (d.width % 16 != 0 || d.height < 1) return -1;
+  if (reinterpret_cast<uintptr_t>(video) % 16 != 0) return -1;
+  if (d.frames == 0) return 0;
+  auto enc = encode_fn();
+  if (!enc) return -1;
+
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static thread_local PlanCache cache;
+  if (cache.W != d.width || cache.H != d.height || cache.dev != dev) {
+    int sms = 0, smem_optin = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (!choose_tiles(d.width, d.height, sms, size_t(smem_optin), &cache.tp)) return -1;
+    cache.W = d.width;
+    cache.H = d.height;
+    cache.dev = dev;
+  }
+  const TilePlan& tp = cache.tp;
+
+  Args a;
+  std::memset(&a, 0, sizeof a);
+  layout(tp.tw, tp.th, &a);
+  a.out = static_cast<uint8_t*>(out);
+  a.W = d.width;
+  a.H = d.height;
+  a.n_frames = d.frames;
+  a.n_warm = n_warm;
+  a.th = tp.th;
+  a.tiles_x = tp.tiles_x;
+  a.state_in = state_in;
+  a.state_out = state_out;
+  a.alpha = si->alpha;
+  a.beta = 1.0f - si->alpha;
+  a.alpha_half = si->alpha == 0.5f;
+  const float fold = a.alpha_half ? 0.5f : 1.0f;  // exact power-of-two scale
+  a.wr = sgray->wr * fold;
+  a.wg = sgray->wg * fold;
+  a.wb = sgray->wb * fold;
+  a.wrm = -a.wr * 8388608.0f;
+  a.wgm = -a.wg * 8388608.0f;
+  a.wbm = -a.wb * 8388608.0f;
+  // Separable fast taps from the centre row of the reference taps: in exact
+  // arithmetic w[2][k] / sum_k w[2][k] is the normalised 1-D gaussian.
+  double e[5], row = 0.0, es = 0.0;
+  for (int k = 0; k < 5; ++k) row += double(sg->g_w[10 + k]);
+  for (int k = 0; k < 5; ++k) es += (e[k] = double(sg->g_w[10 + k]) / row);
+  a.h0 = float(e[0] / es);
+  a.h1 = float(e[1] / es);
+  a.h2 = float(e[2] / es);
+  const float hh[5] = {a.h0, a.h1, a.h2, a.h1, a.h0};
+  double dw = 0.0;  // worst relative mismatch of h_i h_j vs the reference taps
+  for (int j = 0; j < 5; ++j)
+    for (int i = 0; i < 5; ++i) {
+      double ref = sg->g_w[j * 5 + i];
+      dw = std::max(dw, std::fabs(double(hh[j]) * hh[i] - ref) / ref);
+    }
+  if (!(dw < 1e-5)) return -1;  // not separable enough to certify
+  std::memcpy(a.taps, sg->g_w, sizeof a.taps);
+  a.th_val = sthr->th;
+  // M* = min float m with sqrtf(m) >= th
+  float m = sthr->th * sthr->th;
+  while (m > 0.0f && std::sqrt(std::nextafter(m, 0.0f)) >= sthr->th) m = std::nextafter(m, 0.0f);
+  while (std::sqrt(m) < sthr->th) m = std::nextafter(m, INFINITY);
+  a.mstar = m;
+  double gray_max = 255.0 * (double(sgray->wr) + double(sgray->wg) + double(sgray->wb));
+  double tap_sum = 0.0;
+  for (int k = 0; k < 25; ++k) tap_sum += sg->g_w[k];
+  a.band = certify_band(a.mstar, gray_max * tap_sum * 1.001, dw);
+
+  CUtensorMap map;
+  cuuint64_t dims[3] = {cuuint64_t(d.width), cuuint64_t(d.height), cuuint64_t(4) * d.frames};
+  cuuint64_t strides[2] = {cuuint64_t(d.width), cuuint64_t(d.width) * d.height};
+  cuuint32_t box[3] = {cuuint32_t(a.BWB), cuuint32_t(a.RH), 3};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(video), dims, strides,
+          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
+  const int grid = tp.tiles_x * tp.tiles_y;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (tp.tw) {
+    case 32: return launch<32>(map, a, grid, tp.smem, st);
+    case 48: return launch<48>(map, a, grid, tp.smem, st);
+    case 64: return launch<64>(map, a, grid, tp.smem, st);
+    case 80: return launch<80>(map, a, grid, tp.smem, st);
+    case 96: return launch<96>(map, a, grid, tp.smem, st);
+    case 128: return launch<128>(map, a, grid, tp.smem, st);
+    case 160: return launch<160>(map, a, grid, tp.smem, st);
+    default: return -1;
+  }
+}
+
+extern "C" long long fc_last_recheck_count(void) {
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_rechecks, sizeof v) != cudaSuccess) return -1;
+  return (long long)v;
+}

@@ -104,6 +104,45 @@ def test_larger_hash_video_dense_mask(fp, cuda, oracle):
             np.testing.assert_array_equal(out, want, err_msg=f"{part} {variant}")
 
 
+@pytest.mark.parametrize("shape,th", [((64, 48, 20), 128.0), ((160, 120, 24), 24.0),
+                                      ((192, 96, 17), 40.0), ((48, 37, 9), 24.0),
+                                      ((800, 64, 6), 24.0), ((16, 8, 5), 12.0)])
+def test_fast_certified_path_exact(fp, cuda, oracle, shape, th):
+    """The certified FP32 kernel (variant='fast' fails loudly if it does not
+    apply) is bit-exact, including pixels that took the FP64 recheck."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    W, H, F = shape
+    pipe = spec_chain(W, H, F, th=th)
+    v = hash_video_u8(F, 4, H, W, 4242)
+    want = oracle.orc_chain(pipe, v)
+    out, ex = run(fp, pipe, v, {"force_partition": "1-5"}, variant="fast", torch_dev=cuda)
+    np.testing.assert_array_equal(out, want)
+    assert ex.describe()["exact_rechecks_total"] >= 0
+
+
+def test_fast_path_rechecks_happen_and_are_exact(fp, cuda, oracle):
+    """A threshold placed in the bulk of the gradient distribution forces many
+    pixels into the uncertain band; all of them must resolve exactly."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    W, H, F = 128, 64, 12
+    v = hash_video_u8(F, 4, H, W, 99)
+    pipe = spec_chain(W, H, F, th=20.0)
+    grads = oracle.orc_run_sequential(dict(pipe, kernels=pipe["kernels"][:4]), v)[-1]
+    th = float(np.float32(np.median(grads)))
+    pipe = spec_chain(W, H, F, th=th)
+    want = oracle.orc_chain(pipe, v)
+    p = fp.Pipeline(json.dumps(pipe))
+    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": "1-5"}),
+                     variant="fast")
+    before = ex.describe()["exact_rechecks_total"]
+    import torch
+    out = ex.run(torch.from_numpy(v).to(cuda))
+    torch.cuda.synchronize()
+    after = ex.describe()["exact_rechecks_total"]
+    assert after > before
+    np.testing.assert_array_equal(out.cpu().numpy().astype(np.float32), want)
+
+
 def test_state_carry_and_warm_restart(fp, cuda, oracle):
     """run_range: resuming from the carried state is exact; a warm-up restart
     equals the oracle's restart semantics at the same frame."""
