@@ -4,11 +4,13 @@
 // runs at packed-FP32 rate.
 //
 // Work decomposition
-//   * one CTA (1024 threads) per spatial tile of TW x th output pixels (TW a
-//     compile-time width, th chosen at launch); the CTA marches over all
-//     frames carrying the exact IIR state of its haloed tile in registers --
-//     the recurrence is never split (SURVEY finding 5);
-//   * the host picks (TW, th) so every tile is resident and SM work balanced;
+//   * one CTA (NT threads, MAXB CTAs per SM) per spatial tile of TW x th
+//     output pixels (TW compile-time, th chosen at launch); the CTA marches
+//     over all frames carrying the exact IIR state of its haloed tile -- the
+//     recurrence is never split (SURVEY finding 5);
+//   * CTAs whose haloed tile lies inside the video run a specialised body with
+//     no clamping and no bounds checks (BORDER = false); border tiles run the
+//     general body;
 //   * frames are processed in PAIRS (t, t+1): every stencil value is a float2
 //     (frame t, frame t+1), so each spatial op is one f32x2 instruction
 //     (FFMA2 / FADD2 / FMUL2) with no lane shuffling;
@@ -24,14 +26,15 @@
 //      commutes with rounding for these normal values), and the IIR
 //      fl(fl(a x) + fl(b y)) evaluated as FMA(0.5, y, a x): identical, because
 //      a x is either 0 or >= 0.057 and 0.5 y is exact unless y is subnormal, in
-//      which case both forms round to a x.  P2 <- (y_t, y_t+1).
+//      which case both forms round to a x.  P2 <- (y_t, y_t+1); the .y half is
+//      also the carried state.
 //   B  horizontal 5-tap FP32 gaussian pass (separable taps)        -> H2
 //   C  vertical 5-tap FP32 pass -> approximate S3                  -> G2
 //   D  Sobel, m = gx^2 + gy^2; the mask bit is sqrtf(m) >= th <=> m >= M*
 //      (M* = min{m : sqrtf(m) >= th}, found on the host).  Pixels with
-//      |m - M*| inside the certified error band (certify_band) are recomputed
-//      EXACTLY from the exact IIR plane: FP64 gaussian in the reference's tap
-//      order, reference Sobel, IEEE sqrt.  Everything else is decided by m.
+//      |m - M*| inside the certified error band (certify_band) are queued
+//   E  and recomputed EXACTLY from the exact IIR plane: FP64 gaussian in the
+//      reference's tap order, reference Sobel, IEEE sqrt.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -42,6 +45,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "fc_kernels.h"
 
@@ -50,7 +54,7 @@ namespace fcfast {
 constexpr int NT = 256;   // threads per CTA
 constexpr int MAXB = 2;   // CTAs per SM (2 x 256 threads x 128 registers)
 constexpr int NS = 4;     // TMA frame slots (even: a pair never straddles a wrap)
-constexpr int KA = 4;     // max 4-cell IIR groups per thread
+constexpr int QCAP = 2048;  // queued uncertain pixels per frame pair
 
 struct Args {
   uint8_t* out;
@@ -62,13 +66,20 @@ struct Args {
   unsigned off_p2, off_h2, off_g2, off_bar, off_taps, off_queue;
   const float* state_in;
   float* state_out;
-  float wr, wg, wb, wrm, wgm, wbm;  // gray weights (x alpha when folded), -w*2^23
-  float alpha, beta;
-  int alpha_half;
+  float wr, wg, wb, wrm, wgm, wbm;  // gray weights x 0.5 (alpha folded), -w*2^23
   float h0, h1, h2;                 // separable fast taps: |d|=2, |d|=1, centre
   float taps[25];                   // reference taps for the exact recheck
   float mstar, band, th_val;
+  long long* dbg;  // optional per-CTA phase clocks (FUSEPLAN_FAST_PROFILE)
 };
+
+// Phase timing (diagnostic): thread 0 accumulates clock64 deltas per phase.
+#define FC_MARK(k)                               \
+  if (prof) {                                    \
+    long long now_ = clock64();                  \
+    tacc[k] += now_ - tlast;                     \
+    tlast = now_;                                \
+  }
 
 __device__ unsigned long long g_rechecks;
 
@@ -137,6 +148,15 @@ __device__ __forceinline__ float2 tap5(float2 a, float2 b, float2 c, float2 d, f
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
 
+// 0xFF where dm >= 0 (white), else 0, for four values -> one word.  dm is
+// never -0 for m < M* (Sterbenz: the difference of nearby floats is exact),
+// so the sign bit is the decision.
+__device__ __forceinline__ uint32_t pack_white(float a, float b, float c, float d) {
+  uint32_t sa = uint32_t(__float_as_int(a) >> 31), sb = uint32_t(__float_as_int(b) >> 31);
+  uint32_t sc = uint32_t(__float_as_int(c) >> 31), sd = uint32_t(__float_as_int(d) >> 31);
+  return ~__byte_perm(__byte_perm(sa, sb, 0x0040), __byte_perm(sc, sd, 0x0040), 0x5410);
+}
+
 // Exact reference threshold decision at (x, y), frame component f, from the
 // exact IIR plane (simulator.cpp:63-89): FP64 gaussian in dy/dx order at the
 // 3x3 clamped centres, Sobel in the reference's float order, IEEE sqrt.
@@ -166,34 +186,32 @@ __device__ __noinline__ bool exact_white(const Args& a, const float2* P2, const 
   return __fsqrt_rn(__fadd_rn(__fmul_rn(gx, gx), __fmul_rn(gy, gy))) >= a.th_val;
 }
 
-// Fast Sobel for output pixels (x, x+1) of tile row i from G2 (cols 2q..2q+3
-// hold x-1 .. x+2, rows i..i+2 hold y-1..y+1): dm[k] = m - M* for pixel
-// x + k, both frames.  gx = v(x+1) - v(x-1) with v the [1 2 1] column sum,
-// gy = d(x-1) + 2 d(x) + d(x+1) with d = g(y+1) - g(y-1).
-template <int HP>
-__device__ __forceinline__ void sobel_dm(const float2* G2, int i, int q, float mstar,
-                                         float2 (&dm)[2]) {
-  float2 v[4], dd[4];
+// Fast Sobel terms for output pixels x .. x+K-1 of tile row i from G2
+// (cols c0 .. c0+K+1 hold x-1 .. x+K, rows i..i+2 hold y-1..y+1):
+// dm[k] = m - M*, both frames.  gx = v(x+1) - v(x-1) with v the [1 2 1]
+// column sum, gy = d(x-1) + 2 d(x) + d(x+1) with d = g(y+1) - g(y-1).
+template <int K>
+__device__ __forceinline__ void sobel_dm(const float2* r0, const float2* r1, const float2* r2,
+                                         float mstar, float2 (&dm)[K]) {
+  float2 v[K + 2], dd[K + 2];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    float4 t0 = *reinterpret_cast<const float4*>(G2 + i * HP + 2 * q + 2 * h);
-    float4 t1 = *reinterpret_cast<const float4*>(G2 + (i + 1) * HP + 2 * q + 2 * h);
-    float4 t2 = *reinterpret_cast<const float4*>(G2 + (i + 2) * HP + 2 * q + 2 * h);
+  for (int h = 0; h < (K + 2) / 2; ++h) {
+    float4 t0 = reinterpret_cast<const float4*>(r0)[h];
+    float4 t1 = reinterpret_cast<const float4*>(r1)[h];
+    float4 t2 = reinterpret_cast<const float4*>(r2)[h];
     v[2 * h] = __fadd2_rn(__ffma2_rn(splat(2.0f), lo2(t1), lo2(t0)), lo2(t2));
     v[2 * h + 1] = __fadd2_rn(__ffma2_rn(splat(2.0f), hi2(t1), hi2(t0)), hi2(t2));
     dd[2 * h] = __ffma2_rn(splat(-1.0f), lo2(t0), lo2(t2));
     dd[2 * h + 1] = __ffma2_rn(splat(-1.0f), hi2(t0), hi2(t2));
   }
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < K; ++k) {
     float2 gx = __ffma2_rn(splat(-1.0f), v[k], v[k + 2]);
     float2 gy = __fadd2_rn(__ffma2_rn(splat(2.0f), dd[k + 1], dd[k]), dd[k + 2]);
     float2 m = __ffma2_rn(gx, gx, __fmul2_rn(gy, gy));
     dm[k] = __fadd2_rn(m, splat(-mstar));
   }
 }
-
-constexpr int QCAP = 2048;  // queued uncertain pixels per frame pair
 
 template <int TW>
 struct Geom {
@@ -202,292 +220,328 @@ struct Geom {
   static constexpr int PW = RW + 4;       // P2 pitch (float2), col c at c + 1
   static constexpr int HC = TW + 2;       // H2 / G2 columns: x0-1 .. x0+TW
   static constexpr int HP = TW + 4;       // H2 / G2 pitch (float2)
-  static constexpr int BPAIRS = HC / 2;   // phase-B items per row
-  static constexpr int DQ = TW / 2;       // phase-D items per row (2 px each)
 };
 
-template <int TW>
-__global__ void __launch_bounds__(NT, MAXB)
-    k_chain_fast(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
-  using G = Geom<TW>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* rgb = smem;
-  float2* P2 = reinterpret_cast<float2*>(smem + a.off_p2);
-  float2* H2 = reinterpret_cast<float2*>(smem + a.off_h2);
-  float2* G2 = reinterpret_cast<float2*>(smem + a.off_g2);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.off_bar);
-  double* taps = reinterpret_cast<double*>(smem + a.off_taps);
-  unsigned* queue = reinterpret_cast<unsigned*>(smem + a.off_queue);
-  unsigned* qcount = queue + QCAP;
+struct Smem {
+  unsigned char* rgb;
+  float2 *P2, *H2, *G2;
+  uint64_t* bar;
+  double* taps;
+  unsigned *queue, *qcount;
+};
 
+// The frame march of one CTA.  BORDER = false: the haloed region lies inside
+// the video (no clamping anywhere, (th + 2) % 4 == 0, full tile).
+template <int TW, bool BORDER>
+__device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, const Smem& s,
+                                      int x0, int y0) {
+  // BORDER tiles (the haloed tile crosses a video edge) run the same body as
+  // interior tiles plus three cheap remaps that realise the per-stage
+  // clamp-to-edge rule (simulator.cpp:202-210):
+  //   A  out-of-video rows read the clamped RGB row; an out-of-video 4-cell
+  //      group (groups never straddle the edge: W % 4 == 0) replicates the
+  //      edge byte with one PRMT -> the IIR plane holds clamped values;
+  //   C  an out-of-video G2 column is computed from the edge H2 column;
+  //   D  out-of-video G2 rows are read as the edge row.
+  // The horizontal pass needs no remap: H rows are row-local and the columns
+  // it produces outside the video are replaced in C.
+  using G = Geom<TW>;
   const int tid = threadIdx.x;
-  const int tile_x = blockIdx.x % a.tiles_x, tile_y = blockIdx.x / a.tiles_x;
-  const int x0 = tile_x * TW, y0 = tile_y * a.th;
   const int W = a.W, H = a.H, n = a.n_frames, th = a.th, RH = a.RH;
-  // region cell (0,0) = global (x0-4, y0-3); TMA box starts at the 16-byte
-  // aligned column tx0 <= bx
   const int bx = x0 - 4, by = y0 - 3;
   const int tx0 = bx >= 0 ? (bx & ~15) : -((-bx + 15) & ~15);
   const int xoff = bx - tx0;
-
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
-    *qcount = 0;
-  }
-  if (tid < 25) taps[tid] = double(a.taps[tid]);
-  __syncthreads();
-  if (tid == 0)
-    for (int t = 0; t < NS && t < n; ++t) {
-      mbar_expect_tx(&bar[t], a.slot_bytes);
-      tma_load_3d(rgb + t * a.slot_stride, &tmap, &bar[t], tx0, by, 4 * t);
-    }
-
-  // ---- loop-invariant ownership of IIR cells: groups of 4 region cells
   const int n_groups = G::GPR * RH;
-  int g_src[KA], g_dst[KA];  // RGB byte offset in a slot plane; P2 float2 index
-  bool g_border[KA];
-  // The IIR state of a cell is the .y (frame t+1) component of its P2 entry:
-  // phase A reads it back from shared memory instead of pinning 4*KA
-  // registers for the whole march.
   const bool fresh = a.state_in == nullptr;
-#pragma unroll
-  for (int k = 0; k < KA; ++k) {
-    int g = tid + k * NT;
-    int r = g / G::GPR, c = (g - r * G::GPR) * 4;
-    int gy = clampi(by + r, 0, H - 1);
-    g_src[k] = (gy - by) * a.BWB + xoff + c;
-    g_dst[k] = r * G::PW + c + 1;
-    g_border[k] = (bx + c < 0) || (bx + c + 3 > W - 1);
-    if (g < n_groups && !fresh) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        int gx = clampi(bx + c + i, 0, W - 1);
-        P2[g_dst[k] + i] = make_float2(0.0f, a.state_in[(long long)gy * W + gx]);
-      }
-    }
-  }
-  const bool border_x = (x0 - 1 < 0) || (x0 + TW > W - 1);
-  const bool border_y = (y0 - 1 < 0) || (y0 + th > H - 1);
   const long long hw = (long long)W * H;
   const int plane = RH * a.BWB;
   const float h0 = a.h0, h1 = a.h1, h2 = a.h2;
+  float2* const P2 = s.P2;
+  float2* const H2 = s.H2;
+  float2* const G2 = s.G2;
 
+  // the carried IIR state is the .y half of P2
+  if (!fresh)
+    for (int g = tid; g < n_groups; g += NT) {
+      int r = g / G::GPR, c = (g - r * G::GPR) * 4;
+      int gy = clampi(by + r, 0, H - 1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        P2[r * G::PW + c + 1 + i] =
+            make_float2(0.0f, a.state_in[(long long)gy * W + clampi(bx + c + i, 0, W - 1)]);
+    }
+
+  const bool prof = a.dbg != nullptr && tid == 0;
+  long long tacc[6] = {0, 0, 0, 0, 0, 0}, tlast = prof ? clock64() : 0;
+  int slot = 0;          // ring slot of frame t
+  unsigned parity = 0;   // mbarrier phase of that slot
   for (int t = 0; t < n; t += 2) {
     const bool has1 = t + 1 < n;
-    const int s0 = t % NS, s1 = (t + 1) % NS;
-    mbar_wait(&bar[s0], (t / NS) & 1);
-    if (has1) mbar_wait(&bar[s1], ((t + 1) / NS) & 1);
-    const unsigned char* f0 = rgb + s0 * a.slot_stride;
-    const unsigned char* f1 = rgb + s1 * a.slot_stride;
+    const int s0 = slot, s1 = slot + 1;
+    mbar_wait(&s.bar[s0], parity);
+    if (has1) mbar_wait(&s.bar[s1], parity);
+    FC_MARK(0)
+    const unsigned char* f0 = s.rgb + s0 * a.slot_stride;
+    const unsigned char* f1 = s.rgb + s1 * a.slot_stride;
+    const bool steady = has1 && !(fresh && t == 0);
 
     // ---------------- A: gray + IIR (exact) -> P2
-    // one group at a time (descriptors recomputed: GPR is a compile-time
-    // constant, so this is a few integer ops and keeps register use low)
-#pragma unroll 1
-    for (int g = tid; g < n_groups; g += NT) {
-      const int r = g / G::GPR, cbase = (g - r * G::GPR) * 4;
-      const int src = (clampi(by + r, 0, H - 1) - by) * a.BWB + xoff + cbase;
-      const int dst = r * G::PW + cbase + 1;
-      uint32_t w0[3], w1[3];
-      if (bx + cbase >= 0 && bx + cbase + 3 <= W - 1) {
+    {
+      constexpr int DR = NT / G::GPR, DC = (NT % G::GPR) * 4;
+      int c4 = (tid % G::GPR) * 4, r = tid / G::GPR;
+      int dst = r * G::PW + c4 + 1;
+#pragma unroll 2
+      for (int g = tid; g < n_groups; g += NT) {
+        const int rowsrc = (BORDER ? clampi(by + r, 0, H - 1) - by : r) * a.BWB;
+        uint32_t w0[3], w1[3];
+        const int x = bx + c4;
+        if (!BORDER || (x >= 0 && x + 3 <= W - 1)) {
+          const unsigned char* p0 = f0 + rowsrc + xoff + c4;
+          const unsigned char* p1 = f1 + rowsrc + xoff + c4;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          w0[c] = *reinterpret_cast<const uint32_t*>(f0 + c * plane + src);
-          w1[c] = *reinterpret_cast<const uint32_t*>(f1 + c * plane + src);
-        }
-      } else {  // clamped per-cell gathers at the left / right video border
-        int rowb = src - xoff - cbase;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          uint32_t v0 = 0, v1 = 0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            int col = clampi(bx + cbase + i, 0, W - 1) - bx + xoff;
-            v0 |= uint32_t(f0[c * plane + rowb + col]) << (8 * i);
-            v1 |= uint32_t(f1[c * plane + rowb + col]) << (8 * i);
+          for (int c = 0; c < 3; ++c) {
+            w0[c] = *reinterpret_cast<const uint32_t*>(p0 + c * plane);
+            w1[c] = *reinterpret_cast<const uint32_t*>(p1 + c * plane);
           }
-          w0[c] = v0;
-          w1[c] = v1;
+        } else {  // whole group outside the video: replicate the edge byte
+          const int edge = x < 0 ? 0 : W - 1;
+          const int wcol = (edge & ~3) - bx + xoff;
+          const unsigned sel = unsigned(edge & 3) * 0x1111u;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            w0[c] = __byte_perm(*reinterpret_cast<const uint32_t*>(f0 + c * plane + rowsrc + wcol), 0, sel);
+            w1[c] = __byte_perm(*reinterpret_cast<const uint32_t*>(f1 + c * plane + rowsrc + wcol), 0, sel);
+          }
         }
-      }
-      float2* d = P2 + dst;  // dst odd: d + 1 is 16-byte aligned
-      float st[4];
-      {
+        float2* d = P2 + dst;  // dst odd: d + 1 is 16-byte aligned
         float2 q0 = d[0], q3 = d[3];
         float4 q12 = *reinterpret_cast<const float4*>(d + 1);
-        st[0] = q0.y;
-        st[1] = q12.y;
-        st[2] = q12.w;
-        st[3] = q3.y;
-      }
-      float2 y2[4];
-#define FC_CELL(I)                                                                   \
-  {                                                                                    \
-    float2 pr = wprod(f2(magic<I>(w0[0]), magic<I>(w1[0])), a.wr, a.wrm);              \
-    float2 pg = wprod(f2(magic<I>(w0[1]), magic<I>(w1[1])), a.wg, a.wgm);              \
-    float2 pb = wprod(f2(magic<I>(w0[2]), magic<I>(w1[2])), a.wb, a.wbm);              \
-    float2 gq = __fadd2_rn(__fadd2_rn(pr, pg), pb);                                    \
-    float ya, yb;                                                                      \
-    if (a.alpha_half) {                                                                \
-      ya = (fresh && t == 0) ? __fadd_rn(gq.x, gq.x) : __fmaf_rn(0.5f, st[I], gq.x);    \
-      yb = has1 ? __fmaf_rn(0.5f, ya, gq.y) : ya;                                      \
-    } else {                                                                           \
-      ya = (fresh && t == 0)                                                           \
-               ? gq.x                                                                  \
-               : __fadd_rn(__fmul_rn(a.alpha, gq.x), __fmul_rn(a.beta, st[I]));        \
-      yb = has1 ? __fadd_rn(__fmul_rn(a.alpha, gq.y), __fmul_rn(a.beta, ya)) : ya;     \
-    }                                                                                  \
-    y2[I] = f2(ya, yb);                                                                \
+        const float st[4] = {q0.y, q12.y, q12.w, q3.y};
+        float2 y2[4];
+#define FC_CELL(I)                                                                    \
+  {                                                                                   \
+    float2 pr = wprod(f2(magic<I>(w0[0]), magic<I>(w1[0])), a.wr, a.wrm);             \
+    float2 pg = wprod(f2(magic<I>(w0[1]), magic<I>(w1[1])), a.wg, a.wgm);             \
+    float2 pb = wprod(f2(magic<I>(w0[2]), magic<I>(w1[2])), a.wb, a.wbm);             \
+    float2 gq = __fadd2_rn(__fadd2_rn(pr, pg), pb); /* = 0.5 * gray, exactly */      \
+    float ya, yb;                                                                     \
+    if (steady) {                                                                     \
+      ya = __fmaf_rn(0.5f, st[I], gq.x);                                              \
+      yb = __fmaf_rn(0.5f, ya, gq.y);                                                 \
+    } else {                                                                          \
+      ya = (fresh && t == 0) ? __fadd_rn(gq.x, gq.x) : __fmaf_rn(0.5f, st[I], gq.x);  \
+      yb = has1 ? __fmaf_rn(0.5f, ya, gq.y) : ya;                                     \
+    }                                                                                 \
+    y2[I] = f2(ya, yb);                                                               \
   }
-      FC_CELL(0) FC_CELL(1) FC_CELL(2) FC_CELL(3)
+        FC_CELL(0) FC_CELL(1) FC_CELL(2) FC_CELL(3)
 #undef FC_CELL
-      d[0] = y2[0];
-      *reinterpret_cast<float4*>(d + 1) = make_float4(y2[1].x, y2[1].y, y2[2].x, y2[2].y);
-      d[3] = y2[3];
+        d[0] = y2[0];
+        *reinterpret_cast<float4*>(d + 1) = make_float4(y2[1].x, y2[1].y, y2[2].x, y2[2].y);
+        d[3] = y2[3];
+        c4 += DC;
+        r += DR;
+        dst += DR * G::PW + DC;
+        if (c4 >= G::RW) {
+          c4 -= G::RW;
+          ++r;
+          dst += G::PW - G::RW;
+        }
+      }
     }
     __syncthreads();  // P2 complete; RGB slots of t, t+1 consumed
+    FC_MARK(1)
 
     if (tid == 0) {  // refill the two slots with frames t+NS, t+NS+1
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       for (int q = 0; q < 2; ++q) {
         int tf = t + q + NS;
         if (tf < n) {
-          int s = tf % NS;
-          mbar_expect_tx(&bar[s], a.slot_bytes);
-          tma_load_3d(rgb + s * a.slot_stride, &tmap, &bar[s], tx0, by, 4 * tf);
+          mbar_expect_tx(&s.bar[slot + q], a.slot_bytes);
+          tma_load_3d(s.rgb + (slot + q) * a.slot_stride, &tmap, &s.bar[slot + q], tx0, by, 4 * tf);
         }
       }
+    }
+    slot += 2;
+    if (slot == NS) {
+      slot = 0;
+      parity ^= 1u;
     }
     const bool out0 = t >= a.n_warm, out1 = has1 && t + 1 >= a.n_warm;
     if (!out0 && !out1) continue;  // warm-up pair: state only
 
-    // ---------------- B: horizontal pass, H2[r][j] centred at x0-1+j (clamped)
-    if (!border_x) {
-      // centre region col = j + 3, window cols j+1..j+6 -> P2 float2 j+2..j+7
-      for (int it = tid; it < RH * G::BPAIRS; it += NT) {
-        int r = it / G::BPAIRS, j0 = (it - r * G::BPAIRS) * 2;
+    // ---------------- B: horizontal pass, 4 outputs per item: H2[r][j] for
+    // centre region col j + 3, window P2 float2 j0+2 .. j0+9
+    {
+      constexpr int IPR = (TW + 4) / 4;
+      for (int it = tid; it < RH * IPR; it += NT) {
+        int r = it / IPR, j0 = (it - r * IPR) * 4;
         const float4* p = reinterpret_cast<const float4*>(P2 + r * G::PW + j0 + 2);
-        float4 u0 = p[0], u1 = p[1], u2 = p[2];
-        float2 o0 = tap5(lo2(u0), hi2(u0), lo2(u1), hi2(u1), lo2(u2), h0, h1, h2);
-        float2 o1 = tap5(hi2(u0), lo2(u1), hi2(u1), lo2(u2), hi2(u2), h0, h1, h2);
-        *reinterpret_cast<float4*>(H2 + r * G::HP + j0) = make_float4(o0.x, o0.y, o1.x, o1.y);
-      }
-    } else {
-      for (int it = tid; it < RH * G::BPAIRS; it += NT) {
-        int r = it / G::BPAIRS, j0 = (it - r * G::BPAIRS) * 2;
-        int c0 = clampi(x0 - 1 + j0, 0, W - 1) - bx;
-        int c1 = clampi(x0 + j0, 0, W - 1) - bx;
-        const float2* p = P2 + r * G::PW + c0 - 1;
-        float2 o0 = tap5(p[0], p[1], p[2], p[3], p[4], h0, h1, h2);
-        float2 o1 = o0;
-        if (c1 != c0) o1 = tap5(p[1], p[2], p[3], p[4], p[5], h0, h1, h2);
-        *reinterpret_cast<float4*>(H2 + r * G::HP + j0) = make_float4(o0.x, o0.y, o1.x, o1.y);
+        float4 u0 = p[0], u1 = p[1], u2 = p[2], u3 = p[3];
+        float2 v[8] = {lo2(u0), hi2(u0), lo2(u1), hi2(u1), lo2(u2), hi2(u2), lo2(u3), hi2(u3)};
+        float2 o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[k] = tap5(v[k], v[k + 1], v[k + 2], v[k + 3], v[k + 4], h0, h1, h2);
+        float4* q = reinterpret_cast<float4*>(H2 + r * G::HP + j0);
+        q[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+        q[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
       }
     }
     __syncthreads();
-    // ---------------- C: vertical pass, G2[i][j] centred at y0-1+i (clamped)
+    FC_MARK(2)
+    // ---------------- C: vertical pass, 4 G rows per item from H2 rows
+    // i0 .. i0+7 ((th + 2) % 4 == 0 by construction)
     {
-      const int ipairs = (th + 3) >> 1;
-      for (int it = tid; it < ipairs * G::HC; it += NT) {
-        int ip = it / G::HC, j = it - ip * G::HC;
-        int i0 = ip * 2;
-        int r0 = border_y ? clampi(y0 - 1 + i0, 0, H - 1) - by : i0 + 2;
-        const float2* p = H2 + (r0 - 2) * G::HP + j;
-        float2 v0 = p[0], v1 = p[G::HP], v2 = p[2 * G::HP], v3 = p[3 * G::HP],
-               v4 = p[4 * G::HP];
-        float2 o0 = tap5(v0, v1, v2, v3, v4, h0, h1, h2);
-        G2[i0 * G::HP + j] = o0;
-        if (i0 + 1 < th + 2) {
-          int r1 = border_y ? clampi(y0 + i0, 0, H - 1) - by : r0 + 1;
-          float2 o1 = o0;
-          if (r1 != r0) o1 = tap5(v1, v2, v3, v4, p[5 * G::HP], h0, h1, h2);
-          G2[(i0 + 1) * G::HP + j] = o1;
+      const int iq = (th + 2) >> 2;
+      for (int it = tid; it < iq * G::HC; it += NT) {
+        int m = it / G::HC, j = it - m * G::HC;
+        int i0 = 4 * m;
+        const int jc = BORDER ? clampi(x0 - 1 + j, 0, W - 1) - (x0 - 1) : j;
+        const float2* p = H2 + i0 * G::HP + jc;
+        float2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = p[k * G::HP];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          G2[(i0 + k) * G::HP + j] = tap5(v[k], v[k + 1], v[k + 2], v[k + 3], v[k + 4], h0, h1, h2);
+      }
+    }
+    __syncthreads();
+    FC_MARK(3)
+    // ---------------- D: Sobel + certified threshold, 4 pixels x 2 frames
+    unsigned char* o0p = a.out + (long long)(t - a.n_warm) * hw;
+    const float band = a.band, mstar = a.mstar;
+    {
+      constexpr int Q = TW / 4;
+      for (int it = tid; it < th * Q; it += NT) {
+        const int i = it / Q, q = it - i * Q;
+        const int x = x0 + 4 * q, y = y0 + i;
+        if (BORDER && (x >= W || y >= H)) continue;  // partial tile
+        int k0 = i, k1 = i + 1, k2 = i + 2;  // G2 rows of y-1, y, y+1
+        if (BORDER) {
+          k0 = clampi(y - 1, 0, H - 1) - (y0 - 1);
+          k2 = clampi(y + 1, 0, H - 1) - (y0 - 1);
+        }
+        float2 dm[4];
+        sobel_dm<4>(G2 + k0 * G::HP + 4 * q, G2 + k1 * G::HP + 4 * q, G2 + k2 * G::HP + 4 * q,
+                    mstar, dm);
+        if (!has1) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) dm[k].y = INFINITY;
+        }
+        const long long o = (long long)y * W + x;
+        if (out0) *reinterpret_cast<uint32_t*>(o0p + o) = pack_white(dm[0].x, dm[1].x, dm[2].x, dm[3].x);
+        if (out1) *reinterpret_cast<uint32_t*>(o0p + hw + o) = pack_white(dm[0].y, dm[1].y, dm[2].y, dm[3].y);
+        float amin = fminf(fminf(fminf(fabsf(dm[0].x), fabsf(dm[1].x)), fminf(fabsf(dm[2].x), fabsf(dm[3].x))),
+                           fminf(fminf(fabsf(dm[0].y), fabsf(dm[1].y)), fminf(fabsf(dm[2].y), fabsf(dm[3].y))));
+        if (amin <= band) {
+          unsigned amb = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            amb |= (fabsf(dm[k].x) <= band ? 1u : 0u) << k;
+            amb |= (fabsf(dm[k].y) <= band ? 1u : 0u) << (4 + k);
+          }
+          unsigned pos = atomicAdd(s.qcount, unsigned(__popc(amb)));
+          for (int k = 0; k < 8; ++k)
+            if (amb & (1u << k)) {
+              if (pos < QCAP)
+                s.queue[pos] = (unsigned(k >> 2) << 31) | (unsigned(i) << 16) | unsigned(4 * q + (k & 3));
+              ++pos;
+            }
         }
       }
     }
     __syncthreads();
-    // ---------------- D: Sobel + certified threshold, 2 pixels x 2 frames.
-    // Uncertain pixels are queued and resolved exactly in phase E, so the
-    // FP64 recheck code never holds registers in this loop.
-    unsigned char* o0p = a.out + (long long)(t - a.n_warm) * hw;
-    for (int it = tid; it < th * G::DQ; it += NT) {
-      int i = it / G::DQ, q = it - i * G::DQ;
-      int x = x0 + 2 * q, y = y0 + i;
-      if (x >= W || y >= H) continue;
-      float2 dm[2];
-      sobel_dm<G::HP>(G2, i, q, a.mstar, dm);
-      uint32_t b0 = (dm[0].x >= 0.0f ? 0xFFu : 0u) | (dm[1].x >= 0.0f ? 0xFF00u : 0u);
-      uint32_t b1 = (dm[0].y >= 0.0f ? 0xFFu : 0u) | (dm[1].y >= 0.0f ? 0xFF00u : 0u);
-      long long o = (long long)y * W + x;
-      if (out0) *reinterpret_cast<uint16_t*>(o0p + o) = uint16_t(b0);
-      if (out1) *reinterpret_cast<uint16_t*>(o0p + hw + o) = uint16_t(b1);
-      // branch-free uncertainty mask; the (rare) queue push is one branch
-      const float band = a.band;
-      unsigned amb = (fabsf(dm[0].x) <= band ? 1u : 0u) | (fabsf(dm[1].x) <= band ? 2u : 0u) |
-                     (has1 && fabsf(dm[0].y) <= band ? 4u : 0u) |
-                     (has1 && fabsf(dm[1].y) <= band ? 8u : 0u);
-      if (amb) {
-        unsigned pos = atomicAdd(qcount, unsigned(__popc(amb)));
-        for (int k = 0; k < 4; ++k)
-          if (amb & (1u << k)) {
-            if (pos < QCAP)
-              queue[pos] = (unsigned(k >> 1) << 31) | (unsigned(i) << 16) |
-                           unsigned(2 * q + (k & 1));
-            ++pos;
-          }
-      }
-    }
-    __syncthreads();
+    FC_MARK(4)
     // ---------------- E: exact recheck of the queued pixels (rare)
-    const unsigned n_amb = *qcount;
+    const unsigned n_amb = *s.qcount;
     if (n_amb) {
       for (unsigned e = tid; e < min(n_amb, unsigned(QCAP)); e += NT) {
-        unsigned code = queue[e];
+        unsigned code = s.queue[e];
         int f = int(code >> 31), i = int((code >> 16) & 0x7FFF), xl = int(code & 0xFFFF);
         int x = x0 + xl, y = y0 + i;
-        bool wv = exact_white(a, P2, taps, G::PW, bx, by, x, y, f);
-        if (f ? out1 : out0)
-          o0p[(f ? hw : 0) + (long long)y * W + x] = wv ? 0xFF : 0x00;
+        bool wv = exact_white(a, P2, s.taps, G::PW, bx, by, x, y, f);
+        if (f ? out1 : out0) o0p[(f ? hw : 0) + (long long)y * W + x] = wv ? 0xFF : 0x00;
       }
-      if (n_amb > unsigned(QCAP)) {  // queue overflow: sweep the tile again
-        for (int it = tid; it < th * G::DQ; it += NT) {
-          int i = it / G::DQ, q = it - i * G::DQ;
-          int x = x0 + 2 * q, y = y0 + i;
+      if (n_amb > unsigned(QCAP)) {  // queue overflow: recheck every uncertain pixel
+        constexpr int Q = TW / 4;
+        for (int it = tid; it < th * Q; it += NT) {
+          const int i = it / Q, q = it - i * Q;
+          const int x = x0 + 4 * q, y = y0 + i;
           if (x >= W || y >= H) continue;
-          float2 dm[2];
-          sobel_dm<G::HP>(G2, i, q, a.mstar, dm);
-          for (int k = 0; k < 4; ++k) {
-            float v = (k & 2) ? dm[k & 1].y : dm[k & 1].x;
-            int f = k >> 1;
-            if (!(fabsf(v) <= a.band) || (f == 1 && !has1) || !(f ? out1 : out0)) continue;
-            bool wv = exact_white(a, P2, taps, G::PW, bx, by, x + (k & 1), y, f);
-            o0p[(f ? hw : 0) + (long long)y * W + x + (k & 1)] = wv ? 0xFF : 0x00;
+          int k0 = clampi(y - 1, 0, H - 1) - (y0 - 1), k2 = clampi(y + 1, 0, H - 1) - (y0 - 1);
+          float2 dm[4];
+          sobel_dm<4>(G2 + k0 * G::HP + 4 * q, G2 + (i + 1) * G::HP + 4 * q,
+                      G2 + k2 * G::HP + 4 * q, mstar, dm);
+          for (int k = 0; k < 8; ++k) {
+            const int f = k >> 2, px = k & 3;
+            const float v = f ? dm[px].y : dm[px].x;
+            if (!(fabsf(v) <= band) || (f == 1 && !has1) || !(f ? out1 : out0)) continue;
+            bool wv = exact_white(a, P2, s.taps, G::PW, bx, by, x + px, y, f);
+            o0p[(f ? hw : 0) + (long long)y * W + x + px] = wv ? 0xFF : 0x00;
           }
         }
       }
       if (tid == 0) atomicAdd(&g_rechecks, (unsigned long long)n_amb);
     }
     __syncthreads();  // E (reads P2, queue) done before the next A
-    if (tid == 0) *qcount = 0;
+    if (tid == 0) *s.qcount = 0;
+    FC_MARK(5)
   }
+  if (prof)
+    for (int k = 0; k < 6; ++k) a.dbg[blockIdx.x * 8 + k] = tacc[k];
 
-  if (a.state_out) {
-#pragma unroll
-    for (int k = 0; k < KA; ++k) {
-      int g = tid + k * NT;
-      if (g >= n_groups) break;
+  if (a.state_out)
+    for (int g = tid; g < n_groups; g += NT) {
       int r = g / G::GPR, c = (g - r * G::GPR) * 4;
       int gy = by + r;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         int gx = bx + c + i;
         bool own = gx >= x0 && gx < x0 + TW && gy >= y0 && gy < y0 + th && gx < W && gy < H;
-        if (own) a.state_out[(long long)gy * W + gx] = P2[g_dst[k] + i].y;
+        if (own) a.state_out[(long long)gy * W + gx] = P2[r * G::PW + c + 1 + i].y;
       }
     }
+}
+template <int TW>
+__global__ void __launch_bounds__(NT, MAXB)
+    k_chain_fast(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Smem s;
+  s.rgb = smem;
+  s.P2 = reinterpret_cast<float2*>(smem + a.off_p2);
+  s.H2 = reinterpret_cast<float2*>(smem + a.off_h2);
+  s.G2 = reinterpret_cast<float2*>(smem + a.off_g2);
+  s.bar = reinterpret_cast<uint64_t*>(smem + a.off_bar);
+  s.taps = reinterpret_cast<double*>(smem + a.off_taps);
+  s.queue = reinterpret_cast<unsigned*>(smem + a.off_queue);
+  s.qcount = s.queue + QCAP;
+
+  const int tid = threadIdx.x;
+  const int tile_x = blockIdx.x % a.tiles_x, tile_y = blockIdx.x / a.tiles_x;
+  const int x0 = tile_x * TW, y0 = tile_y * a.th;
+  const int bx = x0 - 4, by = y0 - 3;
+  const int tx0 = bx >= 0 ? (bx & ~15) : -((-bx + 15) & ~15);
+
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&s.bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+    *s.qcount = 0;
   }
+  if (tid < 25) s.taps[tid] = double(a.taps[tid]);
+  __syncthreads();
+  if (tid == 0)
+    for (int t = 0; t < NS && t < a.n_frames; ++t) {
+      mbar_expect_tx(&s.bar[t], a.slot_bytes);
+      tma_load_3d(s.rgb + t * a.slot_stride, &tmap, &s.bar[t], tx0, by, 4 * t);
+    }
+  const bool interior = bx >= 0 && x0 + TW + 3 <= a.W - 1 && by >= 0 &&
+                        y0 + a.th + 2 <= a.H - 1 && ((a.th + 2) & 3) == 0;
+  if (interior)
+    march<TW, false>(tmap, a, s, x0, y0);
+  else
+    march<TW, true>(tmap, a, s, x0, y0);
 }
 
 // ------------------------------------------------------------------ host
@@ -508,7 +562,7 @@ size_t layout(int tw, int th, Args* a) {
   size_t off_p2 = off;
   off += size_t(RH) * PW * 8;
   size_t off_h2 = (off + 15) / 16 * 16;
-  off = off_h2 + size_t(RH) * HP * 8;
+  off = off_h2 + size_t(RH + 2) * HP * 8;
   size_t off_g2 = (off + 15) / 16 * 16;
   off = off_g2 + size_t(th + 3) * HP * 8;
   size_t off_bar = (off + 7) / 8 * 8;
@@ -518,7 +572,6 @@ size_t layout(int tw, int th, Args* a) {
   size_t off_queue = (off + 15) / 16 * 16;
   off = off_queue + (QCAP + 4) * 4;
   if (a) {
-    a->off_queue = unsigned(off_queue);
     a->RH = RH;
     a->BWB = BWB;
     a->slot_bytes = unsigned(slot);
@@ -528,15 +581,14 @@ size_t layout(int tw, int th, Args* a) {
     a->off_g2 = unsigned(off_g2);
     a->off_bar = unsigned(off_bar);
     a->off_taps = unsigned(off_taps);
+    a->off_queue = unsigned(off_queue);
   }
   return off;
 }
 
-// Every tile runs every frame, so a tile's cost is its per-frame work; the
-// kernel time is (waves) x (largest tile work).  Work model in lane-ops per
-// frame: ~8 per IIR cell, ~3 per H2 / G2 value, ~10 per output pixel.
 // An SM runs ceil(tiles / SMs) tiles over the whole march; two co-resident
 // CTAs hide each other's barrier waits, so single-CTA tilings pay a penalty.
+// th = 2 (mod 4) keeps interior tiles on the specialised body.
 // FUSEPLAN_FAST_TILE="tw,th" overrides the choice (tuning).
 bool choose_tiles(int W, int H, int sms, size_t smem_cap, TilePlan* best) {
   const size_t smem_per_sm = 233472;  // 228 KB per SM, 1 KB reserved per CTA
@@ -547,7 +599,7 @@ bool choose_tiles(int W, int H, int sms, size_t smem_cap, TilePlan* best) {
   for (int tw : kWidths) {
     if (force_tw && tw != force_tw) continue;
     int tx = (W + tw - 1) / tw;
-    for (int th = 2; th + 6 <= 256; ++th) {  // TMA box rows <= 256
+    for (int th = 2; th + 6 <= 256; th += 4) {  // TMA box rows <= 256
       if (force_th && th != force_th) continue;
       int ty = (H + th - 1) / th;
       if (!force_th && ty > 1 && (ty - 1) * th >= H) continue;
@@ -556,8 +608,8 @@ bool choose_tiles(int W, int H, int sms, size_t smem_cap, TilePlan* best) {
       int per_sm = int(std::min<size_t>(MAXB, smem_per_sm / (sm + 1024)));
       long long tiles = (long long)tx * ty;
       long long load = (tiles + sms - 1) / sms;
-      double work = 8.0 * (tw + 8) * (th + 6) + 3.0 * (tw + 2) * (th + 6) +
-                    3.0 * (tw + 2) * (th + 2) + 10.0 * tw * th;
+      double work = 8.0 * (tw + 8) * (th + 6) + 3.0 * (tw + 4) * (th + 6) +
+                    3.0 * (tw + 2) * (th + 2) + 8.0 * tw * th;
       double cost = double(load) * work * (per_sm >= 2 ? 1.0 : 1.3);
       if (cost < best_cost) {
         best_cost = cost;
@@ -632,10 +684,12 @@ extern "C" int fc_chain_fast(const fc_stage* sgray, const fc_stage* si, const fc
                              const fc_stage* sthr, const void* video, int in_type,
                              int gray_in, void* out, int out_type, fc_dims d, int n_warm,
                              const float* state_in, float* state_out, void* stream) {
-  // Coverage of the certified path: u8 RGBA video, {0,255} u8 mask, gaussian
-  // r = 2 with separable taps, threshold > 0, width a multiple of 16 (TMA
-  // strides), 16-byte aligned base.  Anything else -> the exact kernel.
+  // Coverage of the certified path: u8 RGBA video, {0,255} u8 mask, IIR
+  // alpha = 0.5, gaussian r = 2 with separable taps, threshold > 0, width a
+  // multiple of 16 (TMA strides), 16-byte aligned base.  Anything else runs
+  // the exact kernel.
   if (in_type != FC_U8 || out_type != FC_U8 || gray_in || sgray == nullptr) return -1;
+  if (si->alpha != 0.5f) return -1;
   if (sg->g_radius != 2 || !(sthr->th > 0.0f)) return -1;
   if (sthr->white != 255.0f || sthr->black != 0.0f) return -1;
   if (d.width % 16 != 0 || d.height < 1) return -1;
@@ -670,13 +724,10 @@ extern "C" int fc_chain_fast(const fc_stage* sgray, const fc_stage* si, const fc
   a.tiles_x = tp.tiles_x;
   a.state_in = state_in;
   a.state_out = state_out;
-  a.alpha = si->alpha;
-  a.beta = 1.0f - si->alpha;
-  a.alpha_half = si->alpha == 0.5f;
-  const float fold = a.alpha_half ? 0.5f : 1.0f;  // exact power-of-two scale
-  a.wr = sgray->wr * fold;
-  a.wg = sgray->wg * fold;
-  a.wb = sgray->wb * fold;
+  // alpha = 0.5 folded into the gray weights (exact power-of-two scale)
+  a.wr = sgray->wr * 0.5f;
+  a.wg = sgray->wg * 0.5f;
+  a.wb = sgray->wb * 0.5f;
   a.wrm = -a.wr * 8388608.0f;
   a.wgm = -a.wg * 8388608.0f;
   a.wbm = -a.wb * 8388608.0f;
@@ -720,16 +771,36 @@ extern "C" int fc_chain_fast(const fc_stage* sgray, const fc_stage* si, const fc
     return -1;
   const int grid = tp.tiles_x * tp.tiles_y;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool profile = std::getenv("FUSEPLAN_FAST_PROFILE") != nullptr;
+  if (profile) cudaMalloc(&a.dbg, sizeof(long long) * 8 * grid);
+  int rc;
   switch (tp.tw) {
-    case 32: return launch<32>(map, a, grid, tp.smem, st);
-    case 48: return launch<48>(map, a, grid, tp.smem, st);
-    case 64: return launch<64>(map, a, grid, tp.smem, st);
-    case 80: return launch<80>(map, a, grid, tp.smem, st);
-    case 96: return launch<96>(map, a, grid, tp.smem, st);
-    case 128: return launch<128>(map, a, grid, tp.smem, st);
-    case 160: return launch<160>(map, a, grid, tp.smem, st);
-    default: return -1;
+    case 32: rc = launch<32>(map, a, grid, tp.smem, st); break;
+    case 48: rc = launch<48>(map, a, grid, tp.smem, st); break;
+    case 64: rc = launch<64>(map, a, grid, tp.smem, st); break;
+    case 80: rc = launch<80>(map, a, grid, tp.smem, st); break;
+    case 96: rc = launch<96>(map, a, grid, tp.smem, st); break;
+    case 128: rc = launch<128>(map, a, grid, tp.smem, st); break;
+    case 160: rc = launch<160>(map, a, grid, tp.smem, st); break;
+    default: rc = -1;
   }
+  if (profile && a.dbg) {  // per-phase clocks per frame pair, averaged over CTAs
+    std::vector<long long> h(size_t(8) * grid);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), a.dbg, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaFree(a.dbg);
+    double sum[6] = {0, 0, 0, 0, 0, 0};
+    for (int b = 0; b < grid; ++b)
+      for (int k = 0; k < 6; ++k) sum[k] += double(h[size_t(b) * 8 + k]);
+    double pairs = (d.frames + 1) / 2;
+    std::fprintf(stderr,
+                 "fc_chain_fast tile %dx%d grid %d smem %zu: cycles/pair wait %.0f A %.0f "
+                 "B %.0f C %.0f D %.0f E %.0f\n",
+                 tp.tw, tp.th, grid, tp.smem, sum[0] / grid / pairs, sum[1] / grid / pairs,
+                 sum[2] / grid / pairs, sum[3] / grid / pairs, sum[4] / grid / pairs,
+                 sum[5] / grid / pairs);
+  }
+  return rc;
 }
 
 extern "C" long long fc_last_recheck_count(void) {
