@@ -45,6 +45,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "fc_kernels.h"
@@ -64,6 +65,7 @@ struct Args {
   unsigned slot_bytes;        // TMA bytes per frame: 3 * RH * BWB
   unsigned slot_stride;       // slot_bytes rounded up to 128
   unsigned off_p2, off_h2, off_g2, off_bar, off_taps, off_queue;
+  unsigned arr_p, arr_h, arr_g;  // byte offset of the O array in each plane
   const float* state_in;
   float* state_out;
   float wr, wg, wb, wrm, wgm, wbm;  // gray weights x 0.5 (alpha folded), -w*2^23
@@ -73,13 +75,18 @@ struct Args {
   long long* dbg;  // optional per-CTA phase clocks (FUSEPLAN_FAST_PROFILE)
 };
 
-// Phase timing (diagnostic): thread 0 accumulates clock64 deltas per phase.
+// Phase timing (diagnostic, build with -DFC_PROFILE): thread 0 accumulates
+// clock64 deltas per phase into Args::dbg.
+#ifdef FC_PROFILE
 #define FC_MARK(k)                               \
   if (prof) {                                    \
     long long now_ = clock64();                  \
     tacc[k] += now_ - tlast;                     \
     tlast = now_;                                \
   }
+#else
+#define FC_MARK(k)
+#endif
 
 __device__ unsigned long long g_rechecks;
 
@@ -148,6 +155,7 @@ __device__ __forceinline__ float2 tap5(float2 a, float2 b, float2 c, float2 d, f
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
 
+
 // 0xFF where dm >= 0 (white), else 0, for four values -> one word.  dm is
 // never -0 for m < M* (Sterbenz: the difference of nearby floats is exact),
 // so the sign bit is the decision.
@@ -157,12 +165,38 @@ __device__ __forceinline__ uint32_t pack_white(float a, float b, float c, float 
   return ~__byte_perm(__byte_perm(sa, sb, 0x0040), __byte_perm(sc, sd, 0x0040), 0x5410);
 }
 
+// ---- shared-memory planes -------------------------------------------------
+// A float2 plane (frame t, frame t+1 per cell) is stored as two arrays of
+// 16-byte chunks: chunk k of a row (cells 2k, 2k+1) lives in E if k is even,
+// in O if k is odd, at index (k >> 1).  Lanes of every phase touch
+// consecutive chunks of one array (16-byte stride, conflict-free) with
+// compile-time offsets; O starts 64 bytes past a 128-byte boundary relative
+// to E so column-wise float2 accesses (phase C) are conflict-free too.
+extern __shared__ __align__(128) unsigned char fc_smem[];
+
+struct Plane {
+  unsigned eo, oo;  // byte offsets of the E and O arrays in dynamic smem
+  int pitch;        // chunks per row in each array
+  __device__ __forceinline__ float4* E(int idx) const {
+    return reinterpret_cast<float4*>(fc_smem + eo) + idx;
+  }
+  __device__ __forceinline__ float4* O(int idx) const {
+    return reinterpret_cast<float4*>(fc_smem + oo) + idx;
+  }
+  __device__ __forceinline__ float4* chunk(int r, int k) const {
+    return (k & 1) ? O(r * pitch + (k >> 1)) : E(r * pitch + (k >> 1));
+  }
+  __device__ __forceinline__ float2* cell(int r, int c) const {
+    return reinterpret_cast<float2*>(chunk(r, c >> 1)) + (c & 1);
+  }
+};
+
 // Exact reference threshold decision at (x, y), frame component f, from the
 // exact IIR plane (simulator.cpp:63-89): FP64 gaussian in dy/dx order at the
 // 3x3 clamped centres, Sobel in the reference's float order, IEEE sqrt.
-// P2 region cell (c, r) <-> global (bx + c, by + r), stored at r*PW + c + 1.
-__device__ __noinline__ bool exact_white(const Args& a, const float2* P2, const double* taps,
-                                         int PW, int bx, int by, int x, int y, int f) {
+// P region cell (c, r) <-> global (bx + c, by + r).
+__device__ __noinline__ bool exact_white(const Args& a, const Plane P, const double* taps,
+                                         int bx, int by, int x, int y, int f) {
   float g[3][3];
   for (int j = 0; j < 3; ++j)
     for (int i = 0; i < 3; ++i) {
@@ -172,7 +206,7 @@ __device__ __noinline__ bool exact_white(const Args& a, const float2* P2, const 
         int ry = clampi(cy + dy, 0, a.H - 1) - by;
         for (int dx = -2; dx <= 2; ++dx) {
           int rx = clampi(cx + dx, 0, a.W - 1) - bx;
-          float2 v = P2[ry * PW + rx + 1];
+          float2 v = *P.cell(ry, rx);
           acc = __fma_rn(taps[(dy + 2) * 5 + dx + 2], double(f ? v.y : v.x), acc);
         }
       }
@@ -186,26 +220,31 @@ __device__ __noinline__ bool exact_white(const Args& a, const float2* P2, const 
   return __fsqrt_rn(__fadd_rn(__fmul_rn(gx, gx), __fmul_rn(gy, gy))) >= a.th_val;
 }
 
-// Fast Sobel terms for output pixels x .. x+K-1 of tile row i from G2
-// (cols c0 .. c0+K+1 hold x-1 .. x+K, rows i..i+2 hold y-1..y+1):
-// dm[k] = m - M*, both frames.  gx = v(x+1) - v(x-1) with v the [1 2 1]
-// column sum, gy = d(x-1) + 2 d(x) + d(x+1) with d = g(y+1) - g(y-1).
-template <int K>
-__device__ __forceinline__ void sobel_dm(const float2* r0, const float2* r1, const float2* r2,
-                                         float mstar, float2 (&dm)[K]) {
-  float2 v[K + 2], dd[K + 2];
+// Fast Sobel terms for output pixels x .. x+3 of one tile row from the G
+// plane (row pointers for y-1, y, y+1 at chunk q' = 2q: cols 4q .. 4q+5 hold
+// x-1 .. x+4): dm[k] = m - M*, both frames.  gx = v(x+1) - v(x-1) with v
+// the [1 2 1] column sum, gy = d(x-1) + 2 d(x) + d(x+1), d = g(y+1) - g(y-1).
+__device__ __forceinline__ void sobel_dm4(const Plane& Gp, int k0, int k1, int k2, int q,
+                                          float mstar, float2 (&dm)[4]) {
+  float2 v[6], dd[6];
+  const float4* e0 = Gp.E(k0 * Gp.pitch + q);
+  const float4* e1 = Gp.E(k1 * Gp.pitch + q);
+  const float4* e2 = Gp.E(k2 * Gp.pitch + q);
+  const float4* o0 = Gp.O(k0 * Gp.pitch + q);
+  const float4* o1 = Gp.O(k1 * Gp.pitch + q);
+  const float4* o2 = Gp.O(k2 * Gp.pitch + q);
+  const float4 t0[3] = {e0[0], o0[0], e0[1]};
+  const float4 t1[3] = {e1[0], o1[0], e1[1]};
+  const float4 t2[3] = {e2[0], o2[0], e2[1]};
 #pragma unroll
-  for (int h = 0; h < (K + 2) / 2; ++h) {
-    float4 t0 = reinterpret_cast<const float4*>(r0)[h];
-    float4 t1 = reinterpret_cast<const float4*>(r1)[h];
-    float4 t2 = reinterpret_cast<const float4*>(r2)[h];
-    v[2 * h] = __fadd2_rn(__ffma2_rn(splat(2.0f), lo2(t1), lo2(t0)), lo2(t2));
-    v[2 * h + 1] = __fadd2_rn(__ffma2_rn(splat(2.0f), hi2(t1), hi2(t0)), hi2(t2));
-    dd[2 * h] = __ffma2_rn(splat(-1.0f), lo2(t0), lo2(t2));
-    dd[2 * h + 1] = __ffma2_rn(splat(-1.0f), hi2(t0), hi2(t2));
+  for (int h = 0; h < 3; ++h) {
+    v[2 * h] = __fadd2_rn(__ffma2_rn(splat(2.0f), lo2(t1[h]), lo2(t0[h])), lo2(t2[h]));
+    v[2 * h + 1] = __fadd2_rn(__ffma2_rn(splat(2.0f), hi2(t1[h]), hi2(t0[h])), hi2(t2[h]));
+    dd[2 * h] = __ffma2_rn(splat(-1.0f), lo2(t0[h]), lo2(t2[h]));
+    dd[2 * h + 1] = __ffma2_rn(splat(-1.0f), hi2(t0[h]), hi2(t2[h]));
   }
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
+  for (int k = 0; k < 4; ++k) {
     float2 gx = __ffma2_rn(splat(-1.0f), v[k], v[k + 2]);
     float2 gy = __fadd2_rn(__ffma2_rn(splat(2.0f), dd[k + 1], dd[k]), dd[k + 2]);
     float2 m = __ffma2_rn(gx, gx, __fmul2_rn(gy, gy));
@@ -215,23 +254,22 @@ __device__ __forceinline__ void sobel_dm(const float2* r0, const float2* r1, con
 
 template <int TW>
 struct Geom {
-  static constexpr int RW = TW + 8;       // region cells per row: x0-4 .. x0+TW+3
-  static constexpr int GPR = RW / 4;      // 4-cell groups per region row
-  static constexpr int PW = RW + 4;       // P2 pitch (float2), col c at c + 1
-  static constexpr int HC = TW + 2;       // H2 / G2 columns: x0-1 .. x0+TW
-  static constexpr int HP = TW + 4;       // H2 / G2 pitch (float2)
+  static constexpr int RW = TW + 8;          // region cells per row: x0-4 .. x0+TW+3
+  static constexpr int GPR = RW / 4;         // 4-cell groups per region row
+  static constexpr int PCH = (RW + 4) / 4;   // P chunks per row per array (cols < RW+4)
+  static constexpr int HC = TW + 2;          // H / G columns: x0-1 .. x0+TW
+  static constexpr int HCH = (TW + 8) / 4;   // H / G chunks per row per array
 };
 
 struct Smem {
   unsigned char* rgb;
-  float2 *P2, *H2, *G2;
+  Plane P, Hh, Gg;
   uint64_t* bar;
   double* taps;
   unsigned *queue, *qcount;
 };
 
-// The frame march of one CTA.  BORDER = false: the haloed region lies inside
-// the video (no clamping anywhere, (th + 2) % 4 == 0, full tile).
+// The frame march of one CTA.
 template <int TW, bool BORDER>
 __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, const Smem& s,
                                       int x0, int y0) {
@@ -241,8 +279,8 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, co
   //   A  out-of-video rows read the clamped RGB row; an out-of-video 4-cell
   //      group (groups never straddle the edge: W % 4 == 0) replicates the
   //      edge byte with one PRMT -> the IIR plane holds clamped values;
-  //   C  an out-of-video G2 column is computed from the edge H2 column;
-  //   D  out-of-video G2 rows are read as the edge row.
+  //   C  an out-of-video G column is computed from the edge H column;
+  //   D  out-of-video G rows are read as the edge row.
   // The horizontal pass needs no remap: H rows are row-local and the columns
   // it produces outside the video are replaced in C.
   using G = Geom<TW>;
@@ -256,23 +294,23 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, co
   const long long hw = (long long)W * H;
   const int plane = RH * a.BWB;
   const float h0 = a.h0, h1 = a.h1, h2 = a.h2;
-  float2* const P2 = s.P2;
-  float2* const H2 = s.H2;
-  float2* const G2 = s.G2;
+  const Plane P = s.P, Hp = s.Hh, Gp = s.Gg;
 
-  // the carried IIR state is the .y half of P2
+  // the carried IIR state is the .y half of P
   if (!fresh)
     for (int g = tid; g < n_groups; g += NT) {
       int r = g / G::GPR, c = (g - r * G::GPR) * 4;
       int gy = clampi(by + r, 0, H - 1);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        P2[r * G::PW + c + 1 + i] =
+        *P.cell(r, c + i) =
             make_float2(0.0f, a.state_in[(long long)gy * W + clampi(bx + c + i, 0, W - 1)]);
     }
 
+#ifdef FC_PROFILE
   const bool prof = a.dbg != nullptr && tid == 0;
   long long tacc[6] = {0, 0, 0, 0, 0, 0}, tlast = prof ? clock64() : 0;
+#endif
   int slot = 0;          // ring slot of frame t
   unsigned parity = 0;   // mbarrier phase of that slot
   for (int t = 0; t < n; t += 2) {
@@ -285,13 +323,14 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, co
     const unsigned char* f1 = s.rgb + s1 * a.slot_stride;
     const bool steady = has1 && !(fresh && t == 0);
 
-    // ---------------- A: gray + IIR (exact) -> P2
+    // ---------------- A: gray + IIR (exact) -> P.  Scalar FP32: the two
+    // frames' products come from different PRMT words, so packing them would
+    // only add register moves.
     {
       constexpr int DR = NT / G::GPR, DC = (NT % G::GPR) * 4;
       int c4 = (tid % G::GPR) * 4, r = tid / G::GPR;
-      int dst = r * G::PW + c4 + 1;
-#pragma unroll 2
-      for (int g = tid; g < n_groups; g += NT) {
+      auto group = [&](auto steady_tag) {
+        constexpr bool STEADY = decltype(steady_tag)::value;
         const int rowsrc = (BORDER ? clampi(by + r, 0, H - 1) - by : r) * a.BWB;
         uint32_t w0[3], w1[3];
         const int x = bx + c4;
@@ -313,43 +352,48 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, co
             w1[c] = __byte_perm(*reinterpret_cast<const uint32_t*>(f1 + c * plane + rowsrc + wcol), 0, sel);
           }
         }
-        float2* d = P2 + dst;  // dst odd: d + 1 is 16-byte aligned
-        float2 q0 = d[0], q3 = d[3];
-        float4 q12 = *reinterpret_cast<const float4*>(d + 1);
-        const float st[4] = {q0.y, q12.y, q12.w, q3.y};
-        float2 y2[4];
-#define FC_CELL(I)                                                                    \
-  {                                                                                   \
-    float2 pr = wprod(f2(magic<I>(w0[0]), magic<I>(w1[0])), a.wr, a.wrm);             \
-    float2 pg = wprod(f2(magic<I>(w0[1]), magic<I>(w1[1])), a.wg, a.wgm);             \
-    float2 pb = wprod(f2(magic<I>(w0[2]), magic<I>(w1[2])), a.wb, a.wbm);             \
-    float2 gq = __fadd2_rn(__fadd2_rn(pr, pg), pb); /* = 0.5 * gray, exactly */      \
-    float ya, yb;                                                                     \
-    if (steady) {                                                                     \
-      ya = __fmaf_rn(0.5f, st[I], gq.x);                                              \
-      yb = __fmaf_rn(0.5f, ya, gq.y);                                                 \
-    } else {                                                                          \
-      ya = (fresh && t == 0) ? __fadd_rn(gq.x, gq.x) : __fmaf_rn(0.5f, st[I], gq.x);  \
-      yb = has1 ? __fmaf_rn(0.5f, ya, gq.y) : ya;                                     \
-    }                                                                                 \
-    y2[I] = f2(ya, yb);                                                               \
+        float4* d01 = P.E(r * P.pitch + (c4 >> 2));  // cells c4, c4+1 (chunk c4/2)
+        float4* d23 = P.O(r * P.pitch + (c4 >> 2));  // cells c4+2, c4+3
+        const float4 q01 = *d01, q23 = *d23;
+        const float st[4] = {q01.y, q01.w, q23.y, q23.w};
+        float y0v[4], y1v[4];
+#define FC_CELL(I)                                                                     \
+  {                                                                                    \
+    float g0 = __fadd_rn(__fadd_rn(__fmaf_rn(a.wr, magic<I>(w0[0]), a.wrm),            \
+                                   __fmaf_rn(a.wg, magic<I>(w0[1]), a.wgm)),           \
+                         __fmaf_rn(a.wb, magic<I>(w0[2]), a.wbm));                     \
+    float g1 = __fadd_rn(__fadd_rn(__fmaf_rn(a.wr, magic<I>(w1[0]), a.wrm),            \
+                                   __fmaf_rn(a.wg, magic<I>(w1[1]), a.wgm)),           \
+                         __fmaf_rn(a.wb, magic<I>(w1[2]), a.wbm));                     \
+    /* g = 0.5 * gray, exactly; y = fl(0.5 x + fl(0.5 y)) == FMA(0.5, y, g) */        \
+    if (STEADY) {                                                                      \
+      y0v[I] = __fmaf_rn(0.5f, st[I], g0);                                             \
+      y1v[I] = __fmaf_rn(0.5f, y0v[I], g1);                                            \
+    } else {                                                                           \
+      y0v[I] = (fresh && t == 0) ? __fadd_rn(g0, g0) : __fmaf_rn(0.5f, st[I], g0);     \
+      y1v[I] = has1 ? __fmaf_rn(0.5f, y0v[I], g1) : y0v[I];                            \
+    }                                                                                  \
   }
         FC_CELL(0) FC_CELL(1) FC_CELL(2) FC_CELL(3)
 #undef FC_CELL
-        d[0] = y2[0];
-        *reinterpret_cast<float4*>(d + 1) = make_float4(y2[1].x, y2[1].y, y2[2].x, y2[2].y);
-        d[3] = y2[3];
+        *d01 = make_float4(y0v[0], y1v[0], y0v[1], y1v[1]);
+        *d23 = make_float4(y0v[2], y1v[2], y0v[3], y1v[3]);
         c4 += DC;
         r += DR;
-        dst += DR * G::PW + DC;
         if (c4 >= G::RW) {
           c4 -= G::RW;
           ++r;
-          dst += G::PW - G::RW;
         }
+      };
+      if (steady) {
+#pragma unroll 2
+        for (int g = tid; g < n_groups; g += NT) group(std::true_type{});
+      } else {
+#pragma unroll 1
+        for (int g = tid; g < n_groups; g += NT) group(std::false_type{});
       }
     }
-    __syncthreads();  // P2 complete; RGB slots of t, t+1 consumed
+    __syncthreads();  // P complete; RGB slots of t, t+1 consumed
     FC_MARK(1)
 
     if (tid == 0) {  // refill the two slots with frames t+NS, t+NS+1
@@ -370,40 +414,44 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, co
     const bool out0 = t >= a.n_warm, out1 = has1 && t + 1 >= a.n_warm;
     if (!out0 && !out1) continue;  // warm-up pair: state only
 
-    // ---------------- B: horizontal pass, 4 outputs per item: H2[r][j] for
-    // centre region col j + 3, window P2 float2 j0+2 .. j0+9
+    // ---------------- B: horizontal pass, 4 outputs per item: H[r][j] for
+    // centre region col j + 3; the window chunks cover cols j0 .. j0+9
     {
       constexpr int IPR = (TW + 4) / 4;
       for (int it = tid; it < RH * IPR; it += NT) {
-        int r = it / IPR, j0 = (it - r * IPR) * 4;
-        const float4* p = reinterpret_cast<const float4*>(P2 + r * G::PW + j0 + 2);
-        float4 u0 = p[0], u1 = p[1], u2 = p[2], u3 = p[3];
-        float2 v[8] = {lo2(u0), hi2(u0), lo2(u1), hi2(u1), lo2(u2), hi2(u2), lo2(u3), hi2(u3)};
+        const int r = it / IPR, m = it - r * IPR;
+        const float4* pe = P.E(r * P.pitch + m);
+        const float4* po = P.O(r * P.pitch + m);
+        const float4 u0 = pe[0], u1 = po[0], u2 = pe[1], u3 = po[1], u4 = pe[2];
+        const float2 v[10] = {lo2(u0), hi2(u0), lo2(u1), hi2(u1), lo2(u2),
+                              hi2(u2), lo2(u3), hi2(u3), lo2(u4), hi2(u4)};
         float2 o[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) o[k] = tap5(v[k], v[k + 1], v[k + 2], v[k + 3], v[k + 4], h0, h1, h2);
-        float4* q = reinterpret_cast<float4*>(H2 + r * G::HP + j0);
-        q[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
-        q[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
+        for (int k = 0; k < 4; ++k)
+          o[k] = tap5(v[k + 1], v[k + 2], v[k + 3], v[k + 4], v[k + 5], h0, h1, h2);
+        *Hp.E(r * Hp.pitch + m) = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+        *Hp.O(r * Hp.pitch + m) = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
       }
     }
     __syncthreads();
     FC_MARK(2)
-    // ---------------- C: vertical pass, 4 G rows per item from H2 rows
+    // ---------------- C: vertical pass, 4 G rows per item from H rows
     // i0 .. i0+7 ((th + 2) % 4 == 0 by construction)
     {
       const int iq = (th + 2) >> 2;
+      const int rs = Hp.pitch * 2;  // row stride in float2
       for (int it = tid; it < iq * G::HC; it += NT) {
-        int m = it / G::HC, j = it - m * G::HC;
-        int i0 = 4 * m;
+        const int m = it / G::HC, j = it - m * G::HC;
+        const int i0 = 4 * m;
         const int jc = BORDER ? clampi(x0 - 1 + j, 0, W - 1) - (x0 - 1) : j;
-        const float2* p = H2 + i0 * G::HP + jc;
+        const float2* hp = Hp.cell(i0, jc);
         float2 v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = p[k * G::HP];
+        for (int k = 0; k < 8; ++k) v[k] = hp[k * rs];
+        float2* gp = Gp.cell(i0, j);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          G2[(i0 + k) * G::HP + j] = tap5(v[k], v[k + 1], v[k + 2], v[k + 3], v[k + 4], h0, h1, h2);
+          gp[k * rs] = tap5(v[k], v[k + 1], v[k + 2], v[k + 3], v[k + 4], h0, h1, h2);
       }
     }
     __syncthreads();
@@ -417,14 +465,13 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, co
         const int i = it / Q, q = it - i * Q;
         const int x = x0 + 4 * q, y = y0 + i;
         if (BORDER && (x >= W || y >= H)) continue;  // partial tile
-        int k0 = i, k1 = i + 1, k2 = i + 2;  // G2 rows of y-1, y, y+1
+        int k0 = i, k2 = i + 2;  // G rows of y-1, y+1
         if (BORDER) {
           k0 = clampi(y - 1, 0, H - 1) - (y0 - 1);
           k2 = clampi(y + 1, 0, H - 1) - (y0 - 1);
         }
         float2 dm[4];
-        sobel_dm<4>(G2 + k0 * G::HP + 4 * q, G2 + k1 * G::HP + 4 * q, G2 + k2 * G::HP + 4 * q,
-                    mstar, dm);
+        sobel_dm4(Gp, k0, i + 1, k2, q, mstar, dm);
         if (!has1) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) dm[k].y = INFINITY;
@@ -460,7 +507,7 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, co
         unsigned code = s.queue[e];
         int f = int(code >> 31), i = int((code >> 16) & 0x7FFF), xl = int(code & 0xFFFF);
         int x = x0 + xl, y = y0 + i;
-        bool wv = exact_white(a, P2, s.taps, G::PW, bx, by, x, y, f);
+        bool wv = exact_white(a, P, s.taps, bx, by, x, y, f);
         if (f ? out1 : out0) o0p[(f ? hw : 0) + (long long)y * W + x] = wv ? 0xFF : 0x00;
       }
       if (n_amb > unsigned(QCAP)) {  // queue overflow: recheck every uncertain pixel
@@ -471,25 +518,26 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, co
           if (x >= W || y >= H) continue;
           int k0 = clampi(y - 1, 0, H - 1) - (y0 - 1), k2 = clampi(y + 1, 0, H - 1) - (y0 - 1);
           float2 dm[4];
-          sobel_dm<4>(G2 + k0 * G::HP + 4 * q, G2 + (i + 1) * G::HP + 4 * q,
-                      G2 + k2 * G::HP + 4 * q, mstar, dm);
+          sobel_dm4(Gp, k0, i + 1, k2, q, mstar, dm);
           for (int k = 0; k < 8; ++k) {
             const int f = k >> 2, px = k & 3;
             const float v = f ? dm[px].y : dm[px].x;
             if (!(fabsf(v) <= band) || (f == 1 && !has1) || !(f ? out1 : out0)) continue;
-            bool wv = exact_white(a, P2, s.taps, G::PW, bx, by, x + px, y, f);
+            bool wv = exact_white(a, P, s.taps, bx, by, x + px, y, f);
             o0p[(f ? hw : 0) + (long long)y * W + x + px] = wv ? 0xFF : 0x00;
           }
         }
       }
       if (tid == 0) atomicAdd(&g_rechecks, (unsigned long long)n_amb);
     }
-    __syncthreads();  // E (reads P2, queue) done before the next A
+    __syncthreads();  // E (reads P, queue) done before the next A
     if (tid == 0) *s.qcount = 0;
     FC_MARK(5)
   }
+#ifdef FC_PROFILE
   if (prof)
     for (int k = 0; k < 6; ++k) a.dbg[blockIdx.x * 8 + k] = tacc[k];
+#endif
 
   if (a.state_out)
     for (int g = tid; g < n_groups; g += NT) {
@@ -499,19 +547,21 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, co
       for (int i = 0; i < 4; ++i) {
         int gx = bx + c + i;
         bool own = gx >= x0 && gx < x0 + TW && gy >= y0 && gy < y0 + th && gx < W && gy < H;
-        if (own) a.state_out[(long long)gy * W + gx] = P2[r * G::PW + c + 1 + i].y;
+        if (own) a.state_out[(long long)gy * W + gx] = P.cell(r, c + i)->y;
       }
     }
 }
+
 template <int TW>
 __global__ void __launch_bounds__(NT, MAXB)
     k_chain_fast(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
-  extern __shared__ __align__(128) unsigned char smem[];
+  using G = Geom<TW>;
+  unsigned char* smem = fc_smem;
   Smem s;
   s.rgb = smem;
-  s.P2 = reinterpret_cast<float2*>(smem + a.off_p2);
-  s.H2 = reinterpret_cast<float2*>(smem + a.off_h2);
-  s.G2 = reinterpret_cast<float2*>(smem + a.off_g2);
+  s.P = Plane{a.off_p2, a.off_p2 + a.arr_p, G::PCH};
+  s.Hh = Plane{a.off_h2, a.off_h2 + a.arr_h, G::HCH};
+  s.Gg = Plane{a.off_g2, a.off_g2 + a.arr_g, G::HCH};
   s.bar = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   s.taps = reinterpret_cast<double*>(smem + a.off_taps);
   s.queue = reinterpret_cast<unsigned*>(smem + a.off_queue);
@@ -554,17 +604,28 @@ struct TilePlan {
 };
 
 // Dynamic shared-memory layout; fills the offsets of `a` when given.
+// One plane: E then O arrays of rows x chunks float4, O offset so that its
+// bank phase is 64 bytes from E's.  Returns the bytes used; *arr = O - E.
+size_t plane_bytes(int rows, int chunks, unsigned* arr) {
+  size_t e = size_t(rows) * chunks * 16;
+  size_t o_off = (e + 127) / 128 * 128 + 64;
+  if (arr) *arr = unsigned(o_off);
+  return o_off + e;
+}
+
 size_t layout(int tw, int th, Args* a) {
-  const int RW = tw + 8, RH = th + 6, PW = RW + 4, HP = tw + 4;
+  const int RW = tw + 8, RH = th + 6;
+  const int PCH = (RW + 4) / 4, HCH = (tw + 8) / 4;
   const int BWB = (RW + 12 + 15) / 16 * 16;  // + worst-case alignment slack
   size_t slot = size_t(3) * RH * BWB, stride = (slot + 127) / 128 * 128;
   size_t off = NS * stride;
+  unsigned arr_p, arr_h, arr_g;
   size_t off_p2 = off;
-  off += size_t(RH) * PW * 8;
-  size_t off_h2 = (off + 15) / 16 * 16;
-  off = off_h2 + size_t(RH + 2) * HP * 8;
-  size_t off_g2 = (off + 15) / 16 * 16;
-  off = off_g2 + size_t(th + 3) * HP * 8;
+  off += plane_bytes(RH, PCH, &arr_p);
+  size_t off_h2 = (off + 127) / 128 * 128;
+  off = off_h2 + plane_bytes(RH + 2, HCH, &arr_h);
+  size_t off_g2 = (off + 127) / 128 * 128;
+  off = off_g2 + plane_bytes(th + 3, HCH, &arr_g);
   size_t off_bar = (off + 7) / 8 * 8;
   off = off_bar + NS * 8;
   size_t off_taps = (off + 7) / 8 * 8;
@@ -579,6 +640,9 @@ size_t layout(int tw, int th, Args* a) {
     a->off_p2 = unsigned(off_p2);
     a->off_h2 = unsigned(off_h2);
     a->off_g2 = unsigned(off_g2);
+    a->arr_p = arr_p;
+    a->arr_h = arr_h;
+    a->arr_g = arr_g;
     a->off_bar = unsigned(off_bar);
     a->off_taps = unsigned(off_taps);
     a->off_queue = unsigned(off_queue);
