@@ -64,7 +64,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "25"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -153,7 +153,7 @@ def run_reference_arm(args, W, H, F, desc):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
@@ -162,6 +162,9 @@ def main():
     ap.add_argument("--variant", default="auto", choices=["auto", "exact", "fast"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: carry planes staged through the host (lets N ranks "
+                         "share one GPU for testing)")
     args = ap.parse_args()
     W, H, F, desc = CONFIGS[args.config]
 
@@ -175,9 +178,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(torch.cuda.device_count(), 1)
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
@@ -197,45 +204,53 @@ def main():
     video = torch.empty((warm + n_local, 4, H, W), dtype=torch.uint8, device=dev)
     fp.synth_hash_u8(video, t0=lo - warm, seed=1234)
     mask = torch.empty((n_local, H, W), dtype=torch.uint8, device=dev)
-    s_warm = torch.empty((1, H, W), dtype=torch.float32, device=dev)
-    s_end = torch.empty((1, H, W), dtype=torch.float32, device=dev)
     s_recv = torch.empty((1, H, W), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     events = {"fixups": 0}
+
+    from paper_1509_04394_b200.sharding import Shard, run_sharded
+
+    shard = Shard(rank, world, lo, hi, warm)
+    bufs = {}
+
+    def run_shard(first, n, n_warm, state_in):
+        # video holds frames [lo - warm, hi) of the full video
+        v = video[first - (lo - warm):first - (lo - warm) + n]
+        s_out = bufs.setdefault(("s", n_warm > 0), torch.empty((1, H, W), device=dev))
+        o = mask[:0] if n == n_warm else mask
+        ex.run_range(v, n_warm=n_warm, state_in=state_in, state_out=s_out, out=o)
+        return o, s_out
+
+    host_stage = args.dist_backend == "gloo"
+
+    def send(state, dst):
+        dist.send(state.cpu() if host_stage else state, dst)
+
+    def recv(src):
+        if host_stage:
+            t = torch.empty((1, H, W), dtype=torch.float32)
+            dist.recv(t, src)
+            s_recv.copy_(t)
+        else:
+            dist.recv(s_recv, src)
+        return s_recv
 
     def step():
         if world == 1:
             ex.run_range(video, out=mask)
             return
-        if warm:
-            ex.run_range(video[:warm], n_warm=warm, state_out=s_warm,
-                         out=mask[:0])
-            ex.run_range(video[warm:], state_in=s_warm, state_out=s_end, out=mask)
-        else:
-            ex.run_range(video, state_out=s_end, out=mask)
-        # carry exchange + verify (exact fix-up chain on mismatch)
-        for r in range(world - 1):
-            ops = []
-            if rank == r:
-                ops.append(dist.P2POp(dist.isend, s_end, r + 1))
-            if rank == r + 1:
-                ops.append(dist.P2POp(dist.irecv, s_recv, r))
-            if ops:
-                for w_ in dist.batch_isend_irecv(ops):
-                    w_.wait()
-            if rank == r + 1:
-                if not torch.equal(s_recv, s_warm):
-                    events["fixups"] += 1
-                    ex.run_range(video[warm:], state_in=s_recv, state_out=s_end,
-                                 out=mask)
+        # T-shard protocol: warm-up, shard, NCCL carry exchange + bitwise
+        # verify, fix-up re-run on mismatch (paper_1509_04394_b200/sharding.py)
+        run_sharded(shard, run_shard, send, recv, torch.equal, events)
 
+    clocks = ClockSampler(local).__enter__()  # sampling spans warm-up + timed steps
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    if True:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -244,6 +259,7 @@ def main():
             step()
         end.record(stream)
         torch.cuda.synchronize()
+    clocks.__exit__(None, None, None)
     ms = start.elapsed_time(end) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)

@@ -223,3 +223,39 @@ def test_simulate_reports_identical_outputs(fp, cuda):
                                            "channels": 4, "noise_sigma": 8, "seed": 1234,
                                            "markers": [{"x": 20, "y": 20, "vx": 1}]})
     assert "outputs identical: true" in rep
+
+
+@pytest.mark.parametrize("world,warmup", [(4, 64), (4, 2), (3, 0)])
+def test_sharding_protocol_on_device_emulated(fp, cuda, oracle, world, warmup):
+    """The T-shard protocol (sharding.py) with the sm_100a executor as the
+    shard compute; ranks are emulated in order in one process with a mailbox
+    for the carry planes (the real run sends them over NCCL)."""
+    import torch
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    from paper_1509_04394_b200.sharding import run_sharded, shard_of
+    W, H, F = 96, 40, 60
+    pipe = spec_chain(W, H, F, th=24.0)
+    video = torch.from_numpy(hash_video_u8(F, 4, H, W, 31)).to(cuda)
+    p = fp.Pipeline(json.dumps(pipe))
+    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": "1-5"}))
+    mailbox, outs, fixups = {}, {}, {"fixups": 0}
+
+    for rank in range(world):
+        sh = shard_of(rank, world, F, warmup)
+
+        def run_shard(first, n, n_warm, state_in):
+            st = torch.empty((1, H, W), device=cuda)
+            o = ex.run_range(video[first:first + n], n_warm=n_warm, state_in=state_in,
+                             state_out=st)
+            return o, st
+
+        out, _ = run_sharded(sh, run_shard,
+                             lambda s, dst: mailbox.__setitem__(dst, s.clone()),
+                             lambda src: mailbox.pop(sh.rank),
+                             torch.equal, fixups)
+        outs[rank] = out
+    torch.cuda.synchronize()
+    got = torch.cat([outs[r] for r in range(world)]).cpu().numpy().astype(np.float32)
+    np.testing.assert_array_equal(got, oracle.orc_chain(pipe, video.cpu().numpy()))
+    if warmup <= 2:
+        assert fixups["fixups"] >= 1

@@ -1,0 +1,88 @@
+"""Multi-rank T-sharding protocol (paper_1509_04394_b200.sharding) on CPU:
+world sizes 2 and 3 over the gloo backend, each rank computing its shard
+with the oracle; the gathered result must equal the single-process run bit
+for bit, with and without forced fix-ups (tiny warm-up)."""
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, frames, warmup, result_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    from paper_1509_04394_b200.sharding import run_sharded, shard_of
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    W, H = 48, 32
+    pipe = spec_chain(W, H, frames, th=24.0)
+    video = hash_video_u8(frames, 4, H, W, 777)
+    sh = shard_of(rank, world, frames, warmup)
+
+    def run_shard(first, n, n_warm, state_in):
+        out, st = O.orc_chain(pipe, video[first:first + n], t_out=n_warm,
+                              state_in=state_in, return_state=True, nthreads=1)
+        return out, st
+
+    def send(state, dst):
+        dist.send(torch.from_numpy(np.ascontiguousarray(state)), dst)
+
+    def recv(src):
+        t = torch.empty((1, H, W), dtype=torch.float32)
+        dist.recv(t, src)
+        return t.numpy()
+
+    stats = {}
+    out, _ = run_sharded(sh, run_shard, send, recv,
+                         lambda a, b: np.array_equal(a.view(np.uint32), b.view(np.uint32)),
+                         stats)
+    # gather to rank 0
+    full = [None] * world if rank == 0 else None
+    dist.gather_object((sh.lo, out, stats["fixups"] if stats else 0), full, dst=0)
+    if rank == 0:
+        parts = sorted(full, key=lambda p: p[0])
+        got = np.concatenate([p[1] for p in parts])
+        want = O.orc_chain(pipe, video, nthreads=1)
+        np.save(result_path, np.array([int(np.array_equal(got, want)),
+                                       sum(p[2] for p in parts)]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,frames,warmup,expect_fixups",
+                         [(2, 40, 64, False), (2, 40, 3, True), (3, 45, 2, True),
+                          (3, 45, 48, None)])
+def test_sharded_run_is_exact(tmp_path, world, frames, warmup, expect_fixups):
+    out = tmp_path / "r.npy"
+    mp.spawn(_worker, args=(world, _free_port(), frames, warmup, str(out)),
+             nprocs=world, join=True)
+    ok, fixups = np.load(out)
+    assert ok == 1
+    if expect_fixups is True:
+        assert fixups >= 1
+    if expect_fixups is False:
+        assert fixups == 0
+
+
+def test_shard_bounds():
+    from paper_1509_04394_b200.sharding import shard_of
+    shards = [shard_of(r, 8, 1000) for r in range(8)]
+    assert shards[0].lo == 0 and shards[-1].hi == 1000
+    assert all(a.hi == b.lo for a, b in zip(shards, shards[1:]))
+    assert shards[0].warm == 0 and all(s.warm == 64 for s in shards[1:])
