@@ -97,8 +97,10 @@ enum { FP_ELEM_U8 = 0, FP_ELEM_F32 = 1 };
 enum { FP_EXEC_HOST_PTRS = 0, FP_EXEC_DEVICE_PTRS = 1 };
 
 /* Builds an executor for `plan` over `p` on CUDA device `device`.
- * options_json (may be NULL): {"variant": "auto"|"exact"|"fast",
- *   "host_chunk_frames": N}.  FP_ERR_INPUT if a stage has no device kernel,
+ * options_json (may be NULL): {"variant": "auto"|"exact"|"fast"|"fast_tile",
+ *   "host_chunk_frames": N}.  "fast" = the certified strip kernel (fails with
+ *   FP_ERR_INTERNAL when the chain is outside its coverage), "fast_tile" = the
+ *   earlier tile-march kernel (kept for A/B measurement).  FP_ERR_INPUT if a stage has no device kernel,
  * FP_ERR_INTERNAL if no CUDA device is present. */
 fp_status fp_exec_create(const fp_pipeline* p, const fp_plan* plan, int device,
                          const char* options_json, fp_exec** out);

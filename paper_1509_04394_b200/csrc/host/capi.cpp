@@ -452,6 +452,7 @@ fp_status fp_exec_create(const fp_pipeline* p, const fp_plan* fp, int device,
       if (v == "auto") o.variant = Variant::Auto;
       else if (v == "exact") o.variant = Variant::Exact;
       else if (v == "fast") o.variant = Variant::Fast;
+      else if (v == "fast_tile") o.variant = Variant::FastTile;
       else throw Error(ErrorKind::Input, "unknown variant: " + v);
       o.host_chunk_frames = j.value("host_chunk_frames", 0);
     }

@@ -19,7 +19,7 @@
 
 namespace fuseplan {
 
-enum class Variant { Auto = 0, Exact = 1, Fast = 2 };
+enum class Variant { Auto = 0, Exact = 1, Fast = 2, FastTile = 3 };
 
 struct ExecOptions {
   Variant variant = Variant::Auto;

@@ -1,0 +1,206 @@
+// Shared pieces of the certified fast kernels (fc_fast.cu tile march,
+// fc_strip.cu strip march): mbarrier / TMA wrappers, the exact S1+S2
+// arithmetic helpers, the FP32 stencil taps and the host-side certification
+// of the FP32 path (weights, separable taps, M*, error band).
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "fc_kernels.h"
+
+namespace fccommon {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// x (innermost, bytes) must be a multiple of 16 (measured on B200: other
+// offsets raise an illegal-instruction fault; scripts/tma_probe.cu).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// float(byte k of w) + 2^23 in one PRMT: bytes {w.k, 0, 0, 0x4B}
+template <int K>
+__device__ __forceinline__ float magic(uint32_t w) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(0x4B000000u), "n"(0x7440 + K));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 splat(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
+
+// fl(w * c), c in [0,255] held as c + 2^23: FMA(w, c + 2^23, -w 2^23)
+// rounds the exact product w*c once (w 2^23 is exact).
+__device__ __forceinline__ float2 wprod(float2 m, float w, float wm) {
+  return __ffma2_rn(splat(w), m, splat(wm));
+}
+
+// One separable FP32 gaussian tap row: h0 (|d| = 2), h1 (|d| = 1), h2 (centre).
+// The certified band (certify_band) is derived for exactly this order.
+__device__ __forceinline__ float2 tap5(float2 a, float2 b, float2 c, float2 d, float2 e,
+                                       float h0, float h1, float h2) {
+  float2 acc = __fmul2_rn(splat(h0), __fadd2_rn(a, e));
+  acc = __ffma2_rn(splat(h1), __fadd2_rn(b, d), acc);
+  return __ffma2_rn(splat(h2), c, acc);
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
+
+// 0xFF where dm >= 0 (white), else 0, for four values -> one word.  dm is
+// never -0 for m < M* (Sterbenz: the difference of nearby floats is exact),
+// so the sign bit is the decision.
+__device__ __forceinline__ uint32_t pack_white(float a, float b, float c, float d) {
+  uint32_t sa = uint32_t(__float_as_int(a) >> 31), sb = uint32_t(__float_as_int(b) >> 31);
+  uint32_t sc = uint32_t(__float_as_int(c) >> 31), sd = uint32_t(__float_as_int(d) >> 31);
+  return ~__byte_perm(__byte_perm(sa, sb, 0x0040), __byte_perm(sc, sd, 0x0040), 0x5410);
+}
+
+// ------------------------------------------------------------------ host
+
+// Parameters of the certified FP32 path, shared by both fast kernels.
+struct FastParams {
+  float wr, wg, wb, wrm, wgm, wbm;  // gray weights x 0.5 (alpha folded), -w*2^23
+  float h0, h1, h2;                 // separable fast taps: |d|=2, |d|=1, centre
+  float taps[25];                   // reference taps for the exact recheck
+  float mstar, band, th_val;
+};
+
+// Certified error band on m = gx^2 + gy^2 (u = 2^-24, all stencil inputs >= 0):
+//   kappa : relative error of the FP32 separable gaussian vs the reference's
+//           FP64-accumulated, float-rounded value: <= 8.1u (two passes of at
+//           most 4 roundings per term) + dw (separable vs reference taps) + u
+//           (the reference's final rounding) + 25 * 2^-53 (its double sums);
+//   E     : |gx_f - gx_ref| <= (kappa + 6.1u) * S, S = sum of the six taps'
+//           |values| <= 8 gmax (3 roundings on each side);
+//   Em(m) <= 4 E sqrt(m) + 2 E^2 + 4.1 u m   (|g.| <= sqrt(m), 2 roundings
+//           in each of m_f and m_ref);
+//   B solves B >= Em(M* + B); m_f >= M* + B certifies white, m_f < M* - B
+//   black.  The returned band is 2B (margin).
+inline float certify_band(float mstar, double gmax, double dw) {
+  const double u = std::ldexp(1.0, -24);
+  double kappa = 8.1 * u + dw + u + 25.0 * std::ldexp(1.0, -53);
+  double E = (kappa + 6.1 * u) * 8.0 * gmax;
+  double B = 1.0;
+  for (int it = 0; it < 60; ++it)
+    B = 4.0 * E * std::sqrt(double(mstar) + B) + 2.0 * E * E + 4.1 * u * (double(mstar) + B);
+  return float(2.0 * B + 1e-3);
+}
+
+// Coverage of the certified path + its parameters.  Returns false when the
+// chain is outside it (u8 RGBA video, {0,255} u8 mask, IIR alpha = 0.5,
+// gaussian r = 2 with separable taps, threshold > 0, width a multiple of 16
+// (TMA strides), 16-byte aligned base); the caller then runs the exact kernel.
+inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                        const fc_stage* sthr, const void* video, int in_type, int gray_in,
+                        int out_type, fc_dims d, FastParams* p) {
+  if (in_type != FC_U8 || out_type != FC_U8 || gray_in || sgray == nullptr) return false;
+  if (si->alpha != 0.5f) return false;
+  if (sg->g_radius != 2 || !(sthr->th > 0.0f)) return false;
+  if (sthr->white != 255.0f || sthr->black != 0.0f) return false;
+  if (d.width % 16 != 0 || d.height < 1) return false;
+  if (reinterpret_cast<uintptr_t>(video) % 16 != 0) return false;
+  std::memset(p, 0, sizeof *p);
+  // alpha = 0.5 folded into the gray weights (exact power-of-two scale)
+  p->wr = sgray->wr * 0.5f;
+  p->wg = sgray->wg * 0.5f;
+  p->wb = sgray->wb * 0.5f;
+  p->wrm = -p->wr * 8388608.0f;
+  p->wgm = -p->wg * 8388608.0f;
+  p->wbm = -p->wb * 8388608.0f;
+  // Separable fast taps from the centre row of the reference taps: in exact
+  // arithmetic w[2][k] / sum_k w[2][k] is the normalised 1-D gaussian.
+  double e[5], row = 0.0, es = 0.0;
+  for (int k = 0; k < 5; ++k) row += double(sg->g_w[10 + k]);
+  for (int k = 0; k < 5; ++k) es += (e[k] = double(sg->g_w[10 + k]) / row);
+  p->h0 = float(e[0] / es);
+  p->h1 = float(e[1] / es);
+  p->h2 = float(e[2] / es);
+  const float hh[5] = {p->h0, p->h1, p->h2, p->h1, p->h0};
+  double dw = 0.0;  // worst relative mismatch of h_i h_j vs the reference taps
+  for (int j = 0; j < 5; ++j)
+    for (int i = 0; i < 5; ++i) {
+      double ref = sg->g_w[j * 5 + i];
+      dw = std::max(dw, std::fabs(double(hh[j]) * hh[i] - ref) / ref);
+    }
+  if (!(dw < 1e-5)) return false;  // not separable enough to certify
+  std::memcpy(p->taps, sg->g_w, sizeof p->taps);
+  p->th_val = sthr->th;
+  // M* = min float m with sqrtf(m) >= th
+  float m = sthr->th * sthr->th;
+  while (m > 0.0f && std::sqrt(std::nextafter(m, 0.0f)) >= sthr->th) m = std::nextafter(m, 0.0f);
+  while (std::sqrt(m) < sthr->th) m = std::nextafter(m, INFINITY);
+  p->mstar = m;
+  double gray_max = 255.0 * (double(sgray->wr) + double(sgray->wg) + double(sgray->wb));
+  double tap_sum = 0.0;
+  for (int k = 0; k < 25; ++k) tap_sum += sg->g_w[k];
+  p->band = certify_band(p->mstar, gray_max * tap_sum * 1.001, dw);
+  return true;
+}
+
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 3-D map over the planar video [4T][H][W] u8 with a box of (bw, rows, 3):
+// one copy brings the R, G, B planes of a haloed window of one frame.
+inline bool rgb_tensor_map(CUtensorMap* map, const void* video, fc_dims d, int bw, int rows) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {cuuint64_t(d.width), cuuint64_t(d.height), cuuint64_t(4) * d.frames};
+  cuuint64_t strides[2] = {cuuint64_t(d.width), cuuint64_t(d.width) * d.height};
+  cuuint32_t box[3] = {cuuint32_t(bw), cuuint32_t(rows), 3};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(video), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace fccommon

@@ -3,20 +3,20 @@
 
 #include "fc_kernels.h"
 
-extern "C" int fc_chain_exact(const fc_stage* sgray, const fc_stage* si,
-                              const fc_stage* sg, const fc_stage* sthr,
-                              const void* video, int in_type, int gray_in,
-                              void* out, int out_type, fc_dims d, int n_warm,
-                              const float* state_in, float* state_out,
-                              void* stream);
+#define FC_CHAIN_ARGS                                                          \
+  const fc_stage *sgray, const fc_stage *si, const fc_stage *sg,               \
+      const fc_stage *sthr, const void *video, int in_type, int gray_in,       \
+      void *out, int out_type, fc_dims d, int n_warm, const float *state_in,   \
+      float *state_out, void *stream
 
-extern "C" int fc_chain_fast(const fc_stage* sgray, const fc_stage* si,
-                             const fc_stage* sg, const fc_stage* sthr,
-                             const void* video, int in_type, int gray_in,
-                             void* out, int out_type, fc_dims d, int n_warm,
-                             const float* state_in, float* state_out,
-                             void* stream);
+extern "C" int fc_chain_exact(FC_CHAIN_ARGS);  // fc_exact.cu: FP64 everywhere
+extern "C" int fc_chain_strip(FC_CHAIN_ARGS);  // fc_strip.cu: certified, headline
+extern "C" int fc_chain_tile(FC_CHAIN_ARGS);   // fc_fast.cu: certified, tile march
+extern "C" long long fc_strip_recheck_count(void);
+extern "C" long long fc_tile_recheck_count(void);
 
+// variant: 0 auto (strip kernel when covered, else exact), 1 exact,
+//          2 fast (strip kernel or -1), 3 fast_tile (tile kernel or -1).
 extern "C" int fc_fused_chain(const fc_stage* sgray, const fc_stage* si,
                               const fc_stage* sg, const fc_stage* sgrad,
                               const fc_stage* sthr, const void* video,
@@ -24,11 +24,19 @@ extern "C" int fc_fused_chain(const fc_stage* sgray, const fc_stage* si,
                               fc_dims d, int n_warm, const float* state_in,
                               float* state_out, int variant, void* stream) {
   (void)sgrad;
+  if (variant == 3)
+    return fc_chain_tile(sgray, si, sg, sthr, video, in_type, gray_in, out,
+                         out_type, d, n_warm, state_in, state_out, stream);
   if (variant == 2 || variant == 0) {
-    int rc = fc_chain_fast(sgray, si, sg, sthr, video, in_type, gray_in, out,
-                           out_type, d, n_warm, state_in, state_out, stream);
+    int rc = fc_chain_strip(sgray, si, sg, sthr, video, in_type, gray_in, out,
+                            out_type, d, n_warm, state_in, state_out, stream);
     if (rc != -1 || variant == 2) return rc;  // -1: parameters not covered
   }
   return fc_chain_exact(sgray, si, sg, sthr, video, in_type, gray_in, out,
                         out_type, d, n_warm, state_in, state_out, stream);
+}
+
+extern "C" long long fc_last_recheck_count(void) {
+  long long a = fc_strip_recheck_count(), b = fc_tile_recheck_count();
+  return (a < 0 || b < 0) ? -1 : a + b;
 }

@@ -48,9 +48,12 @@
 #include <type_traits>
 #include <vector>
 
+#include "fc_common.cuh"
 #include "fc_kernels.h"
 
 namespace fcfast {
+
+using namespace fccommon;
 
 constexpr int NT = 256;   // threads per CTA
 constexpr int MAXB = 2;   // CTAs per SM (2 x 256 threads x 128 registers)
@@ -89,81 +92,6 @@ struct Args {
 #endif
 
 __device__ unsigned long long g_rechecks;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
-// x (innermost, bytes) must be a multiple of 16 (measured on B200: other
-// offsets raise an illegal-instruction fault; scripts/tma_probe.cu).
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int x, int y, int z) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// float(byte k of w) + 2^23 in one PRMT: bytes {w.k, 0, 0, 0x4B}
-template <int K>
-__device__ __forceinline__ float magic(uint32_t w) {
-  uint32_t r;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(0x4B000000u), "n"(0x7440 + K));
-  return __uint_as_float(r);
-}
-
-__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
-__device__ __forceinline__ float2 splat(float a) { return make_float2(a, a); }
-__device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
-__device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
-
-// fl(w * c), c in [0,255] held as c + 2^23: FMA(w, c + 2^23, -w 2^23)
-// rounds the exact product w*c once (w 2^23 is exact).
-__device__ __forceinline__ float2 wprod(float2 m, float w, float wm) {
-  return __ffma2_rn(splat(w), m, splat(wm));
-}
-
-__device__ __forceinline__ float2 tap5(float2 a, float2 b, float2 c, float2 d, float2 e,
-                                       float h0, float h1, float h2) {
-  float2 acc = __fmul2_rn(splat(h0), __fadd2_rn(a, e));
-  acc = __ffma2_rn(splat(h1), __fadd2_rn(b, d), acc);
-  return __ffma2_rn(splat(h2), c, acc);
-}
-
-__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
-
-
-// 0xFF where dm >= 0 (white), else 0, for four values -> one word.  dm is
-// never -0 for m < M* (Sterbenz: the difference of nearby floats is exact),
-// so the sign bit is the decision.
-__device__ __forceinline__ uint32_t pack_white(float a, float b, float c, float d) {
-  uint32_t sa = uint32_t(__float_as_int(a) >> 31), sb = uint32_t(__float_as_int(b) >> 31);
-  uint32_t sc = uint32_t(__float_as_int(c) >> 31), sd = uint32_t(__float_as_int(d) >> 31);
-  return ~__byte_perm(__byte_perm(sa, sb, 0x0040), __byte_perm(sc, sd, 0x0040), 0x5410);
-}
 
 // ---- shared-memory planes -------------------------------------------------
 // A float2 plane (frame t, frame t+1 per cell) is stored as two arrays of
@@ -684,27 +612,6 @@ bool choose_tiles(int W, int H, int sms, size_t smem_cap, TilePlan* best) {
   return best_cost < 1e300;
 }
 
-// Certified error band on m = gx^2 + gy^2 (u = 2^-24, all stencil inputs >= 0):
-//   kappa : relative error of the FP32 separable gaussian vs the reference's
-//           FP64-accumulated, float-rounded value: <= 8.1u (two passes of at
-//           most 4 roundings per term) + dw (separable vs reference taps) + u
-//           (the reference's final rounding) + 25 * 2^-53 (its double sums);
-//   E     : |gx_f - gx_ref| <= (kappa + 6.1u) * S, S = sum of the six taps'
-//           |values| <= 8 gmax (3 roundings on each side);
-//   Em(m) <= 4 E sqrt(m) + 2 E^2 + 4.1 u m   (|g.| <= sqrt(m), 2 roundings
-//           in each of m_f and m_ref);
-//   B solves B >= Em(M* + B); m_f >= M* + B certifies white, m_f < M* - B
-//   black.  The returned band is 2B (margin).
-float certify_band(float mstar, double gmax, double dw) {
-  const double u = std::ldexp(1.0, -24);
-  double kappa = 8.1 * u + dw + u + 25.0 * std::ldexp(1.0, -53);
-  double E = (kappa + 6.1 * u) * 8.0 * gmax;
-  double B = 1.0;
-  for (int it = 0; it < 60; ++it)
-    B = 4.0 * E * std::sqrt(double(mstar) + B) + 2.0 * E * E + 4.1 * u * (double(mstar) + B);
-  return float(2.0 * B + 1e-3);
-}
-
 template <int TW>
 int launch(const CUtensorMap& map, const Args& a, int grid, size_t smem, cudaStream_t st) {
   static size_t configured = 0;
@@ -724,19 +631,6 @@ using namespace fcfast;
 
 namespace {
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
 struct PlanCache {
   int W = -1, H = -1, dev = -1;
   TilePlan tp;
@@ -744,24 +638,14 @@ struct PlanCache {
 
 }  // namespace
 
-extern "C" int fc_chain_fast(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+extern "C" int fc_chain_tile(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
                              const fc_stage* sthr, const void* video, int in_type,
                              int gray_in, void* out, int out_type, fc_dims d, int n_warm,
                              const float* state_in, float* state_out, void* stream) {
-  // Coverage of the certified path: u8 RGBA video, {0,255} u8 mask, IIR
-  // alpha = 0.5, gaussian r = 2 with separable taps, threshold > 0, width a
-  // multiple of 16 (TMA strides), 16-byte aligned base.  Anything else runs
-  // the exact kernel.
-  if (in_type != FC_U8 || out_type != FC_U8 || gray_in || sgray == nullptr) return -1;
-  if (si->alpha != 0.5f) return -1;
-  if (sg->g_radius != 2 || !(sthr->th > 0.0f)) return -1;
-  if (sthr->white != 255.0f || sthr->black != 0.0f) return -1;
-  if (d.width % 16 != 0 || d.height < 1) return -1;
-  if (reinterpret_cast<uintptr_t>(video) % 16 != 0) return -1;
+  FastParams fp;
+  if (!fast_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d, &fp)) return -1;
   if (d.frames == 0) return 0;
-  auto enc = encode_fn();
-  if (!enc) return -1;
-
+  (void)si;
   int dev = 0;
   cudaGetDevice(&dev);
   static thread_local PlanCache cache;
@@ -788,51 +672,13 @@ extern "C" int fc_chain_fast(const fc_stage* sgray, const fc_stage* si, const fc
   a.tiles_x = tp.tiles_x;
   a.state_in = state_in;
   a.state_out = state_out;
-  // alpha = 0.5 folded into the gray weights (exact power-of-two scale)
-  a.wr = sgray->wr * 0.5f;
-  a.wg = sgray->wg * 0.5f;
-  a.wb = sgray->wb * 0.5f;
-  a.wrm = -a.wr * 8388608.0f;
-  a.wgm = -a.wg * 8388608.0f;
-  a.wbm = -a.wb * 8388608.0f;
-  // Separable fast taps from the centre row of the reference taps: in exact
-  // arithmetic w[2][k] / sum_k w[2][k] is the normalised 1-D gaussian.
-  double e[5], row = 0.0, es = 0.0;
-  for (int k = 0; k < 5; ++k) row += double(sg->g_w[10 + k]);
-  for (int k = 0; k < 5; ++k) es += (e[k] = double(sg->g_w[10 + k]) / row);
-  a.h0 = float(e[0] / es);
-  a.h1 = float(e[1] / es);
-  a.h2 = float(e[2] / es);
-  const float hh[5] = {a.h0, a.h1, a.h2, a.h1, a.h0};
-  double dw = 0.0;  // worst relative mismatch of h_i h_j vs the reference taps
-  for (int j = 0; j < 5; ++j)
-    for (int i = 0; i < 5; ++i) {
-      double ref = sg->g_w[j * 5 + i];
-      dw = std::max(dw, std::fabs(double(hh[j]) * hh[i] - ref) / ref);
-    }
-  if (!(dw < 1e-5)) return -1;  // not separable enough to certify
-  std::memcpy(a.taps, sg->g_w, sizeof a.taps);
-  a.th_val = sthr->th;
-  // M* = min float m with sqrtf(m) >= th
-  float m = sthr->th * sthr->th;
-  while (m > 0.0f && std::sqrt(std::nextafter(m, 0.0f)) >= sthr->th) m = std::nextafter(m, 0.0f);
-  while (std::sqrt(m) < sthr->th) m = std::nextafter(m, INFINITY);
-  a.mstar = m;
-  double gray_max = 255.0 * (double(sgray->wr) + double(sgray->wg) + double(sgray->wb));
-  double tap_sum = 0.0;
-  for (int k = 0; k < 25; ++k) tap_sum += sg->g_w[k];
-  a.band = certify_band(a.mstar, gray_max * tap_sum * 1.001, dw);
+  a.wr = fp.wr, a.wg = fp.wg, a.wb = fp.wb, a.wrm = fp.wrm, a.wgm = fp.wgm, a.wbm = fp.wbm;
+  a.h0 = fp.h0, a.h1 = fp.h1, a.h2 = fp.h2;
+  std::memcpy(a.taps, fp.taps, sizeof a.taps);
+  a.mstar = fp.mstar, a.band = fp.band, a.th_val = fp.th_val;
 
   CUtensorMap map;
-  cuuint64_t dims[3] = {cuuint64_t(d.width), cuuint64_t(d.height), cuuint64_t(4) * d.frames};
-  cuuint64_t strides[2] = {cuuint64_t(d.width), cuuint64_t(d.width) * d.height};
-  cuuint32_t box[3] = {cuuint32_t(a.BWB), cuuint32_t(a.RH), 3};
-  cuuint32_t estr[3] = {1, 1, 1};
-  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(video), dims, strides,
-          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-          CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return -1;
+  if (!rgb_tensor_map(&map, video, d, a.BWB, a.RH)) return -1;
   const int grid = tp.tiles_x * tp.tiles_y;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool profile = std::getenv("FUSEPLAN_FAST_PROFILE") != nullptr;
@@ -867,7 +713,7 @@ extern "C" int fc_chain_fast(const fc_stage* sgray, const fc_stage* si, const fc
   return rc;
 }
 
-extern "C" long long fc_last_recheck_count(void) {
+extern "C" long long fc_tile_recheck_count(void) {
   unsigned long long v = 0;
   if (cudaMemcpyFromSymbol(&v, g_rechecks, sizeof v) != cudaSuccess) return -1;
   return (long long)v;

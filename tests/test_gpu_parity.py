@@ -104,23 +104,28 @@ def test_larger_hash_video_dense_mask(fp, cuda, oracle):
             np.testing.assert_array_equal(out, want, err_msg=f"{part} {variant}")
 
 
+@pytest.mark.parametrize("variant", ["fast", "fast_tile"])
 @pytest.mark.parametrize("shape,th", [((64, 48, 20), 128.0), ((160, 120, 24), 24.0),
                                       ((192, 96, 17), 40.0), ((48, 37, 9), 24.0),
-                                      ((800, 64, 6), 24.0), ((16, 8, 5), 12.0)])
-def test_fast_certified_path_exact(fp, cuda, oracle, shape, th):
-    """The certified FP32 kernel (variant='fast' fails loudly if it does not
-    apply) is bit-exact, including pixels that took the FP64 recheck."""
+                                      ((800, 64, 6), 24.0), ((16, 8, 5), 12.0),
+                                      ((256, 200, 11), 24.0), ((368, 131, 4), 30.0),
+                                      ((240, 1, 3), 8.0), ((128, 300, 2), 24.0)])
+def test_fast_certified_path_exact(fp, cuda, oracle, shape, th, variant):
+    """The certified FP32 kernels (variant='fast' = strip march, 'fast_tile' =
+    tile march; both fail loudly if they do not apply) are bit-exact,
+    including pixels that took the FP64 recheck."""
     from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
     W, H, F = shape
     pipe = spec_chain(W, H, F, th=th)
     v = hash_video_u8(F, 4, H, W, 4242)
     want = oracle.orc_chain(pipe, v)
-    out, ex = run(fp, pipe, v, {"force_partition": "1-5"}, variant="fast", torch_dev=cuda)
+    out, ex = run(fp, pipe, v, {"force_partition": "1-5"}, variant=variant, torch_dev=cuda)
     np.testing.assert_array_equal(out, want)
     assert ex.describe()["exact_rechecks_total"] >= 0
 
 
-def test_fast_path_rechecks_happen_and_are_exact(fp, cuda, oracle):
+@pytest.mark.parametrize("variant", ["fast", "fast_tile"])
+def test_fast_path_rechecks_happen_and_are_exact(fp, cuda, oracle, variant):
     """A threshold placed in the bulk of the gradient distribution forces many
     pixels into the uncertain band; all of them must resolve exactly."""
     from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
@@ -133,7 +138,7 @@ def test_fast_path_rechecks_happen_and_are_exact(fp, cuda, oracle):
     want = oracle.orc_chain(pipe, v)
     p = fp.Pipeline(json.dumps(pipe))
     ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": "1-5"}),
-                     variant="fast")
+                     variant=variant)
     before = ex.describe()["exact_rechecks_total"]
     import torch
     out = ex.run(torch.from_numpy(v).to(cuda))
