@@ -62,6 +62,26 @@ __device__ __forceinline__ float magic(uint32_t w) {
   return __uint_as_float(r);
 }
 
+// Same with the 0x4B000000 word in a register the compiler cannot see
+// through (kernel parameter): the selector then stays an immediate instead
+// of being re-materialised into a register for every PRMT.
+template <int K>
+__device__ __forceinline__ float magic_r(uint32_t w, uint32_t k4b) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(k4b), "n"(0x7440 + K));
+  return __uint_as_float(r);
+}
+
+// 0xFF where nd < 0, else 0, for four values -> one word: PRMT's
+// sign-replicate mode (selector nibble 8 + byte) on byte 3 of each float.
+__device__ __forceinline__ uint32_t pack_neg(float a, float b, float c, float d) {
+  uint32_t ab, cd, r;
+  asm("prmt.b32 %0, %1, %2, 0x00FB;" : "=r"(ab) : "r"(__float_as_uint(a)), "r"(__float_as_uint(b)));
+  asm("prmt.b32 %0, %1, %2, 0x00FB;" : "=r"(cd) : "r"(__float_as_uint(c)), "r"(__float_as_uint(d)));
+  asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(r) : "r"(ab), "r"(cd));
+  return r;
+}
+
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 splat(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
@@ -101,6 +121,8 @@ struct FastParams {
   float h0, h1, h2;                 // separable fast taps: |d|=2, |d|=1, centre
   float taps[25];                   // reference taps for the exact recheck
   float mstar, band, th_val;
+  float mlo;        // largest float below M*: white <=> m > mlo <=> mlo - m < 0
+  uint32_t k4b;     // 0x4B000000 (see magic_r)
 };
 
 // Certified error band on m = gx^2 + gy^2 (u = 2^-24, all stencil inputs >= 0):
@@ -111,7 +133,8 @@ struct FastParams {
 //   E     : |gx_f - gx_ref| <= (kappa + 6.1u) * S, S = sum of the six taps'
 //           |values| <= 8 gmax (3 roundings on each side);
 //   Em(m) <= 4 E sqrt(m) + 2 E^2 + 4.1 u m   (|g.| <= sqrt(m), 2 roundings
-//           in each of m_f and m_ref);
+//           in each of m_f and m_ref) + 2u (M* + m) (the strip kernel forms
+//           mlo - gy^2 - gx^2 with two FMAs instead of m - M*);
 //   B solves B >= Em(M* + B); m_f >= M* + B certifies white, m_f < M* - B
 //   black.  The returned band is 2B (margin).
 inline float certify_band(float mstar, double gmax, double dw) {
@@ -120,7 +143,8 @@ inline float certify_band(float mstar, double gmax, double dw) {
   double E = (kappa + 6.1 * u) * 8.0 * gmax;
   double B = 1.0;
   for (int it = 0; it < 60; ++it)
-    B = 4.0 * E * std::sqrt(double(mstar) + B) + 2.0 * E * E + 4.1 * u * (double(mstar) + B);
+    B = 4.0 * E * std::sqrt(double(mstar) + B) + 2.0 * E * E + 4.1 * u * (double(mstar) + B) +
+        2.0 * u * (2.0 * double(mstar) + B);
   return float(2.0 * B + 1e-3);
 }
 
@@ -168,6 +192,8 @@ inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stag
   while (m > 0.0f && std::sqrt(std::nextafter(m, 0.0f)) >= sthr->th) m = std::nextafter(m, 0.0f);
   while (std::sqrt(m) < sthr->th) m = std::nextafter(m, INFINITY);
   p->mstar = m;
+  p->mlo = std::nextafter(m, 0.0f);
+  p->k4b = 0x4B000000u;
   double gray_max = 255.0 * (double(sgray->wr) + double(sgray->wg) + double(sgray->wb));
   double tap_sum = 0.0;
   for (int k = 0; k < 25; ++k) tap_sum += sg->g_w[k];

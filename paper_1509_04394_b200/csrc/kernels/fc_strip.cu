@@ -48,7 +48,7 @@ constexpr int NWMAX = 9;   // warps per CTA (bounded by shared memory)
 constexpr int NSF = 4;     // TMA frame slots (two frame pairs in flight)
 constexpr int SW = 120;    // output columns per strip (window 128 = SW + 8)
 constexpr int BWB = 144;   // TMA box row bytes: 128 + worst-case 16-B alignment slack
-constexpr int ROWB = 1024; // bytes per plane row: 2 halves x 32 lanes x float4
+constexpr int ROWB = 1024; // bytes per plane row: 4 cell slots x 32 lanes x float2
 
 struct Args {
   uint8_t* out;
@@ -72,15 +72,16 @@ __device__ __forceinline__ float2 shfl_down2(float2 v) {
                      __shfl_down_sync(0xffffffffu, v.y, 1));
 }
 
-// Plane row r, half h (cells 4L, 4L+1 | 4L+2, 4L+3 of every lane L), this lane.
-__device__ __forceinline__ float4* prow(unsigned off, int r, int h, int lane) {
-  return reinterpret_cast<float4*>(fs_smem + off + r * ROWB + h * 512) + lane;
+// Plane cell (row r, cell j of every lane L = window col 4L + j), this lane:
+// slot j of a row is a contiguous float2[32] (conflict-free 8-byte accesses).
+__device__ __forceinline__ float2* pcell(unsigned off, int r, int j, int lane) {
+  return reinterpret_cast<float2*>(fs_smem + off + r * ROWB + j * 256) + lane;
 }
 
 // Frame component f of IIR cell (window row r, window col c).
 __device__ __forceinline__ float iir_cell(unsigned off, int r, int c, int f) {
-  return *reinterpret_cast<const float*>(fs_smem + off + r * ROWB + ((c & 3) >> 1) * 512 +
-                                         (c >> 2) * 16 + (c & 1) * 8 + f * 4);
+  return *reinterpret_cast<const float*>(fs_smem + off + r * ROWB + (c & 3) * 256 +
+                                         (c >> 2) * 8 + f * 4);
 }
 
 // Exact reference threshold decision at (x, y), frame component f, from the
@@ -144,14 +145,20 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, in
 #pragma unroll
   for (int i = 0; i < RY; ++i) outr[i] = r0 + i >= 3 && r0 + i <= R - 4 && by + r0 + i < H;
 
-  float st[RY][4];  // exact IIR state of the lane's 16 cells
+  // IIR values of the lane's 16 cells for the current pair (frame t, t+1);
+  // .y is the exact carried state
+  float2 sv[RY][4];
 #pragma unroll
   for (int i = 0; i < RY; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      st[i][j] = fresh ? 0.0f
-                       : a.state_in[(long long)clampi(by + r0 + i, 0, H - 1) * W +
-                                    clampi(xl + j, 0, W - 1)];
+      sv[i][j].y = fresh ? 0.0f
+                         : a.state_in[(long long)clampi(by + r0 + i, 0, H - 1) * W +
+                                      clampi(xl + j, 0, W - 1)];
+  uint32_t orow[RY];  // mask offset of the lane's first cell in each row
+#pragma unroll
+  for (int i = 0; i < RY; ++i) orow[i] = uint32_t((by + r0 + i) * W + xl);
+  const uint32_t k4b = a.p.k4b;
 
   float2 hreg[RY][4];  // horizontal-pass values of the lane's cells
   int slot = 0;
@@ -180,39 +187,34 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, in
             w1[c] = __byte_perm(w1[c], 0, sel);
           }
         }
-        float2 v[4];
-#define FS_CELL(J)                                                                     \
-  {                                                                                    \
-    const float2 g = __fadd2_rn(                                                       \
-        __fadd2_rn(wprod(f2(magic<J>(w0[0]), magic<J>(w1[0])), a.p.wr, a.p.wrm),       \
-                   wprod(f2(magic<J>(w0[1]), magic<J>(w1[1])), a.p.wg, a.p.wgm)),      \
-        wprod(f2(magic<J>(w0[2]), magic<J>(w1[2])), a.p.wb, a.p.wbm));                 \
-    /* g = 0.5 * gray, exactly; y = fl(0.5 x + fl(0.5 y)) == FMA(0.5, y, g) */        \
-    float y0v, y1v;                                                                    \
-    if (STEADY) {                                                                      \
-      y0v = __fmaf_rn(0.5f, st[i][J], g.x);                                            \
-      y1v = __fmaf_rn(0.5f, y0v, g.y);                                                 \
-    } else {                                                                           \
-      y0v = (fresh && t == 0) ? __fadd_rn(g.x, g.x) : __fmaf_rn(0.5f, st[i][J], g.x);  \
-      y1v = has1 ? __fmaf_rn(0.5f, y0v, g.y) : y0v;                                    \
-    }                                                                                  \
-    st[i][J] = y1v;                                                                    \
-    v[J] = f2(y0v, y1v);                                                               \
+        float2* v = sv[i];
+#define FS_CELL(J)                                                                          \
+  {                                                                                         \
+    const float2 g = __fadd2_rn(                                                            \
+        __fadd2_rn(wprod(f2(magic_r<J>(w0[0], k4b), magic_r<J>(w1[0], k4b)), a.p.wr, a.p.wrm), \
+                   wprod(f2(magic_r<J>(w0[1], k4b), magic_r<J>(w1[1], k4b)), a.p.wg, a.p.wgm)), \
+        wprod(f2(magic_r<J>(w0[2], k4b), magic_r<J>(w1[2], k4b)), a.p.wb, a.p.wbm));          \
+    /* g = 0.5 * gray, exactly; y = fl(0.5 x + fl(0.5 y)) == FMA(0.5, y, g) */             \
+    if (STEADY) {                                                                           \
+      v[J].x = __fmaf_rn(0.5f, v[J].y, g.x);                                                \
+      v[J].y = __fmaf_rn(0.5f, v[J].x, g.y);                                                \
+    } else {                                                                                \
+      v[J].x = (fresh && t == 0) ? __fadd_rn(g.x, g.x) : __fmaf_rn(0.5f, v[J].y, g.x);      \
+      v[J].y = has1 ? __fmaf_rn(0.5f, v[J].x, g.y) : v[J].x;                                \
+    }                                                                                       \
   }
         FS_CELL(0) FS_CELL(1) FS_CELL(2) FS_CELL(3)
 #undef FS_CELL
-        *prow(iir_off, r0 + i, 0, lane) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
-        *prow(iir_off, r0 + i, 1, lane) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) *pcell(iir_off, r0 + i, j, lane) = v[j];
         const float2 l2 = shfl_up2(v[2]), l1 = shfl_up2(v[3]);
         const float2 q1 = shfl_down2(v[0]), q2 = shfl_down2(v[1]);
         hreg[i][0] = tap5(l2, l1, v[0], v[1], v[2], h0, h1, h2);
         hreg[i][1] = tap5(l1, v[0], v[1], v[2], v[3], h0, h1, h2);
         hreg[i][2] = tap5(v[0], v[1], v[2], v[3], q1, h0, h1, h2);
         hreg[i][3] = tap5(v[1], v[2], v[3], q1, q2, h0, h1, h2);
-        *prow(h_off, r0 + i, 0, lane) =
-            make_float4(hreg[i][0].x, hreg[i][0].y, hreg[i][1].x, hreg[i][1].y);
-        *prow(h_off, r0 + i, 1, lane) =
-            make_float4(hreg[i][2].x, hreg[i][2].y, hreg[i][3].x, hreg[i][3].y);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) *pcell(h_off, r0 + i, j, lane) = hreg[i][j];
       }
     };
     if (has1 && !(fresh && t == 0))
@@ -249,11 +251,8 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, in
         for (int j = 0; j < 4; ++j) hh[k][j] = hreg[k - 3][j];
       } else {
         const int r = clampi(r0 - 3 + k, 0, R - 1);
-        const float4 A = *prow(h_off, r, 0, lane), B = *prow(h_off, r, 1, lane);
-        hh[k][0] = lo2(A);
-        hh[k][1] = hi2(A);
-        hh[k][2] = lo2(B);
-        hh[k][3] = hi2(B);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) hh[k][j] = *pcell(h_off, r, j, lane);
       }
     }
     float2 g[RY + 2][4];  // G rows r0-1 .. r0+4
@@ -265,8 +264,10 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, in
                        h1, h2);
 
     unsigned char* o0p = a.out + (long long)(t - a.n_warm) * hw;
-    const float mstar = a.p.mstar, band = a.p.band;
-    float2 dm[RY][4];
+    unsigned char* o1p = o0p + hw;
+    const float mlo = a.p.mlo, band = a.p.band;
+    const bool st0 = outl && out0, st1 = outl && out1;
+    float2 dm[RY][4];  // mlo - m per cell and frame
     float amin = INFINITY;
 #pragma unroll
     for (int i = 0; i < RY; ++i) {
@@ -294,20 +295,18 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, in
       for (int j = 0; j < 4; ++j) {
         const float2 gx = __ffma2_rn(splat(-1.0f), S[j], S[j + 2]);
         const float2 gy = __fadd2_rn(__ffma2_rn(splat(2.0f), D[j + 1], D[j]), D[j + 2]);
-        const float2 m = __ffma2_rn(gx, gx, __fmul2_rn(gy, gy));
-        dm[i][j] = __fadd2_rn(m, splat(-mstar));
-        if (!has1) dm[i][j].y = INFINITY;
+        // nd = mlo - gy^2 - gx^2 (< 0 <=> white); two roundings, covered by
+        // certify_band's 2u (M* + m) term
+        const float2 ngx = f2(-gx.x, -gx.y), ngy = f2(-gy.x, -gy.y);
+        dm[i][j] = __ffma2_rn(ngx, gx, __ffma2_rn(ngy, gy, splat(mlo)));
       }
       if (outr[i]) {
-        if (outl) {
-          const long long o = (long long)y * W + xl;
-          if (out0)
-            *reinterpret_cast<uint32_t*>(o0p + o) =
-                pack_white(dm[i][0].x, dm[i][1].x, dm[i][2].x, dm[i][3].x);
-          if (out1)
-            *reinterpret_cast<uint32_t*>(o0p + hw + o) =
-                pack_white(dm[i][0].y, dm[i][1].y, dm[i][2].y, dm[i][3].y);
-        }
+        if (st0)
+          *reinterpret_cast<uint32_t*>(o0p + orow[i]) =
+              pack_neg(dm[i][0].x, dm[i][1].x, dm[i][2].x, dm[i][3].x);
+        if (st1)
+          *reinterpret_cast<uint32_t*>(o1p + orow[i]) =
+              pack_neg(dm[i][0].y, dm[i][1].y, dm[i][2].y, dm[i][3].y);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           amin = fminf(amin, fminf(fabsf(dm[i][j].x), fabsf(dm[i][j].y)));
@@ -348,7 +347,7 @@ __device__ __forceinline__ void march(const CUtensorMap& tmap, const Args& a, in
       if (outr[i])
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          a.state_out[(long long)(by + r0 + i) * W + xl + j] = st[i][j];
+          a.state_out[(long long)(by + r0 + i) * W + xl + j] = sv[i][j].y;
 }
 
 __global__ void __launch_bounds__(NWMAX * 32, 1)
