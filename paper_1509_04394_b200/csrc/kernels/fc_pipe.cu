@@ -1,0 +1,820 @@
+// F12345 certified fast path, FRAME PIPELINE (the headline kernel).
+//
+// Same arithmetic contract as fc_fast.cu / fc_strip.cu (exact S1+S2,
+// certified packed-FP32 S3-S5, exact FP64 recheck inside the error band; see
+// fc_fast.cu's header and fccommon::certify_band).  What changes is the work
+// decomposition, built around the one serial dependency of the chain: only
+// the IIR (S2) carries state across frames; S3-S5 of different frames are
+// independent once the frame's IIR plane exists.  A CTA owns a spatial window
+// and runs three warp roles connected by mbarrier rings in shared memory:
+//
+//   producer warp   one lane streams the window's R, G, B planes of every
+//                   frame into an NSF-slot TMA ring (alpha never leaves HBM);
+//   IIR warps (NI)  each lane owns fixed cells of the window and keeps their
+//                   exact IIR state in registers for the whole march: gray +
+//                   IIR (exact) per frame, the IIR plane written into a
+//                   K-slot ring of IIR frames;
+//   stencil warps   warps 2f, 2f+1 take frames f, f+NF, ... from the IIR ring
+//   (2 NF)          (one 64-column half of the window each) and march the
+//                   frame's window rows top to bottom:
+//                   horizontal 5-tap pass, vertical 5-tap pass and Sobel all
+//                   in registers (sliding row windows), certified threshold,
+//                   mask bytes straight to HBM, exact rechecks read the
+//                   frame's exact IIR plane still held in the ring.
+//
+// Geometry.  Window = 128 columns (lane L owns columns 4L..4L+3) x R = 2 OH + 6
+// rows; outputs = the central 120 columns x 2 OH rows (halo: 3 rows and 4
+// columns each side for gaussian r=2 + Sobel r=1).  Every value is a float2
+// pairing window rows (p, p + OH): the top and bottom halves of the window run
+// in lock-step, so every stencil op and the IIR update is one FFMA2 / FADD2 /
+// FMUL2.  Pair-row p (0 <= p < OH + 6) of an IIR slot holds, for all 128
+// columns, the float2 {IIR(row p), IIR(row p + OH)}; a pair-row is 1 KB laid
+// out as 64 16-byte chunks (two columns each), even chunks first, odd chunks
+// second, so every warp-wide 16-byte access below touches 512 contiguous
+// bytes (conflict-free).
+//
+// Video borders (BORDER instantiation): window rows / 4-column groups outside
+// the video read the clamped RGB row / replicate the edge byte, so the IIR and
+// H values hold clamp-to-edge values (simulator.cpp:202-210); Sobel clamps its
+// G rows / columns at the first and last video row / column.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+#include <vector>
+
+#include "fc_common.cuh"
+
+// Warp-role counts (fc_pipe_cfg*.cu re-include this file with other values
+// under another namespace / entry name for tuning comparisons).
+#ifndef FP_NF
+#define FP_NF 5
+#define FP_NI 5
+#define FP_KSLACK 2
+#define FP_NAMESPACE fcpipe
+#define FP_ENTRY fc_chain_pipe
+#define FP_RECHECKS fc_pipe_recheck_count
+#endif
+
+namespace FP_NAMESPACE {
+
+using namespace fccommon;
+
+constexpr int NF = FP_NF;   // frames in flight in the stencil (two warps each)
+constexpr int NS = 2 * NF;  // stencil warps
+constexpr int NI = FP_NI;   // IIR warps
+constexpr int NWARP = NS + NI + 1;
+constexpr int NTHR = NWARP * 32;
+constexpr int K = NF + FP_KSLACK;  // IIR frame slots (slack: frames the IIR may run ahead)
+constexpr int NSF = 4;      // TMA RGB frame slots
+constexpr int SW = 120;     // output columns per strip (window 128 = SW + 8)
+constexpr int BWB = 144;    // TMA box row bytes: 128 + worst-case 16-B alignment slack
+constexpr int PROW = 1024;  // bytes per IIR pair-row
+constexpr int QC = 64;      // recheck queue records per stencil warp
+
+struct Args {
+  uint8_t* out;
+  int W, H, n_frames, n_warm;
+  int strips;
+  unsigned rgb_bytes, rgb_stride;  // TMA bytes per frame, RGB slot pitch
+  unsigned off_iir, iir_stride;    // IIR ring base, IIR slot pitch
+  unsigned off_bar, off_taps, off_queue;
+  const float* state_in;
+  float* state_out;
+  long long* dbg;  // optional per-CTA timing (FUSEPLAN_PIPE_PROFILE), 8 slots per CTA
+  FastParams p;
+};
+
+__device__ unsigned long long g_rechecks;
+extern __shared__ __align__(128) unsigned char fp_smem[];
+
+// mbarrier layout: rgb_full[NSF], rgb_empty[NSF], iir_full[K], iir_empty[K]
+__device__ __forceinline__ uint64_t* bar_rgb_full(const Args& a, int i) {
+  return reinterpret_cast<uint64_t*>(fp_smem + a.off_bar) + i;
+}
+__device__ __forceinline__ uint64_t* bar_rgb_empty(const Args& a, int i) {
+  return reinterpret_cast<uint64_t*>(fp_smem + a.off_bar) + NSF + i;
+}
+__device__ __forceinline__ uint64_t* bar_iir_full(const Args& a, int i) {
+  return reinterpret_cast<uint64_t*>(fp_smem + a.off_bar) + 2 * NSF + i;
+}
+__device__ __forceinline__ uint64_t* bar_iir_empty(const Args& a, int i) {
+  return reinterpret_cast<uint64_t*>(fp_smem + a.off_bar) + 2 * NSF + K + i;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Blocking wait: the suspend-time hint parks the warp in the barrier unit
+// instead of spinning through issue slots the working warps need.
+__device__ __forceinline__ void wait_phase(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(1000000u)
+      : "memory");
+}
+
+__device__ __forceinline__ long long clk() { return clock64(); }
+
+// Byte offset of chunk k (columns 2k, 2k+1; 16 bytes) inside a pair-row:
+// even chunks at positions 0..31, odd chunks at 32 + ((k >> 1) + 4) % 32.
+// IIR lanes store chunks 2L and 2L+1 (each store: 32 consecutive positions);
+// stencil lanes load chunks b + L (8 lanes per wavefront: 4 even + 4 odd
+// chunks, the rotation by 4 puts the two groups on disjoint banks).
+__device__ __forceinline__ unsigned chunk_off(int k) {
+  return unsigned((k & 1) ? 32 + (((k >> 1) + 4) & 31) : (k >> 1)) << 4;
+}
+
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(unsigned addr, float2 a, float2 b) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a.x), "f"(a.y),
+               "f"(b.x), "f"(b.y)
+               : "memory");
+}
+
+// 0xFF where nd < 0 for two values -> the low 16 bits (sign-replicate PRMT)
+__device__ __forceinline__ uint32_t pack_neg2(float a, float b) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x00FB;" : "=r"(r) : "r"(__float_as_uint(a)), "r"(__float_as_uint(b)));
+  return r;
+}
+
+__device__ __forceinline__ float2 shfl_up2(float2 v) {
+  return make_float2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ float2 shfl_down2(float2 v) {
+  return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1),
+                     __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+
+// ------------------------------------------------------------------ IIR warps
+
+template <int OH, bool BX, bool BY>
+__device__ __forceinline__ void iir_role(const Args& a, int iw, int lane, int bx, int by,
+                                         int xoff) {
+  constexpr int NP = OH + 6;               // pair-rows
+  constexpr int NR = (NP + NI - 1) / NI;   // pair-rows of this warp: p = iw + NI r
+  constexpr int R = 2 * OH + 6;
+  const int W = a.W, H = a.H, n = a.n_frames, n_warm = a.n_warm;
+  const int cplane = R * BWB;
+  const int xl = bx + 4 * lane;
+  const uint32_t k4b = a.p.k4b;
+  const float wr = a.p.wr, wg = a.p.wg, wb = a.p.wb;
+  const float wrm = a.p.wrm, wgm = a.p.wgm, wbm = a.p.wbm;
+
+  int rowx[NR], rowy[NR];  // RGB slot byte offsets of the two window rows
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int p = iw + NI * r;
+    const int rx = p, ry = p + OH;
+    rowx[r] = (BY ? clampi(by + rx, 0, H - 1) - by : rx) * BWB;
+    rowy[r] = (BY ? clampi(by + ry, 0, H - 1) - by : ry) * BWB;
+  }
+  int coloff = xoff + 4 * lane;
+  unsigned sel = 0x3210u;
+  if (BX && (xl < 0 || xl > W - 1)) {
+    const int edge = xl < 0 ? 0 : W - 1;
+    coloff = (edge & ~3) - bx + xoff;
+    sel = unsigned(edge & 3) * 0x1111u;
+  }
+  const unsigned so0 = chunk_off(2 * lane), so1 = chunk_off(2 * lane + 1);
+
+  // exact IIR state of the lane's cells: v[r][j] = {row p, row p + OH}, col 4L + j
+  float2 v[NR][4];
+  const bool fresh = a.state_in == nullptr;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int p = iw + NI * r;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (fresh || p >= NP) {
+        v[r][j] = make_float2(0.0f, 0.0f);
+      } else {
+        const int cx = clampi(xl + j, 0, W - 1);
+        v[r][j].x = a.state_in[(long long)clampi(by + p, 0, H - 1) * W + cx];
+        v[r][j].y = a.state_in[(long long)clampi(by + p + OH, 0, H - 1) * W + cx];
+      }
+    }
+  }
+
+  const unsigned smem0 = smem_u32(fp_smem);
+  int rslot = 0, islot = 0;
+  unsigned rpar = 0, ipar = 0;
+  long long w_rgb = 0, w_slot = 0;
+  const long long t_begin = clk();
+  for (int t = 0; t < n; ++t) {
+    if (a.dbg) {
+      const long long c0 = clk();
+      wait_phase(bar_rgb_full(a, rslot), rpar);
+      w_rgb += clk() - c0;
+    } else {
+      wait_phase(bar_rgb_full(a, rslot), rpar);
+    }
+    const unsigned char* f = fp_smem + rslot * a.rgb_stride;
+    auto body = [&](auto first_tag) {
+      constexpr bool FIRST = decltype(first_tag)::value;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        if (iw + NI * r >= NP) continue;
+        uint32_t wx[3], wy[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          wx[c] = *reinterpret_cast<const uint32_t*>(f + c * cplane + rowx[r] + coloff);
+          wy[c] = *reinterpret_cast<const uint32_t*>(f + c * cplane + rowy[r] + coloff);
+          if (BX) {
+            wx[c] = __byte_perm(wx[c], 0, sel);
+            wy[c] = __byte_perm(wy[c], 0, sel);
+          }
+        }
+#define FP_CELL(J)                                                                          \
+  {                                                                                         \
+    const float2 g = __fadd2_rn(                                                            \
+        __fadd2_rn(wprod(f2(magic_r<J>(wx[0], k4b), magic_r<J>(wy[0], k4b)), wr, wrm),      \
+                   wprod(f2(magic_r<J>(wx[1], k4b), magic_r<J>(wy[1], k4b)), wg, wgm)),     \
+        wprod(f2(magic_r<J>(wx[2], k4b), magic_r<J>(wy[2], k4b)), wb, wbm));                \
+    /* g = 0.5 gray exactly; IIR y = fl(0.5 x + fl(0.5 y)) == FMA(0.5, y, g) */            \
+    v[r][J] = FIRST ? __fadd2_rn(g, g) : __ffma2_rn(splat(0.5f), v[r][J], g);               \
+  }
+        FP_CELL(0) FP_CELL(1) FP_CELL(2) FP_CELL(3)
+#undef FP_CELL
+      }
+    };
+    if (t == 0 && fresh)
+      body(std::true_type{});
+    else
+      body(std::false_type{});
+    __syncwarp();  // the warp's RGB reads are done (values in registers)
+    if (lane == 0) mbar_arrive(bar_rgb_empty(a, rslot));
+    if (++rslot == NSF) {
+      rslot = 0;
+      rpar ^= 1u;
+    }
+    if (t < n_warm) continue;  // warm-up frame: state only
+    if (a.dbg) {
+      const long long c0 = clk();
+      wait_phase(bar_iir_empty(a, islot), ipar ^ 1u);
+      w_slot += clk() - c0;
+    } else {
+      wait_phase(bar_iir_empty(a, islot), ipar ^ 1u);
+    }
+    const unsigned base = smem0 + a.off_iir + islot * a.iir_stride;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int p = iw + NI * r;
+      if (p >= NP) continue;
+      sts128(base + p * PROW + so0, v[r][0], v[r][1]);
+      sts128(base + p * PROW + so1, v[r][2], v[r][3]);
+    }
+    __syncwarp();  // the warp's IIR stores precede the release arrive
+    if (lane == 0) mbar_arrive(bar_iir_full(a, islot));
+    if (++islot == K) {
+      islot = 0;
+      ipar ^= 1u;
+    }
+  }
+
+  if (a.dbg && lane == 0) {
+    long long* d = a.dbg + 8 * blockIdx.x;
+    atomicAdd(reinterpret_cast<unsigned long long*>(d + 3), (unsigned long long)w_rgb);
+    atomicAdd(reinterpret_cast<unsigned long long*>(d + 4), (unsigned long long)w_slot);
+    atomicAdd(reinterpret_cast<unsigned long long*>(d + 6), (unsigned long long)(clk() - t_begin));
+  }
+  if (a.state_out && lane >= 1 && lane <= 30 && xl < W) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int p = iw + NI * r;
+      if (p < 3 || p > OH + 2) continue;  // output rows of both halves
+      const int yx = by + p, yy = by + p + OH;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (yx < H) a.state_out[(long long)yx * W + xl + j] = v[r][j].x;
+        if (yy < H) a.state_out[(long long)yy * W + xl + j] = v[r][j].y;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ stencil warps
+
+// Exact IIR value of window cell (window row rho, col c) in the slot at `base`.
+template <int OH>
+__device__ __forceinline__ float iir_at(const unsigned char* base, int rho, int c, int half) {
+  const int p = rho - half * OH;
+  return *reinterpret_cast<const float*>(base + p * PROW + chunk_off(c >> 1) + (c & 1) * 8 +
+                                         half * 4);
+}
+
+// Exact reference threshold decision at video (x, y) whose window row lies in
+// half `half` (rows p + half OH): FP64 gaussian in dy/dx order at the 3x3
+// clamped centres, Sobel in the reference's float order, IEEE sqrt
+// (simulator.cpp:63-89).
+template <int OH>
+__device__ __noinline__ bool exact_white(const Args& a, const unsigned char* base,
+                                         const double* taps, int bx, int by, int x, int y,
+                                         int half) {
+  float g[3][3];
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < 3; ++i) {
+      const int cx = clampi(x + i - 1, 0, a.W - 1), cy = clampi(y + j - 1, 0, a.H - 1);
+      double acc = 0.0;
+      for (int dy = -2; dy <= 2; ++dy) {
+        const int ry = clampi(cy + dy, 0, a.H - 1) - by;
+        for (int dx = -2; dx <= 2; ++dx) {
+          const int rx = clampi(cx + dx, 0, a.W - 1) - bx;
+          acc = __fma_rn(taps[(dy + 2) * 5 + dx + 2], double(iir_at<OH>(base, ry, rx, half)),
+                         acc);
+        }
+      }
+      g[j][i] = __double2float_rn(acc);
+    }
+  auto s = [&](int dx, int dy) { return g[dy + 1][dx + 1]; };
+  const float gx =
+      __fsub_rn(__fadd_rn(__fadd_rn(s(1, -1), __fmul_rn(2.0f, s(1, 0))), s(1, 1)),
+                __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(-1, 0))), s(-1, 1)));
+  const float gy =
+      __fsub_rn(__fadd_rn(__fadd_rn(s(-1, 1), __fmul_rn(2.0f, s(0, 1))), s(1, 1)),
+                __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(0, -1))), s(1, -1)));
+  return __fsqrt_rn(__fadd_rn(__fmul_rn(gx, gx), __fmul_rn(gy, gy))) >= a.p.th_val;
+}
+
+template <int N>
+using ic = std::integral_constant<int, N>;
+
+// Stencil warps 2f + side: frames f, f + NF, ... of the IIR ring, side 0 the
+// window columns 2..65 (outputs 4..63), side 1 columns 62..125 (outputs
+// 64..123); lane L owns the column pair c = 2k, 2k + 1 with k = 1 + 30 side + L.
+// The march over the frame's pair-rows p = 0 .. OH + 5 is a loop of 5-step
+// bodies (the H and G row rings have period 5, so every ring index is a
+// compile-time constant and the code stays small for the instruction cache):
+//   step p: H row p (3 x 16-byte loads: chunks k-1, k, k+1);
+//           G row p - 2 (p >= 4); Sobel + threshold at pair-row p - 3 (p >= 6).
+// Uncertain values are queued in shared memory (record: pair-row, lane,
+// 4 value bits) and recomputed exactly after the march.
+template <int OH, bool BORDER>
+__device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, int bx, int by) {
+  constexpr int NP = OH + 6;
+  const int W = a.W, H = a.H;
+  const int n_out = a.n_frames - a.n_warm;
+  const long long hw = (long long)W * H;
+  const float h0 = a.p.h0, h1 = a.p.h1, h2 = a.p.h2;
+  const float mlo = a.p.mlo, band = a.p.band;
+  const double* taps = reinterpret_cast<const double*>(fp_smem + a.off_taps);
+  uint32_t* queue = reinterpret_cast<uint32_t*>(fp_smem + a.off_queue) + sw * QC;
+  const int f0 = sw >> 1, side = sw & 1;
+  const int k = 1 + 30 * side + lane;  // the lane's chunk
+  const int xl = bx + 2 * k;           // video column of the lane's first cell
+  const bool outl = lane >= 1 && lane <= 30 && xl < W;
+  const unsigned cl = chunk_off(k - 1), c0 = chunk_off(k), cr = chunk_off(k + 1);
+  const unsigned smem0 = smem_u32(fp_smem);
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  int slot = f0 % K;
+  unsigned par = (f0 / K) & 1u;
+  long long w_full = 0;
+  const long long t_begin = clk();
+  for (int u = f0; u < n_out; u += NF) {
+    if (a.dbg) {
+      const long long c0 = clk();
+      wait_phase(bar_iir_full(a, slot), par);
+      w_full += clk() - c0;
+    } else {
+      wait_phase(bar_iir_full(a, slot), par);
+    }
+    const unsigned base = smem0 + a.off_iir + slot * a.iir_stride;
+    unsigned char* o = a.out + (long long)u * hw;
+    unsigned char* ox = o + (long long)(by + 3) * W + xl;  // pair-row 3, top half
+    unsigned char* oy = ox + (long long)OH * W;              // bottom half
+    int nq = 0;                                              // queued records
+    float amin = __int_as_float(0x7f800000);                 // running min |nd|
+
+    float2 hr[5][2];  // H row r at ring index r % 5
+    float2 gr[5][2];  // G row r at ring index r % 5
+
+    auto step = [&](auto pm_t, auto v_t, auto s_t, int p) {
+      constexpr int PM = decltype(pm_t)::value;  // p % 5
+      constexpr bool DO_V = decltype(v_t)::value, DO_S = decltype(s_t)::value;
+      // ---- horizontal pass of pair-row p
+      {
+        const unsigned rb = base + p * PROW;
+        const float4 L4 = lds128(rb + cl), A4 = lds128(rb + c0), R4 = lds128(rb + cr);
+        const float2 m2 = lo2(L4), m1 = hi2(L4), v0 = lo2(A4), v1 = hi2(A4), q1 = lo2(R4),
+                     q2 = hi2(R4);
+        hr[PM][0] = tap5(m2, m1, v0, v1, q1, h0, h1, h2);
+        hr[PM][1] = tap5(m1, v0, v1, q1, q2, h0, h1, h2);
+      }
+      // ---- vertical pass: G row p - 2
+      if constexpr (DO_V) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          gr[(PM + 3) % 5][j] = tap5(hr[(PM + 1) % 5][j], hr[(PM + 2) % 5][j],
+                                     hr[(PM + 3) % 5][j], hr[(PM + 4) % 5][j], hr[PM][j], h0,
+                                     h1, h2);
+      }
+      // ---- Sobel + certified threshold at pair-row q = p - 3
+      if constexpr (DO_S) {
+        constexpr int QM = (PM + 2) % 5;  // q % 5
+        const int q = p - 3;
+        const int yx = by + q, yy = by + q + OH;  // video rows of the two halves
+        float2 s2[2], d2[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          float2 gm = gr[(QM + 4) % 5][j], gc = gr[QM][j], gp = gr[(QM + 1) % 5][j];
+          if (BORDER) {  // predicated selects: the step stays one basic block
+            if (yx == 0) gm.x = gc.x;
+            if (yy == 0) gm.y = gc.y;
+            if (yx == H - 1) gp.x = gc.x;
+            if (yy == H - 1) gp.y = gc.y;
+          }
+          s2[j] = __fadd2_rn(__ffma2_rn(splat(2.0f), gc, gm), gp);
+          d2[j] = __ffma2_rn(splat(-1.0f), gm, gp);
+        }
+        float2 sl = shfl_up2(s2[1]), dl = shfl_up2(d2[1]);
+        float2 sr = shfl_down2(s2[0]), dr = shfl_down2(d2[0]);
+        if (BORDER) {
+          if (xl == 0) sl = s2[0], dl = d2[0];
+          if (xl + 1 == W - 1) sr = s2[1], dr = d2[1];
+        }
+        const float2 S[4] = {sl, s2[0], s2[1], sr};
+        const float2 D[4] = {dl, d2[0], d2[1], dr};
+        float2 dm[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const float2 gx = __ffma2_rn(splat(-1.0f), S[j], S[j + 2]);
+          const float2 gy = __fadd2_rn(__ffma2_rn(splat(2.0f), D[j + 1], D[j]), D[j + 2]);
+          // nd = mlo - gy^2 - gx^2 (< 0 <=> white); certify_band's 2u (M* + m) term
+          const float2 ngx = f2(-gx.x, -gx.y), ngy = f2(-gy.x, -gy.y);
+          dm[j] = __ffma2_rn(ngx, gx, __ffma2_rn(ngy, gy, splat(mlo)));
+        }
+        const bool okx = outl && (!BORDER || yx < H);
+        const bool oky = outl && (!BORDER || yy < H);
+        if (okx) *reinterpret_cast<uint16_t*>(ox) = uint16_t(pack_neg2(dm[0].x, dm[1].x));
+        if (oky) *reinterpret_cast<uint16_t*>(oy) = uint16_t(pack_neg2(dm[0].y, dm[1].y));
+        ox += W;  // running row pointers
+        oy += W;
+        // running min of |nd| over the lane's output values (branch-free;
+        // checked once per 5-step body)
+        // (values of rows below the video only cause a harmless extra recheck)
+        amin = fminf(fminf(amin, fminf(fabsf(dm[0].x), fabsf(dm[0].y))),
+                     fminf(fabsf(dm[1].x), fabsf(dm[1].y)));
+      }
+    };
+    // After a body of steps whose Sobel rows are q0 .. q0 + nstep - 1: lanes
+    // whose running min fell inside the band queue those rows for the exact
+    // recheck (all four values of each row; rare)
+    auto flush = [&](int q0, int nstep) {
+      const bool amb = outl && amin <= band;
+      const unsigned ballot = __ballot_sync(0xffffffffu, amb);
+      if (ballot) {
+        if (amb) {
+          const int i = nq + __popc(ballot & lt_mask);
+          if (i < QC) queue[i] = (unsigned(q0) << 16) | (lane << 8) | unsigned(nstep);
+        }
+        nq += __popc(ballot);  // nq > QC: overflow, handled after the march
+        amin = __int_as_float(0x7f800000);
+      }
+    };
+
+    const auto F = std::false_type{};
+    const auto T = std::true_type{};
+    step(ic<0>{}, F, F, 0);
+    step(ic<1>{}, F, F, 1);
+    step(ic<2>{}, F, F, 2);
+    step(ic<3>{}, F, F, 3);
+    step(ic<4>{}, T, F, 4);
+    step(ic<0>{}, T, F, 5);
+#pragma unroll 1
+    for (int p = 6; p + 5 <= NP; p += 5) {  // p % 5 == 1 at the top
+      step(ic<1>{}, T, T, p);
+      step(ic<2>{}, T, T, p + 1);
+      step(ic<3>{}, T, T, p + 2);
+      step(ic<4>{}, T, T, p + 3);
+      step(ic<0>{}, T, T, p + 4);
+      flush(p - 3, 5);
+    }
+    constexpr int PE = NP - (OH % 5);  // epilogue: pair-rows PE .. NP - 1
+    if constexpr (OH % 5 >= 1) step(ic<1>{}, T, T, PE);
+    if constexpr (OH % 5 >= 2) step(ic<2>{}, T, T, PE + 1);
+    if constexpr (OH % 5 >= 3) step(ic<3>{}, T, T, PE + 2);
+    if constexpr (OH % 5 >= 4) step(ic<4>{}, T, T, PE + 3);
+    if constexpr (OH % 5 >= 1) flush(PE - 3, OH % 5);
+
+    // ---- exact recheck of the queued uncertain values (rare)
+    if (nq > QC) {
+      // queue overflow (adversarial input: many values inside the band): the
+      // exact decision for every output pixel of this warp's half-window
+      __syncwarp();
+      const unsigned char* sb = fp_smem + (base - smem0);
+      if (outl)
+        for (int q = 3; q <= OH + 2; ++q)
+          for (int half = 0; half < 2; ++half) {
+            const int y = by + q + half * OH;
+            if (y >= H) continue;
+            for (int j = 0; j < 2; ++j)
+              o[(long long)y * W + xl + j] =
+                  exact_white<OH>(a, sb, taps, bx, by, xl + j, y, half) ? 0xFF : 0x00;
+          }
+      if (lane == 0) atomicAdd(&g_rechecks, (unsigned long long)(60 * 4 * OH));
+      __syncwarp();
+    } else if (nq) {
+      __syncwarp();  // queue records and the warp's mask stores are visible
+      const unsigned char* sb = fp_smem + (base - smem0);
+      unsigned cnt = 0;
+      // work items: record r, row q0 + s, half h, column j -> one exact
+      // decision each, spread over the lanes (latency ~ items / 32 calls)
+      const int items = nq * 20;
+      for (int it = lane; it < items; it += 32) {
+        const uint32_t rec = queue[it / 20];
+        const int e = it % 20, st = e >> 2, half = (e >> 1) & 1, j = e & 1;
+        const int q0 = int(rec >> 16), L = int((rec >> 8) & 31), nstep = int(rec & 0xFFu);
+        if (st >= nstep) continue;
+        const int x = bx + 2 * (1 + 30 * side + L) + j;
+        const int y = by + q0 + st + half * OH;
+        if (y >= H) continue;
+        o[(long long)y * W + x] = exact_white<OH>(a, sb, taps, bx, by, x, y, half) ? 0xFF : 0x00;
+        ++cnt;
+      }
+      for (int k2 = 16; k2 > 0; k2 >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, k2);
+      if (lane == 0) atomicAdd(&g_rechecks, (unsigned long long)cnt);
+      __syncwarp();  // queue reads done before the next frame reuses it
+    }
+    __syncwarp();  // the warp's slot reads (and rechecks) are done
+    if (lane == 0) mbar_arrive(bar_iir_empty(a, slot));
+    slot += NF;
+    if (slot >= K) {
+      slot -= K;
+      par ^= 1u;
+    }
+  }
+  if (a.dbg && lane == 0) {
+    long long* d = a.dbg + 8 * blockIdx.x;
+    atomicAdd(reinterpret_cast<unsigned long long*>(d + 2), (unsigned long long)w_full);
+    atomicAdd(reinterpret_cast<unsigned long long*>(d + 5), (unsigned long long)(clk() - t_begin));
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    atomicMax(reinterpret_cast<unsigned long long*>(d + 1), now);
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+
+__device__ __forceinline__ long long interior_flag(const Args& a, int bx, int by, int R) {
+  return (bx >= 0 && bx + 127 <= a.W - 1 ? 1 : 0) + (by >= 0 && by + R - 1 <= a.H - 1 ? 2 : 0);
+}
+
+template <int OH>
+__global__ void __launch_bounds__(NTHR, 1)
+    k_chain_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
+  constexpr int R = 2 * OH + 6;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int strip = blockIdx.x % a.strips, band = blockIdx.x / a.strips;
+  const int x0 = strip * SW, y0 = band * (2 * OH);
+  const int bx = x0 - 4, by = y0 - 3;
+  const int tx0 = bx >= 0 ? (bx & ~15) : -((-bx + 15) & ~15);
+  double* taps = reinterpret_cast<double*>(fp_smem + a.off_taps);
+  if (tid == 0) {
+    for (int i = 0; i < NSF; ++i) {
+      mbar_init(bar_rgb_full(a, i), 1);
+      mbar_init(bar_rgb_empty(a, i), NI);  // one arrive per IIR warp
+    }
+    for (int i = 0; i < K; ++i) {
+      mbar_init(bar_iir_full(a, i), NI);
+      mbar_init(bar_iir_empty(a, i), 2);  // the frame's two stencil warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < 25) taps[tid] = double(a.p.taps[tid]);
+  if (a.dbg && tid == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    a.dbg[8 * blockIdx.x] = (long long)now;
+    a.dbg[8 * blockIdx.x + 7] = (interior_flag(a, bx, by, 2 * OH + 6));
+  }
+  __syncthreads();  // the only CTA-wide barrier: roles run decoupled from here
+
+  const bool in_x = bx >= 0 && bx + 127 <= a.W - 1, in_y = by >= 0 && by + R - 1 <= a.H - 1;
+  const bool interior = in_x && in_y;
+  if (warp < NS) {
+    if (interior)
+      stencil_role<OH, false>(a, warp, lane, bx, by);
+    else
+      stencil_role<OH, true>(a, warp, lane, bx, by);
+  } else if (warp < NS + NI) {
+    const int iw = warp - NS, xoff = bx - tx0;
+    if (interior)
+      iir_role<OH, false, false>(a, iw, lane, bx, by, xoff);
+    else if (in_x)
+      iir_role<OH, false, true>(a, iw, lane, bx, by, xoff);
+    else if (in_y)
+      iir_role<OH, true, false>(a, iw, lane, bx, by, xoff);
+    else
+      iir_role<OH, true, true>(a, iw, lane, bx, by, xoff);
+  } else if (lane == 0) {
+    // producer: frame t -> RGB slot t % NSF once the IIR warps released it
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+    int slot = 0;
+    unsigned par = 0;
+    for (int t = 0; t < a.n_frames; ++t) {
+      wait_phase(bar_rgb_empty(a, slot), par ^ 1u);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar_rgb_full(a, slot), a.rgb_bytes);
+      tma_load_3d(fp_smem + slot * a.rgb_stride, &tmap, bar_rgb_full(a, slot), tx0, by, 4 * t);
+      if (++slot == NSF) {
+        slot = 0;
+        par ^= 1u;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host
+
+size_t layout(int oh, Args* a) {
+  const int R = 2 * oh + 6;
+  const size_t rgb = size_t(3) * R * BWB, rgb_stride = (rgb + 127) / 128 * 128;
+  size_t off = NSF * rgb_stride;
+  const size_t off_iir = off;
+  const size_t iir_stride = size_t(oh + 6) * PROW;
+  off += K * iir_stride;
+  const size_t off_bar = off;
+  off += (2 * NSF + 2 * K) * 8;
+  const size_t off_taps = (off + 7) / 8 * 8;
+  off = off_taps + 25 * 8;
+  const size_t off_queue = off;  // per stencil warp: QC records
+  off += size_t(NS) * QC * 4;
+  if (a) {
+    a->off_queue = unsigned(off_queue);
+    a->rgb_bytes = unsigned(rgb);
+    a->rgb_stride = unsigned(rgb_stride);
+    a->off_iir = unsigned(off_iir);
+    a->iir_stride = unsigned(iir_stride);
+    a->off_bar = unsigned(off_bar);
+    a->off_taps = unsigned(off_taps);
+  }
+  return off;
+}
+
+using KernelFn = void (*)(CUtensorMap, Args);
+
+#define FP_OH_LIST(X) X(3) X(4) X(5) X(8) X(10) X(12) X(15)
+
+KernelFn kernel_for(int oh) {
+  switch (oh) {
+#define FP_CASE(N) \
+  case N:          \
+    return k_chain_pipe<N>;
+    FP_OH_LIST(FP_CASE)
+#undef FP_CASE
+  }
+  return nullptr;
+}
+
+struct PipePlan {
+  int W = -1, H = -1, dev = -1;
+  int oh = 0, strips = 0, bands = 0;
+  size_t smem = 0;
+};
+
+// Every CTA marches the whole video; an SM's time is ~ (CTAs it runs) x (its
+// CTA's pair-rows).  Pick OH minimising the busiest SM's pair-rows; ties go to
+// the larger window (less halo).  FUSEPLAN_PIPE_OH forces the choice.
+bool choose(int W, int H, int dev, PipePlan* pp) {
+  int sms = 0, optin = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int force = 0;
+  if (const char* env = std::getenv("FUSEPLAN_PIPE_OH")) force = std::atoi(env);
+  const int strips = (W + SW - 1) / SW;
+  double best = 1e300;
+  const int ohs[] = {
+#define FP_ITEM(N) N,
+      FP_OH_LIST(FP_ITEM)
+#undef FP_ITEM
+  };
+  const bool dbg = std::getenv("FUSEPLAN_DEBUG") != nullptr;
+  for (int oh : ohs) {
+    if (force && oh != force) continue;
+    const size_t smem = layout(oh, nullptr);
+    if (smem > size_t(optin)) continue;
+    KernelFn fn = kernel_for(oh);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    int per_sm = 0;
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHR, smem);
+    if (dbg)
+      std::fprintf(stderr, "fc_pipe choose: oh=%d smem=%zu optin=%d err=%s per_sm=%d\n", oh,
+                   smem, optin, cudaGetErrorString(e), per_sm);
+    if (e != cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    const long long bands = (H + 2 * oh - 1) / (2 * oh);
+    const long long ctas = strips * bands;
+    const long long per_busiest = (ctas + sms - 1) / sms;
+    const double cost = double(per_busiest) * (oh + 6) - 1e-3 * oh;
+    if (cost < best) {
+      best = cost;
+      pp->oh = oh;
+      pp->strips = strips;
+      pp->bands = int(bands);
+      pp->smem = smem;
+    }
+  }
+  return best < 1e300;
+}
+
+}  // namespace FP_NAMESPACE
+
+using namespace FP_NAMESPACE;
+
+extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                             const fc_stage* sthr, const void* video, int in_type, int gray_in,
+                             void* out, int out_type, fc_dims d, int n_warm,
+                             const float* state_in, float* state_out, void* stream) {
+  FastParams fp;
+  if (!fast_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d, &fp)) return -1;
+  if (d.frames == 0) return 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static thread_local PipePlan cache;
+  if (cache.W != d.width || cache.H != d.height || cache.dev != dev) {
+    PipePlan pp;
+    if (!choose(d.width, d.height, dev, &pp)) return -1;
+    pp.W = d.width;
+    pp.H = d.height;
+    pp.dev = dev;
+    cache = pp;
+  }
+  Args a;
+  std::memset(&a, 0, sizeof a);
+  layout(cache.oh, &a);
+  a.out = static_cast<uint8_t*>(out);
+  a.W = d.width;
+  a.H = d.height;
+  a.n_frames = d.frames;
+  a.n_warm = n_warm;
+  a.strips = cache.strips;
+  a.state_in = state_in;
+  a.state_out = state_out;
+  a.p = fp;
+  CUtensorMap map;
+  if (!rgb_tensor_map(&map, video, d, BWB, 2 * cache.oh + 6)) return -1;
+  const int grid = cache.strips * cache.bands;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool profile = std::getenv("FUSEPLAN_PIPE_PROFILE") != nullptr;
+  if (profile) {
+    cudaMalloc(&a.dbg, sizeof(long long) * 8 * grid);
+    cudaMemsetAsync(a.dbg, 0, sizeof(long long) * 8 * grid, st);
+  }
+  kernel_for(cache.oh)<<<grid, NTHR, cache.smem, st>>>(map, a);
+  const int rc = int(cudaGetLastError());
+  if (profile && a.dbg) {  // per-CTA span and per-role wait shares
+    std::vector<long long> h(size_t(8) * grid);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), a.dbg, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaFree(a.dbg);
+    long long t0 = h[0], t1 = 0;
+    for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[size_t(b) * 8]);
+    double cls[4][6] = {};
+    for (int b = 0; b < grid; ++b) {
+      const long long* r = &h[size_t(b) * 8];
+      t1 = std::max(t1, r[1]);
+      double* c = cls[r[7] & 3];
+      c[0] += 1;
+      c[1] += double(r[1] - r[0]) / 1e3;
+      c[2] += double(r[2]) / double(r[5]);  // stencil wait share
+      c[3] += double(r[3]) / double(r[6]);  // IIR rgb wait share
+      c[4] += double(r[4]) / double(r[6]);  // IIR slot wait share
+      c[5] = std::max(c[5], double(r[1] - r[0]) / 1e3);
+    }
+    std::fprintf(stderr, "fc_pipe oh=%d grid=%d NF=%d NI=%d K=%d: kernel span %.1f us\n",
+                 cache.oh, grid, NF, NI, K, double(t1 - t0) / 1e3);
+    const char* names[4] = {"corner", "x-interior", "y-interior", "interior"};
+    for (int k = 0; k < 4; ++k)
+      if (cls[k][0] > 0)
+        std::fprintf(stderr,
+                     "  %-10s ctas %3.0f  span avg %.1f max %.1f us  stencil wait %.2f  "
+                     "iir wait rgb %.2f slot %.2f\n",
+                     names[k], cls[k][0], cls[k][1] / cls[k][0], cls[k][5],
+                     cls[k][2] / cls[k][0], cls[k][3] / cls[k][0], cls[k][4] / cls[k][0]);
+  }
+  return rc;
+}
+
+extern "C" long long FP_RECHECKS(void) {
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_rechecks, sizeof v) != cudaSuccess) return -1;
+  return (long long)v;
+}

@@ -1,0 +1,9 @@
+// Tuning variant of the frame pipeline: 6 frames in flight (12 stencil
+// warps), 3 IIR warps, 1 slack IIR slot.  FUSEPLAN_PIPE_CFG=63 selects it.
+#define FP_NF 6
+#define FP_NI 3
+#define FP_KSLACK 1
+#define FP_NAMESPACE fcpipe63
+#define FP_ENTRY fc_chain_pipe63
+#define FP_RECHECKS fc_pipe63_recheck_count
+#include "fc_pipe.cu"
