@@ -123,6 +123,10 @@ struct FastParams {
   float mstar, band, th_val;
   float mlo;        // largest float below M*: white <=> m > mlo <=> mlo - m < 0
   uint32_t k4b;     // 0x4B000000 (see magic_r)
+  // Centre-normalised taps (fc_pipe.cu): g0 = h0 / h2, g1 = h1 / h2, centre 1,
+  // so a 5-tap pass is 4 packed ops; G, gx, gy come out scaled by S = 1 / h2^2
+  // and m by S^2.  mlo_n ~ S^2 M*, band_n: the certified band in that domain.
+  float g0, g1, mlo_n, band_n;
 };
 
 // Certified error band on m = gx^2 + gy^2 (u = 2^-24, all stencil inputs >= 0):
@@ -146,6 +150,23 @@ inline float certify_band(float mstar, double gmax, double dw) {
     B = 4.0 * E * std::sqrt(double(mstar) + B) + 2.0 * E * E + 4.1 * u * (double(mstar) + B) +
         2.0 * u * (2.0 * double(mstar) + B);
   return float(2.0 * B + 1e-3);
+}
+
+// The same certification in the scaled domain of the centre-normalised taps:
+// gx, gy scaled by S, m by S^2, threshold T = S^2 M* represented by the float
+// mlo_n (|mlo_n - T| enters the band).  dw is measured against S x the
+// reference taps; a normalised pass has at most 3 roundings per term (< the 4
+// the 8.1u term allows).
+inline float certify_band_scaled(double T, float mlo_n, double gmax_s, double dw) {
+  const double u = std::ldexp(1.0, -24);
+  double kappa = 8.1 * u + dw + u + 25.0 * std::ldexp(1.0, -53);
+  double E = (kappa + 6.1 * u) * 8.0 * gmax_s;
+  const double dT = std::fabs(double(mlo_n) - T);
+  double B = 1.0;
+  for (int it = 0; it < 60; ++it)
+    B = 4.0 * E * std::sqrt(T + B) + 2.0 * E * E + 4.1 * u * (T + B) + 2.0 * u * (2.0 * T + B) +
+        dT;
+  return float(2.0 * B * (1.0 + 1e-6) + 1e-3 * T / 16384.0);
 }
 
 // Coverage of the certified path + its parameters.  Returns false when the
@@ -198,6 +219,21 @@ inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stag
   double tap_sum = 0.0;
   for (int k = 0; k < 25; ++k) tap_sum += sg->g_w[k];
   p->band = certify_band(p->mstar, gray_max * tap_sum * 1.001, dw);
+  // centre-normalised taps and their certification (scaled domain)
+  const double S = 1.0 / (e[2] / es * (e[2] / es));
+  p->g0 = float((e[0] / es) / (e[2] / es));
+  p->g1 = float((e[1] / es) / (e[2] / es));
+  const double gg[5] = {p->g0, p->g1, 1.0, p->g1, p->g0};
+  double dwn = 0.0;
+  for (int j = 0; j < 5; ++j)
+    for (int i = 0; i < 5; ++i) {
+      const double ref = S * double(sg->g_w[j * 5 + i]);
+      dwn = std::max(dwn, std::fabs(gg[j] * gg[i] - ref) / ref);
+    }
+  if (!(dwn < 1e-5)) return false;
+  const double T = S * S * double(p->mstar);
+  p->mlo_n = float(T);
+  p->band_n = certify_band_scaled(T, p->mlo_n, S * gray_max * tap_sum * 1.001, dwn);
   return true;
 }
 

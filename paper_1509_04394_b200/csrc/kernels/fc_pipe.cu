@@ -82,6 +82,7 @@ struct Args {
   const float* state_in;
   float* state_out;
   long long* dbg;  // optional per-CTA timing (FUSEPLAN_PIPE_PROFILE), 8 slots per CTA
+  int skip;        // timing experiments only (FUSEPLAN_PIPE_SKIP): 1 IIR math, 2 stencil math
   FastParams p;
 };
 
@@ -142,6 +143,13 @@ __device__ __forceinline__ void sts128(unsigned addr, float2 a, float2 b) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a.x), "f"(a.y),
                "f"(b.x), "f"(b.y)
                : "memory");
+}
+
+// Centre-normalised 5-tap pass (centre tap 1): 4 packed ops, at most 3
+// roundings per term (certify_band_scaled).
+__device__ __forceinline__ float2 tap4n(float2 a, float2 b, float2 c, float2 d, float2 e,
+                                        float g0, float g1) {
+  return __ffma2_rn(splat(g1), __fadd2_rn(b, d), __ffma2_rn(splat(g0), __fadd2_rn(a, e), c));
 }
 
 // 0xFF where nd < 0 for two values -> the low 16 bits (sign-replicate PRMT)
@@ -251,7 +259,8 @@ __device__ __forceinline__ void iir_role(const Args& a, int iw, int lane, int bx
 #undef FP_CELL
       }
     };
-    if (t == 0 && fresh)
+    if (a.skip & 1) {
+    } else if (t == 0 && fresh)
       body(std::true_type{});
     else
       body(std::false_type{});
@@ -368,8 +377,8 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
   const int W = a.W, H = a.H;
   const int n_out = a.n_frames - a.n_warm;
   const long long hw = (long long)W * H;
-  const float h0 = a.p.h0, h1 = a.p.h1, h2 = a.p.h2;
-  const float mlo = a.p.mlo, band = a.p.band;
+  const float mlo = a.p.mlo_n, band = a.p.band_n;  // scaled domain (normalised taps)
+  const float g0 = a.p.g0, g1 = a.p.g1;
   const double* taps = reinterpret_cast<const double*>(fp_smem + a.off_taps);
   uint32_t* queue = reinterpret_cast<uint32_t*>(fp_smem + a.off_queue) + sw * QC;
   const int f0 = sw >> 1, side = sw & 1;
@@ -399,38 +408,43 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
     int nq = 0;                                              // queued records
     float amin = __int_as_float(0x7f800000);                 // running min |nd|
 
-    float2 hr[5][2];  // H row r at ring index r % 5
-    float2 gr[5][2];  // G row r at ring index r % 5
+    float2 hr[6][2];  // H row r at ring index r % 6
+    float2 gr[6][2];  // G row r at ring index r % 6
 
-    auto step = [&](auto pm_t, auto v_t, auto s_t, int p) {
-      constexpr int PM = decltype(pm_t)::value;  // p % 5
-      constexpr bool DO_V = decltype(v_t)::value, DO_S = decltype(s_t)::value;
+    // Step p of the skewed march: H row p, G row p - 3 (from H rows p-5..p-1)
+    // and Sobel at pair-row p - 5 (G rows p-6..p-4) are mutually
+    // independent, so the scheduler overlaps the loads and the three
+    // dependency chains of a step.
+    auto step = [&](auto pm_t, auto h_t, auto v_t, auto s_t, int p) {
+      constexpr int PM = decltype(pm_t)::value;  // p % 6
+      constexpr bool DO_H = decltype(h_t)::value, DO_V = decltype(v_t)::value;
+      constexpr bool DO_S = decltype(s_t)::value;
       // ---- horizontal pass of pair-row p
-      {
+      if constexpr (DO_H) {
         const unsigned rb = base + p * PROW;
         const float4 L4 = lds128(rb + cl), A4 = lds128(rb + c0), R4 = lds128(rb + cr);
         const float2 m2 = lo2(L4), m1 = hi2(L4), v0 = lo2(A4), v1 = hi2(A4), q1 = lo2(R4),
                      q2 = hi2(R4);
-        hr[PM][0] = tap5(m2, m1, v0, v1, q1, h0, h1, h2);
-        hr[PM][1] = tap5(m1, v0, v1, q1, q2, h0, h1, h2);
+        hr[PM][0] = tap4n(m2, m1, v0, v1, q1, g0, g1);
+        hr[PM][1] = tap4n(m1, v0, v1, q1, q2, g0, g1);
       }
-      // ---- vertical pass: G row p - 2
+      // ---- vertical pass: G row p - 3
       if constexpr (DO_V) {
 #pragma unroll
         for (int j = 0; j < 2; ++j)
-          gr[(PM + 3) % 5][j] = tap5(hr[(PM + 1) % 5][j], hr[(PM + 2) % 5][j],
-                                     hr[(PM + 3) % 5][j], hr[(PM + 4) % 5][j], hr[PM][j], h0,
-                                     h1, h2);
+          gr[(PM + 3) % 6][j] = tap4n(hr[(PM + 1) % 6][j], hr[(PM + 2) % 6][j],
+                                      hr[(PM + 3) % 6][j], hr[(PM + 4) % 6][j],
+                                      hr[(PM + 5) % 6][j], g0, g1);
       }
-      // ---- Sobel + certified threshold at pair-row q = p - 3
+      // ---- Sobel + certified threshold at pair-row q = p - 5 (G rows q-1..q+1)
       if constexpr (DO_S) {
-        constexpr int QM = (PM + 2) % 5;  // q % 5
-        const int q = p - 3;
+        constexpr int QM = (PM + 1) % 6;  // q % 6
+        const int q = p - 5;
         const int yx = by + q, yy = by + q + OH;  // video rows of the two halves
         float2 s2[2], d2[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          float2 gm = gr[(QM + 4) % 5][j], gc = gr[QM][j], gp = gr[(QM + 1) % 5][j];
+          float2 gm = gr[(QM + 5) % 6][j], gc = gr[QM][j], gp = gr[(QM + 1) % 6][j];
           if (BORDER) {  // predicated selects: the step stays one basic block
             if (yx == 0) gm.x = gc.x;
             if (yy == 0) gm.y = gc.y;
@@ -464,8 +478,8 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
         ox += W;  // running row pointers
         oy += W;
         // running min of |nd| over the lane's output values (branch-free;
-        // checked once per 5-step body)
-        // (values of rows below the video only cause a harmless extra recheck)
+        // checked once per 6-step body; values of rows below the video only
+        // cause a harmless extra recheck)
         amin = fminf(fminf(amin, fminf(fabsf(dm[0].x), fabsf(dm[0].y))),
                      fminf(fabsf(dm[1].x), fabsf(dm[1].y)));
       }
@@ -488,27 +502,37 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
 
     const auto F = std::false_type{};
     const auto T = std::true_type{};
-    step(ic<0>{}, F, F, 0);
-    step(ic<1>{}, F, F, 1);
-    step(ic<2>{}, F, F, 2);
-    step(ic<3>{}, F, F, 3);
-    step(ic<4>{}, T, F, 4);
-    step(ic<0>{}, T, F, 5);
+    if (!(a.skip & 2)) {
+    // Steps p = 0 .. NP + 1: H while p < NP, V for 5 <= p <= NP, Sobel for
+    // 8 <= p <= NP + 1.  Prologue p < 8, a rolled loop of 6-step bodies,
+    // then a compile-time tail.
+    step(ic<0>{}, T, F, F, 0);
+    step(ic<1>{}, T, F, F, 1);
+    step(ic<2>{}, T, F, F, 2);
+    step(ic<3>{}, T, F, F, 3);
+    step(ic<4>{}, T, F, F, 4);
+    step(ic<5>{}, T, T, F, 5);
+    step(ic<0>{}, T, T, F, 6);
+    step(ic<1>{}, T, T, F, 7);
 #pragma unroll 1
-    for (int p = 6; p + 5 <= NP; p += 5) {  // p % 5 == 1 at the top
-      step(ic<1>{}, T, T, p);
-      step(ic<2>{}, T, T, p + 1);
-      step(ic<3>{}, T, T, p + 2);
-      step(ic<4>{}, T, T, p + 3);
-      step(ic<0>{}, T, T, p + 4);
-      flush(p - 3, 5);
+    for (int p = 8; p + 6 <= NP; p += 6) {  // p % 6 == 2 at the top
+      step(ic<2>{}, T, T, T, p);
+      step(ic<3>{}, T, T, T, p + 1);
+      step(ic<4>{}, T, T, T, p + 2);
+      step(ic<5>{}, T, T, T, p + 3);
+      step(ic<0>{}, T, T, T, p + 4);
+      step(ic<1>{}, T, T, T, p + 5);
+      flush(p - 5, 6);
     }
-    constexpr int PE = NP - (OH % 5);  // epilogue: pair-rows PE .. NP - 1
-    if constexpr (OH % 5 >= 1) step(ic<1>{}, T, T, PE);
-    if constexpr (OH % 5 >= 2) step(ic<2>{}, T, T, PE + 1);
-    if constexpr (OH % 5 >= 3) step(ic<3>{}, T, T, PE + 2);
-    if constexpr (OH % 5 >= 4) step(ic<4>{}, T, T, PE + 3);
-    if constexpr (OH % 5 >= 1) flush(PE - 3, OH % 5);
+    constexpr int PT = 8 + 6 * ((NP - 8) / 6);  // tail: full steps PT .. NP - 1
+    if constexpr (NP - PT >= 1) step(ic<2>{}, T, T, T, PT);
+    if constexpr (NP - PT >= 2) step(ic<3>{}, T, T, T, PT + 1);
+    if constexpr (NP - PT >= 3) step(ic<4>{}, T, T, T, PT + 2);
+    if constexpr (NP - PT >= 4) step(ic<5>{}, T, T, T, PT + 3);
+    if constexpr (NP - PT >= 5) step(ic<0>{}, T, T, T, PT + 4);
+    step(ic<NP % 6>{}, F, T, T, NP);
+    step(ic<(NP + 1) % 6>{}, F, F, T, NP + 1);
+    flush(PT - 5, NP + 2 - PT);
 
     // ---- exact recheck of the queued uncertain values (rare)
     if (nq > QC) {
@@ -548,6 +572,7 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
       for (int k2 = 16; k2 > 0; k2 >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, k2);
       if (lane == 0) atomicAdd(&g_rechecks, (unsigned long long)cnt);
       __syncwarp();  // queue reads done before the next frame reuses it
+    }
     }
     __syncwarp();  // the warp's slot reads (and rechecks) are done
     if (lane == 0) mbar_arrive(bar_iir_empty(a, slot));
@@ -769,6 +794,7 @@ extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stag
   a.state_in = state_in;
   a.state_out = state_out;
   a.p = fp;
+  if (const char* e = std::getenv("FUSEPLAN_PIPE_SKIP")) a.skip = std::atoi(e);
   CUtensorMap map;
   if (!rgb_tensor_map(&map, video, d, BWB, 2 * cache.oh + 6)) return -1;
   const int grid = cache.strips * cache.bands;
