@@ -19,7 +19,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -50,54 +49,72 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock + throttle reasons sampled with NVML every 2 ms from a thread
+    while the timed region runs (the B200_PROFILING recipe's clocks line)."""
+
+    REASONS = {  # nvmlClocksEventReason* bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown",
+    }
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
-        self.proc = None
+        self.sm_max = None
+        self._stop = threading.Event()
+        self.thread = None
+        self.err = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "25"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.sm_max = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((sm, rs))
+                    except Exception as e:  # keep sampling; remember why
+                        self.err = str(e)
+                    self._stop.wait(0.002)
+
+            self.thread = threading.Thread(target=run, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:
+            self.err = str(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [s.strip() for s in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.thread:
+            self.thread.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
-                 "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if r[4 + i].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.sm_max, "reasons": ["unsampled"],
+                    "error": self.err}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, rs in self.rows for bit, name in self.REASONS.items()
+                          if rs & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.sm_max,
+                "sm_min_mhz": float(min(sm)), "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_traffic(workload):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture of this workload (profiles/traffic.json, written by
+    scripts/traffic_from_ncu.py), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            j = json.load(fh)
+        e = j.get(workload)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
 
 
 def cpu_reference_rate(W, H, sample_frames, seed=1234):
@@ -243,7 +260,6 @@ def main():
         # verify, fix-up re-run on mismatch (paper_1509_04394_b200/sharding.py)
         run_sharded(shard, run_shard, send, recv, torch.equal, events)
 
-    clocks = ClockSampler(local).__enter__()  # sampling spans warm-up + timed steps
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -254,12 +270,13 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        clocks = ClockSampler(local).__enter__()  # samples during the timed steps
         start.record(stream)
         for _ in range(args.steps):
             step()
         end.record(stream)
         torch.cuda.synchronize()
-    clocks.__exit__(None, None, None)
+        clocks.__exit__(None, None, None)
     ms = start.elapsed_time(end) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -308,7 +325,8 @@ def main():
     if k_ms is not None:
         achieved = alg_bytes / (k_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                "frac": achieved / peak, "traffic": measured_traffic(desc),
+                "peak_kind": peak_kind,
                 "kernel_ms": k_ms, "alg_bytes_per_launch": alg_bytes}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
