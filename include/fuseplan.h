@@ -48,7 +48,13 @@ void fp_device_free(fp_device* d);
 /* ---- planning: fuseplan.h:39-50 / capi.cpp:219-234 ----------------------
  * options_json (may be NULL): {"halo_mode": "cumulative"|"paper-max",
  *   "transfer_variant": "exact"|"paper", "force_partition": "1-2,3-5",
- *   "tile": {"x": 32, "y": 32, "t": 4}} */
+ *   "tile": {"x": 32, "y": 32, "t": 4},
+ *   "iir_streaming": false}
+ * iir_streaming (B200 extension, default false = the reference's planner):
+ * the device executor streams a group containing the causal IIR frame by
+ * frame, so the planner need not pin that group's tile to t = F (the
+ * reference's rule, planner.cpp:73); long videos (e.g. 800x600x16000, which
+ * the reference reports infeasible) then plan normally. */
 fp_status fp_plan_create(const fp_pipeline* p, const fp_device* d,
                          const char* options_json, fp_plan** out);
 void fp_plan_free(fp_plan* plan);

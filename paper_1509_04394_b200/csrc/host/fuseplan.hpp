@@ -266,6 +266,12 @@ struct PlanOptions {
   TransferVariant transfer_variant = TransferVariant::ExactVolume;
   std::optional<std::vector<std::pair<int, int>>> forced_partition;
   std::optional<TileShape> forced_tile;
+  // B200 extension (not in the reference; default = reference semantics):
+  // the GPU executor streams recurrence groups frame by frame with the IIR
+  // state in registers / a carry plane, so a group containing the IIR need not
+  // hold the whole time extent in shared memory (planner.cpp select_group_tile
+  // otherwise pins t = F, planner.cpp:73 of the reference).
+  bool iir_streaming = false;
 };
 
 struct LaunchConfig {
@@ -323,7 +329,8 @@ FusionPlan plan(const Pipeline& pipeline, const Device& device,
 std::string render_plan(const FusionPlan& plan);
 
 // Plan options in the C-ABI JSON form (fuseplan.h:39-45):
-// {"halo_mode", "transfer_variant", "force_partition": "1-2,3-5", "tile"}.
+// {"halo_mode", "transfer_variant", "force_partition": "1-2,3-5", "tile",
+//  "iir_streaming"}.
 PlanOptions parse_plan_options(const char* options_json);
 std::vector<std::pair<int, int>> parse_partition_string(const std::string& s);
 std::string partition_string(const std::vector<std::pair<int, int>>& p);

@@ -259,7 +259,7 @@ GroupTile size_group(std::span<const KernelDesc> ks, const Device& dev,
   lim.constrain_input_box = true;
   lim.max_x = std::max(video.width, video.height);
   lim.max_t = video.frames;
-  if (any_recurrence(ks)) lim.min_t = video.frames;
+  if (any_recurrence(ks) && !opt.iir_streaming) lim.min_t = video.frames;
   try {
     TileSearchResult r = optimal_tile(g.halo, dev.smem_bytes / eb, lim, eb);
     g.tile = r.tile;
@@ -646,6 +646,7 @@ PlanOptions parse_plan_options(const char* text) {
     const auto& t = j["tile"];
     o.forced_tile = TileShape{t.value("x", 1), t.value("y", 1), t.value("t", 1)};
   }
+  if (j.contains("iir_streaming")) o.iir_streaming = j["iir_streaming"].get<bool>();
   return o;
 }
 

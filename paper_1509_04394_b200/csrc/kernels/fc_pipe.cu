@@ -71,6 +71,7 @@ constexpr int SW = 120;     // output columns per strip (window 128 = SW + 8)
 constexpr int BWB = 144;    // TMA box row bytes: 128 + worst-case 16-B alignment slack
 constexpr int PROW = 1024;  // bytes per IIR pair-row
 constexpr int QC = 64;      // recheck queue records per stencil warp
+constexpr int BODY = 6;     // steps per rolled body of the stencil march (= max rows per record)
 
 struct Args {
   uint8_t* out;
@@ -83,6 +84,8 @@ struct Args {
   float* state_out;
   long long* dbg;  // optional per-CTA timing (FUSEPLAN_PIPE_PROFILE), 8 slots per CTA
   int skip;        // timing experiments only (FUSEPLAN_PIPE_SKIP): 1 IIR math, 2 stencil math
+  int dbg_x, dbg_y, dbg_t;  // diagnostics (FUSEPLAN_PIPE_DEBUG_PX=x,y,t): dump the
+  float* dbg_px;            // recheck's 7x7 IIR neighbourhood + decision
   FastParams p;
 };
 
@@ -522,7 +525,7 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
       step(ic<5>{}, T, T, T, p + 3);
       step(ic<0>{}, T, T, T, p + 4);
       step(ic<1>{}, T, T, T, p + 5);
-      flush(p - 5, 6);
+      flush(p - 5, BODY);
     }
     constexpr int PT = 8 + 6 * ((NP - 8) / 6);  // tail: full steps PT .. NP - 1
     if constexpr (NP - PT >= 1) step(ic<2>{}, T, T, T, PT);
@@ -530,9 +533,10 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
     if constexpr (NP - PT >= 3) step(ic<4>{}, T, T, T, PT + 2);
     if constexpr (NP - PT >= 4) step(ic<5>{}, T, T, T, PT + 3);
     if constexpr (NP - PT >= 5) step(ic<0>{}, T, T, T, PT + 4);
+    if constexpr (NP - PT >= 1) flush(PT - 5, NP - PT);  // <= 5 rows per record
     step(ic<NP % 6>{}, F, T, T, NP);
     step(ic<(NP + 1) % 6>{}, F, F, T, NP + 1);
-    flush(PT - 5, NP + 2 - PT);
+    flush(NP - 5, 2);
 
     // ---- exact recheck of the queued uncertain values (rare)
     if (nq > QC) {
@@ -557,17 +561,29 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
       unsigned cnt = 0;
       // work items: record r, row q0 + s, half h, column j -> one exact
       // decision each, spread over the lanes (latency ~ items / 32 calls)
-      const int items = nq * 20;
+      constexpr int PER = 4 * BODY;  // values per record: BODY rows x 2 halves x 2 cols
+      const int items = nq * PER;
       for (int it = lane; it < items; it += 32) {
-        const uint32_t rec = queue[it / 20];
-        const int e = it % 20, st = e >> 2, half = (e >> 1) & 1, j = e & 1;
+        const uint32_t rec = queue[it / PER];
+        const int e = it % PER, st = e >> 2, half = (e >> 1) & 1, j = e & 1;
         const int q0 = int(rec >> 16), L = int((rec >> 8) & 31), nstep = int(rec & 0xFFu);
         if (st >= nstep) continue;
         const int x = bx + 2 * (1 + 30 * side + L) + j;
         const int y = by + q0 + st + half * OH;
         if (y >= H) continue;
-        o[(long long)y * W + x] = exact_white<OH>(a, sb, taps, bx, by, x, y, half) ? 0xFF : 0x00;
+        const bool wv = exact_white<OH>(a, sb, taps, bx, by, x, y, half);
+        o[(long long)y * W + x] = wv ? 0xFF : 0x00;
         ++cnt;
+        if (a.dbg_px && x == a.dbg_x && y == a.dbg_y && u == a.dbg_t) {
+          for (int dy = -3; dy <= 3; ++dy)
+            for (int dx = -3; dx <= 3; ++dx)
+              a.dbg_px[(dy + 3) * 7 + dx + 3] =
+                  iir_at<OH>(sb, clampi(y + dy, 0, H - 1) - by, clampi(x + dx, 0, W - 1) - bx,
+                             half);
+          a.dbg_px[49] = wv ? 1.0f : 0.0f;
+          a.dbg_px[50] = float(half);
+          a.dbg_px[51] = 1.0f;
+        }
       }
       for (int k2 = 16; k2 > 0; k2 >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, k2);
       if (lane == 0) atomicAdd(&g_rechecks, (unsigned long long)cnt);
@@ -795,6 +811,15 @@ extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stag
   a.state_out = state_out;
   a.p = fp;
   if (const char* e = std::getenv("FUSEPLAN_PIPE_SKIP")) a.skip = std::atoi(e);
+  if (const char* e = std::getenv("FUSEPLAN_PIPE_BAND_SCALE"))  // diagnostics only
+    a.p.band_n *= float(std::atof(e));
+  static float* dbg_px = nullptr;
+  if (const char* e = std::getenv("FUSEPLAN_PIPE_DEBUG_PX")) {
+    if (!dbg_px) cudaMalloc(&dbg_px, 64 * sizeof(float));
+    cudaMemset(dbg_px, 0, 64 * sizeof(float));
+    std::sscanf(e, "%d,%d,%d", &a.dbg_x, &a.dbg_y, &a.dbg_t);
+    a.dbg_px = dbg_px;
+  }
   CUtensorMap map;
   if (!rgb_tensor_map(&map, video, d, BWB, 2 * cache.oh + 6)) return -1;
   const int grid = cache.strips * cache.bands;
@@ -835,6 +860,17 @@ extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stag
                      "iir wait rgb %.2f slot %.2f\n",
                      names[k], cls[k][0], cls[k][1] / cls[k][0], cls[k][5],
                      cls[k][2] / cls[k][0], cls[k][3] / cls[k][0], cls[k][4] / cls[k][0]);
+  }
+  if (a.dbg_px) {
+    float h[64];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, a.dbg_px, sizeof h, cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "fc_pipe debug px (%d,%d,%d): seen %g half %g white %g\n", a.dbg_x,
+                 a.dbg_y, a.dbg_t, h[51], h[50], h[49]);
+    for (int r = 0; r < 7; ++r) {
+      for (int c = 0; c < 7; ++c) std::fprintf(stderr, " %.9g", h[r * 7 + c]);
+      std::fprintf(stderr, "\n");
+    }
   }
   return rc;
 }

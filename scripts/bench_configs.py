@@ -1,0 +1,145 @@
+"""Measures every BASELINE.json configuration on one B200 (bench.py times only
+the headline config 3) and checks each against the oracle on the frames the
+oracle can afford.  One JSON line per measurement; run on the GPU box:
+
+    python scripts/bench_configs.py > profiles/rNN_configs.jsonl
+
+cfg1  192x432x600, optimizer partition (the CPU reference's default run)
+cfg2  192x432x600: unfused 1,2,3,4,5 vs optimizer plan vs all-fused 1-5
+cfg3  800x600x1000 fused (same as bench.py)
+cfg4  800x600x16000 streamed from pinned host memory (double-buffered chunks,
+      H2D + compute + D2H overlapped), end to end through fp_exec_run
+cfg5  2048x2048x1000 fused, device resident (16.8 GB RGBA input)
+
+Device timings: CUDA events on the launching stream, median of 5 after 2
+warm-ups; inputs larger than L2 except cfg1/2 (199 MB video, 66 MB mask:
+also > L2 = 126 MB for the video).
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402  (checker only)
+from paper_1509_04394_b200 import fuseplan as fp  # noqa: E402
+
+PEAK = 6558.7
+try:
+    PEAK = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+except Exception:
+    pass
+
+
+def timed(fn, reps=5, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def check_prefix(pipe_spec, video_dev, mask_dev, frames):
+    """Bit-exact check of the first `frames` output frames against the oracle
+    (the IIR starts at frame 0, so a prefix is self-contained)."""
+    sub = video_dev[:frames].cpu().numpy()
+    spec = dict(pipe_spec)
+    spec["video"] = dict(spec["video"], frames=frames)
+    want = O.orc_chain(spec, sub)
+    got = mask_dev[:frames].cpu().numpy().astype(np.float32)
+    return int((got != want).sum())
+
+
+def line(**kw):
+    print(json.dumps(kw), flush=True)
+
+
+def device_config(name, W, H, F, partition, variant="auto", check_frames=8):
+    spec = fp.spec_chain(W, H, F, kalman=True)
+    pipe = fp.Pipeline(json.dumps(spec))
+    opts = None if partition == "plan" else {"force_partition": partition + ",6"}
+    plan = fp.Plan(pipe, fp.Device.load("b200"), opts)
+    ex = fp.Executor(pipe, plan, variant=variant)
+    video = torch.empty((F, 4, H, W), dtype=torch.uint8, device="cuda")
+    fp.synth_hash_u8(video, seed=1234)
+    mask = torch.empty((F, H, W), dtype=torch.uint8, device="cuda")
+    ms = timed(lambda: ex.run(video, out=mask))
+    bad = check_prefix(spec, video, mask, min(check_frames, F))
+    d = ex.describe()
+    line(config=name, workload=f"{W}x{H}x{F}", partition=plan.partition,
+         kernels=[g["kernel"] for g in d["groups"]], launches_per_run=d["launches_per_run"],
+         ms=ms, fps=F / ms * 1e3, mpix_per_s=W * H * F / ms / 1e3,
+         alg_gbps=4 * W * H * F / ms / 1e6, roofline_frac=4 * W * H * F / ms / 1e6 / PEAK,
+         oracle_frames_checked=min(check_frames, F), oracle_mismatches=bad)
+    del video, mask
+    torch.cuda.empty_cache()
+
+
+def streamed_config(name, W, H, F, chunk_check=8):
+    spec = fp.spec_chain(W, H, F, kalman=True)
+    pipe = fp.Pipeline(json.dumps(spec))
+    # the reference's planner pins IIR groups to t = F and reports 16000 frames
+    # infeasible; the streaming executor does not need that (iir_streaming)
+    plan = fp.Plan(pipe, fp.Device.load("b200"),
+                   {"force_partition": "1-5,6", "iir_streaming": True})
+    ex = fp.Executor(pipe, plan)
+    t0 = time.perf_counter()
+    host = torch.empty((F, 4, H, W), dtype=torch.uint8, pin_memory=True)
+    out = torch.empty((F, H, W), dtype=torch.uint8, pin_memory=True)
+    step = 1000
+    dev = torch.empty((step, 4, H, W), dtype=torch.uint8, device="cuda")
+    for t in range(0, F, step):
+        n = min(step, F - t)
+        fp.synth_hash_u8(dev[:n], t0=t, seed=1234)
+        host[t:t + n].copy_(dev[:n])
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    ex.run(host.numpy(), out=out.numpy())  # warm
+    ts = []
+    for _ in range(2):
+        t1 = time.perf_counter()
+        ex.run(host.numpy(), out=out.numpy())
+        ts.append(time.perf_counter() - t1)
+    dt = min(ts)
+    want = O.orc_chain(dict(spec, video=dict(spec["video"], frames=chunk_check)),
+                       host[:chunk_check].numpy())
+    bad = int((out[:chunk_check].numpy().astype(np.float32) != want).sum())
+    line(config=name, workload=f"{W}x{H}x{F}", mode="host-pinned streamed e2e",
+         s=dt, fps=F / dt, mpix_per_s=W * H * F / dt / 1e6,
+         h2d_gbps=3 * W * H * F / dt / 1e9, d2h_gbps=W * H * F / dt / 1e9,
+         setup_s=setup, oracle_frames_checked=chunk_check, oracle_mismatches=bad)
+
+
+def main():
+    which = sys.argv[1:] or ["1", "2", "3", "4", "5"]
+    if "1" in which:
+        device_config("cfg1", 192, 432, 600, "plan")
+    if "2" in which:
+        for part in ["1,2,3,4,5", "plan", "1-2,3-5", "1-5"]:
+            device_config("cfg2", 192, 432, 600, part)
+        device_config("cfg2", 192, 432, 600, "1-5", variant="exact")
+    if "3" in which:
+        device_config("cfg3", 800, 600, 1000, "1-5")
+        device_config("cfg3", 800, 600, 1000, "1,2,3,4,5")
+    if "4" in which:
+        streamed_config("cfg4", 800, 600, 16000)
+    if "5" in which:
+        device_config("cfg5", 2048, 2048, 1000, "1-5", check_frames=4)
+
+
+if __name__ == "__main__":
+    main()

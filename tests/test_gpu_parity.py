@@ -111,8 +111,8 @@ def test_larger_hash_video_dense_mask(fp, cuda, oracle):
                                       ((256, 200, 11), 24.0), ((368, 131, 4), 30.0),
                                       ((240, 1, 3), 8.0), ((128, 300, 2), 24.0)])
 def test_fast_certified_path_exact(fp, cuda, oracle, shape, th, variant):
-    """The certified FP32 kernels (variant='fast' = strip march, 'fast_tile' =
-    tile march; both fail loudly if they do not apply) are bit-exact,
+    """The certified FP32 kernels (variant='fast' = frame pipeline, 'fast_tile'
+    = tile march; both fail loudly if they do not apply) are bit-exact,
     including pixels that took the FP64 recheck."""
     from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
     W, H, F = shape
@@ -146,6 +146,37 @@ def test_fast_path_rechecks_happen_and_are_exact(fp, cuda, oracle, variant):
     after = ex.describe()["exact_rechecks_total"]
     assert after > before
     np.testing.assert_array_equal(out.cpu().numpy().astype(np.float32), want)
+
+
+@pytest.mark.parametrize("kernel", ["pipe", "pipe63", "strip"])
+@pytest.mark.parametrize("shape,seed", [((240, 90, 7), 5), ((368, 131, 5), 6),
+                                        ((2048, 64, 3), 7), ((64, 600, 3), 8),
+                                        ((800, 600, 2), 9)])
+def test_certified_kernels_forced_rechecks(fp, cuda, oracle, monkeypatch, kernel, shape, seed):
+    """Every certified kernel, with the pipe kernel's band scaled x1000 so that
+    several % of all pixels take the exact FP64 recheck (and the per-warp
+    recheck queue overflows): still bit-exact.  Shapes cover strips/bands
+    that end inside the window, multi-wave grids and one-band videos."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    if kernel == "strip":
+        monkeypatch.setenv("FUSEPLAN_FAST_KERNEL", "strip")
+    if kernel == "pipe63":
+        monkeypatch.setenv("FUSEPLAN_PIPE_CFG", "63")
+    monkeypatch.setenv("FUSEPLAN_PIPE_BAND_SCALE", "1000")
+    W, H, F = shape
+    pipe = spec_chain(W, H, F)
+    v = hash_video_u8(F, 4, H, W, seed)
+    want = oracle.orc_chain(pipe, v)
+    p = fp.Pipeline(json.dumps(pipe))
+    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": "1-5"}),
+                     variant="fast")
+    import torch
+    before = ex.describe()["exact_rechecks_total"]
+    out = ex.run(torch.from_numpy(v).to(cuda))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy().astype(np.float32), want)
+    if kernel != "strip":
+        assert ex.describe()["exact_rechecks_total"] - before > W * H * F // 50
 
 
 def test_state_carry_and_warm_restart(fp, cuda, oracle):

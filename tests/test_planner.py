@@ -104,3 +104,23 @@ def test_reports_render(fp):
     assert "TT" in txt and "KK" in txt
     sweep = fp.Device.load("k20_like").tile_sweep([1, 1, 1, 1, 0, 0], 8, 4)
     assert sweep.startswith("x,y,t,du,v,feasible")
+
+
+def test_iir_streaming_option(fp):
+    """B200 extension: by default the planner keeps the reference's rule that
+    an IIR group holds the whole time extent (800x600x16000 -> infeasible,
+    SURVEY P1); with iir_streaming the streaming executor's plan is feasible
+    and the partition / tiles of groups without the IIR are unchanged."""
+    spec = fp.spec_chain(800, 600, 16000, kalman=True)
+    p = fp.Pipeline(json.dumps(spec))
+    dev = fp.Device.load("b200")
+    with pytest.raises(fp.InfeasibleError):
+        fp.Plan(p, dev, {"force_partition": "1-5,6"})
+    plan = fp.Plan(p, dev, {"force_partition": "1-5,6", "iir_streaming": True})
+    assert plan.partition == [(1, 5), (6, 6)]
+    # short videos: the option does not change a plan whose t already fits
+    q = fp.Pipeline(json.dumps(fp.spec_chain(800, 600, 1000, kalman=True)))
+    a = json.loads(fp.Plan(q, dev, {"force_partition": "1-2,3-5,6"}).render_json())
+    b = json.loads(fp.Plan(q, dev, {"force_partition": "1-2,3-5,6",
+                                     "iir_streaming": False}).render_json())
+    assert a == b
