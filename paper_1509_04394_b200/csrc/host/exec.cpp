@@ -42,6 +42,25 @@ struct Scratch {
   float* b;
 };
 
+// Value-range propagation for the certified F345 kernel (inputs must lie in
+// [0, max]): nonnegative-weight averages keep the bound, everything else
+// makes it unknown (-1).
+double stage_range(const fc_stage& s, double in_max) {
+  if (in_max < 0) return -1.0;
+  switch (s.op) {
+    case FC_RGBA2GRAY:
+      if (s.wr < 0 || s.wg < 0 || s.wb < 0) return -1.0;
+      return in_max * (double(s.wr) + double(s.wg) + double(s.wb));
+    case FC_IIR_TEMPORAL:
+      return (s.alpha >= 0.0f && s.alpha <= 1.0f) ? in_max : -1.0;
+    case FC_IDENTITY:
+    case FC_BOX_MEAN:
+      return in_max;
+    default:
+      return -1.0;
+  }
+}
+
 }  // namespace
 
 std::vector<float> gaussian_taps(int radius, double sigma) {
@@ -106,8 +125,8 @@ fc_stage make_stage(const KernelDesc& k) {
 const char* LaunchGroup::kernel_name() const {
   switch (kind) {
     case GrayIir: return "F12 gray+iir (time scan)";
-    case GaussGradThr: return "F345 gauss+grad+thr (frame tiles)";
-    case Chain: return "F12345 streaming chain";
+    case GaussGradThr: return "F345 gauss+grad+thr (certified frame pipeline / exact tiles)";
+    case Chain: return "F12345 streaming chain (certified frame pipeline / exact)";
     default: return "unfused stages";
   }
 }
@@ -248,6 +267,9 @@ void Executor::run_device(const void* video, int in_type, void* out, int n_frame
 
   const void* cur = video;
   int cur_type = in_type;
+  // Upper bound of the values held by `cur` (all >= 0), for the certified
+  // F345 kernel's error band; < 0 = unknown (the exact kernel runs instead).
+  double cur_max = in_type == FC_U8 ? 255.0 : -1.0;
   int frames = n_frames;   // frames held by `cur`
   int warm = n_warm;       // warm-up frames still at the front of `cur`
   int iir_idx = 0;
@@ -294,6 +316,7 @@ void Executor::run_device(const void* video, int in_type, void* out, int n_frame
         break;
       }
       case LaunchGroup::GrayIir:
+        cur_max = stage_range(g.stages[1], stage_range(g.stages[0], cur_max));
         cuda_check(fc_fused_gray_iir(&g.stages[0], &g.stages[1], cur, cur_type,
                                      static_cast<float*>(dst), d, warm,
                                      state_ptr(state_in),
@@ -305,10 +328,11 @@ void Executor::run_device(const void* video, int in_type, void* out, int n_frame
         break;
       case LaunchGroup::GaussGradThr:
         require(cur_type == FC_F32, ErrorKind::Internal, "F345 needs f32 planes");
-        cuda_check(fc_fused_gauss_grad_thr(&g.stages[0], &g.stages[1], &g.stages[2],
-                                           static_cast<const float*>(cur), dst,
-                                           dst_type, d, st),
+        cuda_check(fc_fused_gauss_grad_thr_v(&g.stages[0], &g.stages[1], &g.stages[2],
+                                             static_cast<const float*>(cur), dst, dst_type, d,
+                                             int(opt_.variant), cur_max, st),
                    "F345 launch");
+        cur_max = -1.0;
         break;
       case LaunchGroup::Stages:
         for (std::size_t si = 0; si < g.stages.size(); ++si) {
@@ -331,6 +355,7 @@ void Executor::run_device(const void* video, int in_type, void* out, int n_frame
             cuda_check(fc_stage_spatial(&s, cur, cur_type, sdst, sdst_type, sd, st),
                        "stage launch");
           }
+          cur_max = stage_range(s, cur_max);
           cur = sdst;
           cur_type = sdst_type;
           if (!(last_stage && last_group)) which ^= 1;

@@ -173,23 +173,14 @@ inline float certify_band_scaled(double T, float mlo_n, double gmax_s, double dw
 // chain is outside it (u8 RGBA video, {0,255} u8 mask, IIR alpha = 0.5,
 // gaussian r = 2 with separable taps, threshold > 0, width a multiple of 16
 // (TMA strides), 16-byte aligned base); the caller then runs the exact kernel.
-inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
-                        const fc_stage* sthr, const void* video, int in_type, int gray_in,
-                        int out_type, fc_dims d, FastParams* p) {
-  if (in_type != FC_U8 || out_type != FC_U8 || gray_in || sgray == nullptr) return false;
-  if (si->alpha != 0.5f) return false;
+// Stencil half of the certified path (S3-S5): separable / centre-normalised
+// taps, M*, and the certified bands for inputs in [0, in_max].
+inline bool stencil_params(const fc_stage* sg, const fc_stage* sthr, int out_type,
+                           double in_max, FastParams* p) {
+  if (out_type != FC_U8) return false;
   if (sg->g_radius != 2 || !(sthr->th > 0.0f)) return false;
   if (sthr->white != 255.0f || sthr->black != 0.0f) return false;
-  if (d.width % 16 != 0 || d.height < 1) return false;
-  if (reinterpret_cast<uintptr_t>(video) % 16 != 0) return false;
-  std::memset(p, 0, sizeof *p);
-  // alpha = 0.5 folded into the gray weights (exact power-of-two scale)
-  p->wr = sgray->wr * 0.5f;
-  p->wg = sgray->wg * 0.5f;
-  p->wb = sgray->wb * 0.5f;
-  p->wrm = -p->wr * 8388608.0f;
-  p->wgm = -p->wg * 8388608.0f;
-  p->wbm = -p->wb * 8388608.0f;
+  if (!(in_max > 0.0) || !std::isfinite(in_max)) return false;
   // Separable fast taps from the centre row of the reference taps: in exact
   // arithmetic w[2][k] / sum_k w[2][k] is the normalised 1-D gaussian.
   double e[5], row = 0.0, es = 0.0;
@@ -214,11 +205,9 @@ inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stag
   while (std::sqrt(m) < sthr->th) m = std::nextafter(m, INFINITY);
   p->mstar = m;
   p->mlo = std::nextafter(m, 0.0f);
-  p->k4b = 0x4B000000u;
-  double gray_max = 255.0 * (double(sgray->wr) + double(sgray->wg) + double(sgray->wb));
   double tap_sum = 0.0;
   for (int k = 0; k < 25; ++k) tap_sum += sg->g_w[k];
-  p->band = certify_band(p->mstar, gray_max * tap_sum * 1.001, dw);
+  p->band = certify_band(p->mstar, in_max * tap_sum * 1.001, dw);
   // centre-normalised taps and their certification (scaled domain)
   const double S = 1.0 / (e[2] / es * (e[2] / es));
   p->g0 = float((e[0] / es) / (e[2] / es));
@@ -233,8 +222,29 @@ inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stag
   if (!(dwn < 1e-5)) return false;
   const double T = S * S * double(p->mstar);
   p->mlo_n = float(T);
-  p->band_n = certify_band_scaled(T, p->mlo_n, S * gray_max * tap_sum * 1.001, dwn);
+  p->band_n = certify_band_scaled(T, p->mlo_n, S * in_max * tap_sum * 1.001, dwn);
   return true;
+}
+
+inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                        const fc_stage* sthr, const void* video, int in_type, int gray_in,
+                        int out_type, fc_dims d, FastParams* p) {
+  if (in_type != FC_U8 || out_type != FC_U8 || gray_in || sgray == nullptr) return false;
+  if (si->alpha != 0.5f) return false;
+  if (d.width % 16 != 0 || d.height < 1) return false;
+  if (reinterpret_cast<uintptr_t>(video) % 16 != 0) return false;
+  std::memset(p, 0, sizeof *p);
+  // alpha = 0.5 folded into the gray weights (exact power-of-two scale)
+  p->wr = sgray->wr * 0.5f;
+  p->wg = sgray->wg * 0.5f;
+  p->wb = sgray->wb * 0.5f;
+  p->wrm = -p->wr * 8388608.0f;
+  p->wgm = -p->wg * 8388608.0f;
+  p->wbm = -p->wb * 8388608.0f;
+  p->k4b = 0x4B000000u;
+  // IIR values are convex combinations of gray values in [0, gray_max]
+  const double gray_max = 255.0 * (double(sgray->wr) + double(sgray->wg) + double(sgray->wb));
+  return stencil_params(sg, sthr, out_type, gray_max, p);
 }
 
 inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -248,6 +258,21 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
   }
   return fn;
+}
+
+// 3-D map over f32 planes [T][H][W] with a box of (bw, rows, 1): one copy
+// brings a haloed window of one frame (the F345 input of the pipe kernel).
+inline bool plane_tensor_map(CUtensorMap* map, const void* planes, fc_dims d, int bw, int rows) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {cuuint64_t(d.width), cuuint64_t(d.height), cuuint64_t(d.frames)};
+  cuuint64_t strides[2] = {cuuint64_t(d.width) * 4, cuuint64_t(d.width) * d.height * 4};
+  cuuint32_t box[3] = {cuuint32_t(bw), cuuint32_t(rows), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(planes), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
 }
 
 // 3-D map over the planar video [4T][H][W] u8 with a box of (bw, rows, 3):

@@ -17,6 +17,10 @@ extern "C" int fc_chain_pipe(FC_CHAIN_ARGS);   // fc_pipe.cu: certified, headlin
 extern "C" int fc_chain_pipe63(FC_CHAIN_ARGS); // fc_pipe_cfg63.cu: role-count variant
 extern "C" int fc_chain_strip(FC_CHAIN_ARGS);  // fc_strip.cu: certified, strip march
 extern "C" int fc_chain_tile(FC_CHAIN_ARGS);   // fc_fast.cu: certified, tile march
+extern "C" int fc_f345_pipe(const fc_stage* sg, const fc_stage* sthr, const float* in,
+                            void* out, int out_type, fc_dims d, double in_max, void* stream);
+extern "C" int fc_f345_pipe63(const fc_stage* sg, const fc_stage* sthr, const float* in,
+                              void* out, int out_type, fc_dims d, double in_max, void* stream);
 extern "C" long long fc_strip_recheck_count(void);
 extern "C" long long fc_pipe_recheck_count(void);
 extern "C" long long fc_pipe63_recheck_count(void);
@@ -55,4 +59,17 @@ extern "C" long long fc_last_recheck_count(void) {
   long long a = fc_strip_recheck_count(), b = fc_tile_recheck_count();
   long long c = fc_pipe_recheck_count(), e = fc_pipe63_recheck_count();
   return (a < 0 || b < 0 || c < 0 || e < 0) ? -1 : a + b + c + e;
+}
+
+extern "C" int fc_fused_gauss_grad_thr_v(const fc_stage* sg, const fc_stage* sgrad,
+                                         const fc_stage* sthr, const float* in, void* out,
+                                         int out_type, fc_dims d, int variant, double in_max,
+                                         void* stream) {
+  if (variant != 1 && in_max > 0.0) {
+    const char* cfg = std::getenv("FUSEPLAN_PIPE_CFG");
+    auto* f345 = (cfg && std::strcmp(cfg, "63") == 0) ? fc_f345_pipe63 : fc_f345_pipe;
+    const int rc = f345(sg, sthr, in, out, out_type, d, in_max, stream);
+    if (rc != -1) return rc;  // -1: parameters not covered -> exact
+  }
+  return fc_fused_gauss_grad_thr(sg, sgrad, sthr, in, out, out_type, d, stream);
 }

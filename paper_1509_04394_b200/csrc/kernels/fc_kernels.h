@@ -84,6 +84,14 @@ int fc_fused_gauss_grad_thr(const fc_stage* s_gauss, const fc_stage* s_grad,
                             const fc_stage* s_thr, const float* in, void* out,
                             int out_type, fc_dims d, void* stream);
 
+/* F345 with a variant: 1 = exact (FP64 kernel); 0 / 2 = the certified
+ * frame-pipeline kernel when the inputs are known to lie in [0, in_max]
+ * (in_max > 0; the executor's range analysis), else exact. */
+int fc_fused_gauss_grad_thr_v(const fc_stage* s_gauss, const fc_stage* s_grad,
+                              const fc_stage* s_thr, const float* in, void* out,
+                              int out_type, fc_dims d, int variant, double in_max,
+                              void* stream);
+
 /* variant: 0 = auto, 1 = exact (FP64 gaussian everywhere),
  *          2 = certified FP32 fast path with exact recheck */
 int fc_fused_chain(const fc_stage* s_gray, const fc_stage* s_iir,

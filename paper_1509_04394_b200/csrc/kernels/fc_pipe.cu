@@ -53,6 +53,7 @@
 #define FP_KSLACK 2
 #define FP_NAMESPACE fcpipe
 #define FP_ENTRY fc_chain_pipe
+#define FP_F345_ENTRY fc_f345_pipe
 #define FP_RECHECKS fc_pipe_recheck_count
 #endif
 
@@ -314,6 +315,72 @@ __device__ __forceinline__ void iir_role(const Args& a, int iw, int lane, int bx
         if (yx < H) a.state_out[(long long)yx * W + xl + j] = v[r][j].x;
         if (yy < H) a.state_out[(long long)yy * W + xl + j] = v[r][j].y;
       }
+    }
+  }
+}
+
+// F345 mode: the "IIR" warps load the frame's f32 input plane window (TMA
+// slot, row-major, 512 B per row) and repack it into the pair-row layout; no
+// state.  Window cells outside the video take the clamped row / edge column.
+template <int OH, bool BX, bool BY>
+__device__ __forceinline__ void plane_role(const Args& a, int iw, int lane, int bx, int by) {
+  constexpr int NP = OH + 6;
+  constexpr int NR = (NP + NI - 1) / NI;
+  const int W = a.W, H = a.H, n = a.n_frames;
+  const int xl = bx + 4 * lane;
+  int colb = 16 * lane, comp = -1;  // byte offset of the lane's 4 floats in a slot row
+  if (BX && (xl < 0 || xl > W - 1)) {
+    const int edge = xl < 0 ? 0 : W - 1;
+    colb = ((edge & ~3) - bx) * 4;
+    comp = edge & 3;  // replicate this component
+  }
+  const unsigned so0 = chunk_off(2 * lane), so1 = chunk_off(2 * lane + 1);
+  const unsigned smem0 = smem_u32(fp_smem);
+  int rslot = 0, islot = 0;
+  unsigned rpar = 0, ipar = 0;
+  for (int t = 0; t < n; ++t) {
+    wait_phase(bar_rgb_full(a, rslot), rpar);
+    const unsigned char* f = fp_smem + rslot * a.rgb_stride;
+    float2 v[NR][4];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int p = iw + NI * r;
+      if (p >= NP) continue;
+      const int rx = BY ? clampi(by + p, 0, H - 1) - by : p;
+      const int ry = BY ? clampi(by + p + OH, 0, H - 1) - by : p + OH;
+      float4 qx = *reinterpret_cast<const float4*>(f + rx * 512 + colb);
+      float4 qy = *reinterpret_cast<const float4*>(f + ry * 512 + colb);
+      if (BX && comp >= 0) {
+        const float ex = comp == 0 ? qx.x : comp == 1 ? qx.y : comp == 2 ? qx.z : qx.w;
+        const float ey = comp == 0 ? qy.x : comp == 1 ? qy.y : comp == 2 ? qy.z : qy.w;
+        qx = make_float4(ex, ex, ex, ex);
+        qy = make_float4(ey, ey, ey, ey);
+      }
+      v[r][0] = f2(qx.x, qy.x);
+      v[r][1] = f2(qx.y, qy.y);
+      v[r][2] = f2(qx.z, qy.z);
+      v[r][3] = f2(qx.w, qy.w);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_rgb_empty(a, rslot));
+    if (++rslot == NSF) {
+      rslot = 0;
+      rpar ^= 1u;
+    }
+    wait_phase(bar_iir_empty(a, islot), ipar ^ 1u);
+    const unsigned base = smem0 + a.off_iir + islot * a.iir_stride;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int p = iw + NI * r;
+      if (p >= NP) continue;
+      sts128(base + p * PROW + so0, v[r][0], v[r][1]);
+      sts128(base + p * PROW + so1, v[r][2], v[r][3]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_iir_full(a, islot));
+    if (++islot == K) {
+      islot = 0;
+      ipar ^= 1u;
     }
   }
 }
@@ -614,7 +681,9 @@ __device__ __forceinline__ long long interior_flag(const Args& a, int bx, int by
   return (bx >= 0 && bx + 127 <= a.W - 1 ? 1 : 0) + (by >= 0 && by + R - 1 <= a.H - 1 ? 2 : 0);
 }
 
-template <int OH>
+// SRC_F32 = false: the SPEC chain from the u8 RGBA video (F12345);
+// SRC_F32 = true:  gaussian + gradient + threshold from f32 planes (F345).
+template <int OH, bool SRC_F32>
 __global__ void __launch_bounds__(NTHR, 1)
     k_chain_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
   constexpr int R = 2 * OH + 6;
@@ -651,6 +720,16 @@ __global__ void __launch_bounds__(NTHR, 1)
       stencil_role<OH, false>(a, warp, lane, bx, by);
     else
       stencil_role<OH, true>(a, warp, lane, bx, by);
+  } else if (warp < NS + NI && SRC_F32) {
+    const int iw = warp - NS;
+    if (interior)
+      plane_role<OH, false, false>(a, iw, lane, bx, by);
+    else if (in_x)
+      plane_role<OH, false, true>(a, iw, lane, bx, by);
+    else if (in_y)
+      plane_role<OH, true, false>(a, iw, lane, bx, by);
+    else
+      plane_role<OH, true, true>(a, iw, lane, bx, by);
   } else if (warp < NS + NI) {
     const int iw = warp - NS, xoff = bx - tx0;
     if (interior)
@@ -670,7 +749,11 @@ __global__ void __launch_bounds__(NTHR, 1)
       wait_phase(bar_rgb_empty(a, slot), par ^ 1u);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(bar_rgb_full(a, slot), a.rgb_bytes);
-      tma_load_3d(fp_smem + slot * a.rgb_stride, &tmap, bar_rgb_full(a, slot), tx0, by, 4 * t);
+      if (SRC_F32)  // f32 plane window: x start bx is a multiple of 4 (16-byte aligned)
+        tma_load_3d(fp_smem + slot * a.rgb_stride, &tmap, bar_rgb_full(a, slot), bx, by, t);
+      else
+        tma_load_3d(fp_smem + slot * a.rgb_stride, &tmap, bar_rgb_full(a, slot), tx0, by,
+                    4 * t);
       if (++slot == NSF) {
         slot = 0;
         par ^= 1u;
@@ -681,9 +764,10 @@ __global__ void __launch_bounds__(NTHR, 1)
 
 // ------------------------------------------------------------------ host
 
-size_t layout(int oh, Args* a) {
+size_t layout(int oh, bool src_f32, Args* a) {
   const int R = 2 * oh + 6;
-  const size_t rgb = size_t(3) * R * BWB, rgb_stride = (rgb + 127) / 128 * 128;
+  const size_t rgb = src_f32 ? size_t(R) * 512 : size_t(3) * R * BWB;
+  const size_t rgb_stride = (rgb + 127) / 128 * 128;
   size_t off = NSF * rgb_stride;
   const size_t off_iir = off;
   const size_t iir_stride = size_t(oh + 6) * PROW;
@@ -710,11 +794,11 @@ using KernelFn = void (*)(CUtensorMap, Args);
 
 #define FP_OH_LIST(X) X(3) X(4) X(5) X(8) X(10) X(12) X(15)
 
-KernelFn kernel_for(int oh) {
+KernelFn kernel_for(int oh, bool src_f32) {
   switch (oh) {
 #define FP_CASE(N) \
   case N:          \
-    return k_chain_pipe<N>;
+    return src_f32 ? k_chain_pipe<N, true> : k_chain_pipe<N, false>;
     FP_OH_LIST(FP_CASE)
 #undef FP_CASE
   }
@@ -730,7 +814,7 @@ struct PipePlan {
 // Every CTA marches the whole video; an SM's time is ~ (CTAs it runs) x (its
 // CTA's pair-rows).  Pick OH minimising the busiest SM's pair-rows; ties go to
 // the larger window (less halo).  FUSEPLAN_PIPE_OH forces the choice.
-bool choose(int W, int H, int dev, PipePlan* pp) {
+bool choose(int W, int H, int dev, bool src_f32, PipePlan* pp) {
   int sms = 0, optin = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -746,9 +830,9 @@ bool choose(int W, int H, int dev, PipePlan* pp) {
   const bool dbg = std::getenv("FUSEPLAN_DEBUG") != nullptr;
   for (int oh : ohs) {
     if (force && oh != force) continue;
-    const size_t smem = layout(oh, nullptr);
+    const size_t smem = layout(oh, src_f32, nullptr);
     if (smem > size_t(optin)) continue;
-    KernelFn fn = kernel_for(oh);
+    KernelFn fn = kernel_for(oh, src_f32);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     int per_sm = 0;
@@ -776,23 +860,17 @@ bool choose(int W, int H, int dev, PipePlan* pp) {
   return best < 1e300;
 }
 
-}  // namespace FP_NAMESPACE
-
-using namespace FP_NAMESPACE;
-
-extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
-                             const fc_stage* sthr, const void* video, int in_type, int gray_in,
-                             void* out, int out_type, fc_dims d, int n_warm,
-                             const float* state_in, float* state_out, void* stream) {
-  FastParams fp;
-  if (!fast_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d, &fp)) return -1;
+// Shared launcher of both modes (src_f32: F345 from f32 planes).
+int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, fc_dims d,
+                int n_warm, const float* state_in, float* state_out, void* stream) {
   if (d.frames == 0) return 0;
   int dev = 0;
   cudaGetDevice(&dev);
-  static thread_local PipePlan cache;
+  static thread_local PipePlan caches[2];
+  PipePlan& cache = caches[src_f32 ? 1 : 0];
   if (cache.W != d.width || cache.H != d.height || cache.dev != dev) {
     PipePlan pp;
-    if (!choose(d.width, d.height, dev, &pp)) return -1;
+    if (!choose(d.width, d.height, dev, src_f32, &pp)) return -1;
     pp.W = d.width;
     pp.H = d.height;
     pp.dev = dev;
@@ -800,7 +878,7 @@ extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stag
   }
   Args a;
   std::memset(&a, 0, sizeof a);
-  layout(cache.oh, &a);
+  layout(cache.oh, src_f32, &a);
   a.out = static_cast<uint8_t*>(out);
   a.W = d.width;
   a.H = d.height;
@@ -821,7 +899,9 @@ extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stag
     a.dbg_px = dbg_px;
   }
   CUtensorMap map;
-  if (!rgb_tensor_map(&map, video, d, BWB, 2 * cache.oh + 6)) return -1;
+  if (src_f32 ? !plane_tensor_map(&map, in, d, 128, 2 * cache.oh + 6)
+              : !rgb_tensor_map(&map, in, d, BWB, 2 * cache.oh + 6))
+    return -1;
   const int grid = cache.strips * cache.bands;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool profile = std::getenv("FUSEPLAN_PIPE_PROFILE") != nullptr;
@@ -829,7 +909,7 @@ extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stag
     cudaMalloc(&a.dbg, sizeof(long long) * 8 * grid);
     cudaMemsetAsync(a.dbg, 0, sizeof(long long) * 8 * grid, st);
   }
-  kernel_for(cache.oh)<<<grid, NTHR, cache.smem, st>>>(map, a);
+  kernel_for(cache.oh, src_f32)<<<grid, NTHR, cache.smem, st>>>(map, a);
   const int rc = int(cudaGetLastError());
   if (profile && a.dbg) {  // per-CTA span and per-role wait shares
     std::vector<long long> h(size_t(8) * grid);
@@ -873,6 +953,32 @@ extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stag
     }
   }
   return rc;
+}
+
+}  // namespace FP_NAMESPACE
+
+using namespace FP_NAMESPACE;
+
+extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                        const fc_stage* sthr, const void* video, int in_type, int gray_in,
+                        void* out, int out_type, fc_dims d, int n_warm,
+                        const float* state_in, float* state_out, void* stream) {
+  FastParams fp;
+  if (!fast_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d, &fp)) return -1;
+  return launch_pipe(false, fp, video, out, d, n_warm, state_in, state_out, stream);
+}
+
+// F345 (gaussian r=2 + Sobel + threshold) on f32 planes whose values lie in
+// [0, in_max] (in_max from the executor's range analysis; <= 0: unknown ->
+// -1, the caller runs the exact kernel).
+extern "C" int FP_F345_ENTRY(const fc_stage* sg, const fc_stage* sthr, const float* in,
+                             void* out, int out_type, fc_dims d, double in_max,
+                             void* stream) {
+  FastParams fp;
+  std::memset(&fp, 0, sizeof fp);
+  if (d.width % 4 != 0 || reinterpret_cast<uintptr_t>(in) % 16 != 0) return -1;
+  if (!stencil_params(sg, sthr, out_type, in_max, &fp)) return -1;
+  return launch_pipe(true, fp, in, out, d, 0, nullptr, nullptr, stream);
 }
 
 extern "C" long long FP_RECHECKS(void) {

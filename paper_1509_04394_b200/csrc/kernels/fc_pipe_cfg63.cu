@@ -5,5 +5,6 @@
 #define FP_KSLACK 1
 #define FP_NAMESPACE fcpipe63
 #define FP_ENTRY fc_chain_pipe63
+#define FP_F345_ENTRY fc_f345_pipe63
 #define FP_RECHECKS fc_pipe63_recheck_count
 #include "fc_pipe.cu"

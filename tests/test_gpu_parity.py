@@ -148,12 +148,15 @@ def test_fast_path_rechecks_happen_and_are_exact(fp, cuda, oracle, variant):
     np.testing.assert_array_equal(out.cpu().numpy().astype(np.float32), want)
 
 
-@pytest.mark.parametrize("kernel", ["pipe", "pipe63", "strip"])
+@pytest.mark.parametrize("kernel,part", [("pipe", "1-5"), ("pipe63", "1-5"), ("strip", "1-5"),
+                                         ("pipe", "1-2,3-5"), ("pipe63", "1-2,3-5")])
 @pytest.mark.parametrize("shape,seed", [((240, 90, 7), 5), ((368, 131, 5), 6),
                                         ((2048, 64, 3), 7), ((64, 600, 3), 8),
                                         ((800, 600, 2), 9)])
-def test_certified_kernels_forced_rechecks(fp, cuda, oracle, monkeypatch, kernel, shape, seed):
-    """Every certified kernel, with the pipe kernel's band scaled x1000 so that
+def test_certified_kernels_forced_rechecks(fp, cuda, oracle, monkeypatch, kernel, part, shape,
+                                           seed):
+    """Every certified kernel (all-fused F12345 and the optimizer's F345 group
+    on f32 IIR planes), with the pipe kernel's band scaled x1000 so that
     several % of all pixels take the exact FP64 recheck (and the per-warp
     recheck queue overflows): still bit-exact.  Shapes cover strips/bands
     that end inside the window, multi-wave grids and one-band videos."""
@@ -168,14 +171,14 @@ def test_certified_kernels_forced_rechecks(fp, cuda, oracle, monkeypatch, kernel
     v = hash_video_u8(F, 4, H, W, seed)
     want = oracle.orc_chain(pipe, v)
     p = fp.Pipeline(json.dumps(pipe))
-    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": "1-5"}),
-                     variant="fast")
+    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": part}),
+                     variant="fast" if part == "1-5" else "auto")
     import torch
     before = ex.describe()["exact_rechecks_total"]
     out = ex.run(torch.from_numpy(v).to(cuda))
     torch.cuda.synchronize()
     np.testing.assert_array_equal(out.cpu().numpy().astype(np.float32), want)
-    if kernel != "strip":
+    if kernel != "strip":  # (the strip kernel has its own band; no scaling)
         assert ex.describe()["exact_rechecks_total"] - before > W * H * F // 50
 
 
