@@ -519,11 +519,19 @@ int fc_stage_iir(const fc_stage* s, const float* in, float* out, fc_dims d,
   return status();
 }
 
+int fc_gray_iir_stream(const fc_stage* sg, const fc_stage* si, const void* video,
+                       int in_type, float* out, fc_dims d, int n_warm,
+                       const float* state_in, float* state_out, void* stream);  // fc_f12.cu
+
 int fc_fused_gray_iir(const fc_stage* sg, const fc_stage* si, const void* video,
                       int in_type, float* out, fc_dims d, int n_warm,
                       const float* state_in, float* state_out, void* stream) {
   long long hw = (long long)d.width * d.height;
   if (hw == 0 || d.frames == 0) return 0;
+  // streaming bulk-copy kernel for u8 video (fc_f12.cu); -1 = not applicable
+  const int rc = fc_gray_iir_stream(sg, si, video, in_type, out, d, n_warm, state_in,
+                                    state_out, stream);
+  if (rc != -1) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float beta = 1.0f - si->alpha;
   int grid = int((hw + 127) / 128);
