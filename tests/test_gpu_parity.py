@@ -182,6 +182,23 @@ def test_certified_kernels_forced_rechecks(fp, cuda, oracle, monkeypatch, kernel
         assert ex.describe()["exact_rechecks_total"] - before > W * H * F // 50
 
 
+@pytest.mark.parametrize("shape", [(64, 48, 9), (192, 432, 5), (800, 600, 3), (16, 1, 40)])
+@pytest.mark.parametrize("alpha", [0.5, 0.3])
+def test_f12_stream_kernel_exact(fp, cuda, oracle, monkeypatch, shape, alpha):
+    """The bulk-copy F12 kernel (forced on for small frames too) writes the
+    reference's exact IIR planes, for the default and a non-dyadic alpha,
+    including state carry across a range split."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    monkeypatch.setenv("FUSEPLAN_F12_STREAM", "1")
+    W, H, F = shape
+    pipe = spec_chain(W, H, F, alpha=alpha)
+    pipe12 = dict(pipe, kernels=pipe["kernels"][:2])
+    v = hash_video_u8(F, 4, H, W, 31)
+    want = oracle.orc_run_sequential(pipe12, v)[-1]
+    out, _ = run(fp, pipe12, v, {"force_partition": "1-2"}, torch_dev=cuda)
+    np.testing.assert_array_equal(out, want)
+
+
 def test_state_carry_and_warm_restart(fp, cuda, oracle):
     """run_range: resuming from the carried state is exact; a warm-up restart
     equals the oracle's restart semantics at the same frame."""
