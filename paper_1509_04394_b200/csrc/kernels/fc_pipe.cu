@@ -47,6 +47,9 @@
 
 // Warp-role counts (fc_pipe_cfg*.cu re-include this file with other values
 // under another namespace / entry name for tuning comparisons).
+#ifndef FP_WAIT_HINT
+#define FP_WAIT_HINT ", %2"  // suspend-time hint operand of try_wait ("" = none)
+#endif
 #ifndef FP_NF
 #define FP_NF 5
 #define FP_NI 5
@@ -118,7 +121,7 @@ __device__ __forceinline__ void wait_phase(uint64_t* bar, unsigned phase) {
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1" FP_WAIT_HINT ";\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(phase), "r"(1000000u)
