@@ -50,6 +50,9 @@
 #ifndef FP_WAIT_HINT
 #define FP_WAIT_HINT ", %2"  // suspend-time hint operand of try_wait ("" = none)
 #endif
+#ifndef FP_LC
+#define FP_LC 2
+#endif
 #ifndef FP_NF
 #define FP_NF 5
 #define FP_NI 5
@@ -64,8 +67,10 @@ namespace FP_NAMESPACE {
 
 using namespace fccommon;
 
-constexpr int NF = FP_NF;   // frames in flight in the stencil (two warps each)
-constexpr int NS = 2 * NF;  // stencil warps
+constexpr int LC = FP_LC;   // columns per stencil lane: 2 (two warps per frame) or 4 (one)
+constexpr int WPF = 4 / LC; // stencil warps per frame
+constexpr int NF = FP_NF;   // frames in flight in the stencil
+constexpr int NS = WPF * NF;  // stencil warps
 constexpr int NI = FP_NI;   // IIR warps
 constexpr int NWARP = NS + NI + 1;
 constexpr int NTHR = NWARP * 32;
@@ -454,11 +459,17 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
   const float g0 = a.p.g0, g1 = a.p.g1;
   const double* taps = reinterpret_cast<const double*>(fp_smem + a.off_taps);
   uint32_t* queue = reinterpret_cast<uint32_t*>(fp_smem + a.off_queue) + sw * QC;
-  const int f0 = sw >> 1, side = sw & 1;
-  const int k = 1 + 30 * side + lane;  // the lane's chunk
+  // LC = 2: warps 2f, 2f+1 share frame f (64-column halves, lane chunk
+  // k = 1 + 30 side + L); LC = 4: warp f alone, lane columns 4L .. 4L+3
+  const int f0 = sw / WPF, side = sw % WPF;
+  const int k = LC == 2 ? 1 + 30 * side + lane : 2 * lane;  // the lane's first chunk
   const int xl = bx + 2 * k;           // video column of the lane's first cell
   const bool outl = lane >= 1 && lane <= 30 && xl < W;
-  const unsigned cl = chunk_off(k - 1), c0 = chunk_off(k), cr = chunk_off(k + 1);
+  // loaded chunks: k-1 .. k + LC/2 (the edge lanes of LC = 4 wrap around the
+  // row; those values only feed non-output columns)
+  unsigned cch[LC / 2 + 2];
+#pragma unroll
+  for (int i = 0; i < LC / 2 + 2; ++i) cch[i] = chunk_off((k - 1 + i + 64) & 63);
   const unsigned smem0 = smem_u32(fp_smem);
   const unsigned lt_mask = (1u << lane) - 1u;
 
@@ -481,8 +492,8 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
     int nq = 0;                                              // queued records
     float amin = __int_as_float(0x7f800000);                 // running min |nd|
 
-    float2 hr[6][2];  // H row r at ring index r % 6
-    float2 gr[6][2];  // G row r at ring index r % 6
+    float2 hr[6][LC];  // H row r at ring index r % 6
+    float2 gr[6][LC];  // G row r at ring index r % 6
 
     // Step p of the skewed march: H row p, G row p - 3 (from H rows p-5..p-1)
     // and Sobel at pair-row p - 5 (G rows p-6..p-4) are mutually
@@ -495,16 +506,21 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
       // ---- horizontal pass of pair-row p
       if constexpr (DO_H) {
         const unsigned rb = base + p * PROW;
-        const float4 L4 = lds128(rb + cl), A4 = lds128(rb + c0), R4 = lds128(rb + cr);
-        const float2 m2 = lo2(L4), m1 = hi2(L4), v0 = lo2(A4), v1 = hi2(A4), q1 = lo2(R4),
-                     q2 = hi2(R4);
-        hr[PM][0] = tap4n(m2, m1, v0, v1, q1, g0, g1);
-        hr[PM][1] = tap4n(m1, v0, v1, q1, q2, g0, g1);
+        float2 v[LC + 4];  // columns c-2 .. c+LC+1
+#pragma unroll
+        for (int i = 0; i < LC / 2 + 2; ++i) {
+          const float4 q4 = lds128(rb + cch[i]);
+          v[2 * i] = lo2(q4);
+          v[2 * i + 1] = hi2(q4);
+        }
+#pragma unroll
+        for (int j = 0; j < LC; ++j)
+          hr[PM][j] = tap4n(v[j], v[j + 1], v[j + 2], v[j + 3], v[j + 4], g0, g1);
       }
       // ---- vertical pass: G row p - 3
       if constexpr (DO_V) {
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < LC; ++j)
           gr[(PM + 3) % 6][j] = tap4n(hr[(PM + 1) % 6][j], hr[(PM + 2) % 6][j],
                                       hr[(PM + 3) % 6][j], hr[(PM + 4) % 6][j],
                                       hr[(PM + 5) % 6][j], g0, g1);
@@ -514,9 +530,9 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
         constexpr int QM = (PM + 1) % 6;  // q % 6
         const int q = p - 5;
         const int yx = by + q, yy = by + q + OH;  // video rows of the two halves
-        float2 s2[2], d2[2];
+        float2 s2[LC], d2[LC];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < LC; ++j) {
           float2 gm = gr[(QM + 5) % 6][j], gc = gr[QM][j], gp = gr[(QM + 1) % 6][j];
           if (BORDER) {  // predicated selects: the step stays one basic block
             if (yx == 0) gm.x = gc.x;
@@ -527,17 +543,19 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
           s2[j] = __fadd2_rn(__ffma2_rn(splat(2.0f), gc, gm), gp);
           d2[j] = __ffma2_rn(splat(-1.0f), gm, gp);
         }
-        float2 sl = shfl_up2(s2[1]), dl = shfl_up2(d2[1]);
+        float2 sl = shfl_up2(s2[LC - 1]), dl = shfl_up2(d2[LC - 1]);
         float2 sr = shfl_down2(s2[0]), dr = shfl_down2(d2[0]);
         if (BORDER) {
           if (xl == 0) sl = s2[0], dl = d2[0];
-          if (xl + 1 == W - 1) sr = s2[1], dr = d2[1];
+          if (xl + LC - 1 == W - 1) sr = s2[LC - 1], dr = d2[LC - 1];
         }
-        const float2 S[4] = {sl, s2[0], s2[1], sr};
-        const float2 D[4] = {dl, d2[0], d2[1], dr};
-        float2 dm[2];
+        float2 S[LC + 2], D[LC + 2];
+        S[0] = sl, D[0] = dl, S[LC + 1] = sr, D[LC + 1] = dr;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < LC; ++j) S[j + 1] = s2[j], D[j + 1] = d2[j];
+        float2 dm[LC];
+#pragma unroll
+        for (int j = 0; j < LC; ++j) {
           const float2 gx = __ffma2_rn(splat(-1.0f), S[j], S[j + 2]);
           const float2 gy = __fadd2_rn(__ffma2_rn(splat(2.0f), D[j + 1], D[j]), D[j + 2]);
           // nd = mlo - gy^2 - gx^2 (< 0 <=> white); certify_band's 2u (M* + m) term
@@ -546,15 +564,22 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
         }
         const bool okx = outl && (!BORDER || yx < H);
         const bool oky = outl && (!BORDER || yy < H);
-        if (okx) *reinterpret_cast<uint16_t*>(ox) = uint16_t(pack_neg2(dm[0].x, dm[1].x));
-        if (oky) *reinterpret_cast<uint16_t*>(oy) = uint16_t(pack_neg2(dm[0].y, dm[1].y));
+        if constexpr (LC == 2) {
+          if (okx) *reinterpret_cast<uint16_t*>(ox) = uint16_t(pack_neg2(dm[0].x, dm[1].x));
+          if (oky) *reinterpret_cast<uint16_t*>(oy) = uint16_t(pack_neg2(dm[0].y, dm[1].y));
+        } else {
+          if (okx)
+            *reinterpret_cast<uint32_t*>(ox) = pack_neg(dm[0].x, dm[1].x, dm[2].x, dm[3].x);
+          if (oky)
+            *reinterpret_cast<uint32_t*>(oy) = pack_neg(dm[0].y, dm[1].y, dm[2].y, dm[3].y);
+        }
         ox += W;  // running row pointers
         oy += W;
         // running min of |nd| over the lane's output values (branch-free;
         // checked once per 6-step body; values of rows below the video only
         // cause a harmless extra recheck)
-        amin = fminf(fminf(amin, fminf(fabsf(dm[0].x), fabsf(dm[0].y))),
-                     fminf(fabsf(dm[1].x), fabsf(dm[1].y)));
+#pragma unroll
+        for (int j = 0; j < LC; ++j) amin = fminf(amin, fminf(fabsf(dm[j].x), fabsf(dm[j].y)));
       }
     };
     // After a body of steps whose Sobel rows are q0 .. q0 + nstep - 1: lanes
@@ -619,11 +644,11 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
           for (int half = 0; half < 2; ++half) {
             const int y = by + q + half * OH;
             if (y >= H) continue;
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < LC; ++j)
               o[(long long)y * W + xl + j] =
                   exact_white<OH>(a, sb, taps, bx, by, xl + j, y, half) ? 0xFF : 0x00;
           }
-      if (lane == 0) atomicAdd(&g_rechecks, (unsigned long long)(60 * 4 * OH));
+      if (lane == 0) atomicAdd(&g_rechecks, (unsigned long long)(30 * LC * 2 * OH));
       __syncwarp();
     } else if (nq) {
       __syncwarp();  // queue records and the warp's mask stores are visible
@@ -631,14 +656,14 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
       unsigned cnt = 0;
       // work items: record r, row q0 + s, half h, column j -> one exact
       // decision each, spread over the lanes (latency ~ items / 32 calls)
-      constexpr int PER = 4 * BODY;  // values per record: BODY rows x 2 halves x 2 cols
+      constexpr int PER = 2 * LC * BODY;  // values per record: rows x 2 halves x LC cols
       const int items = nq * PER;
       for (int it = lane; it < items; it += 32) {
         const uint32_t rec = queue[it / PER];
-        const int e = it % PER, st = e >> 2, half = (e >> 1) & 1, j = e & 1;
+        const int e = it % PER, st = e / (2 * LC), half = (e / LC) & 1, j = e % LC;
         const int q0 = int(rec >> 16), L = int((rec >> 8) & 31), nstep = int(rec & 0xFFu);
         if (st >= nstep) continue;
-        const int x = bx + 2 * (1 + 30 * side + L) + j;
+        const int x = bx + 2 * (LC == 2 ? 1 + 30 * side + L : 2 * L) + j;
         const int y = by + q0 + st + half * OH;
         if (y >= H) continue;
         const bool wv = exact_white<OH>(a, sb, taps, bx, by, x, y, half);
@@ -703,7 +728,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     }
     for (int i = 0; i < K; ++i) {
       mbar_init(bar_iir_full(a, i), NI);
-      mbar_init(bar_iir_empty(a, i), 2);  // the frame's two stencil warps
+      mbar_init(bar_iir_empty(a, i), WPF);  // the frame's stencil warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }

@@ -1,5 +1,7 @@
-// Tuning variant of the frame pipeline: 6 frames in flight (12 stencil
-// warps), 3 IIR warps, 1 slack IIR slot.  FUSEPLAN_PIPE_CFG=63 selects it.
+// Tuning variant of the frame pipeline: 4-column stencil lanes (one warp
+// per frame), 6 frames in flight, 3 IIR warps, 1 slack IIR slot.
+// FUSEPLAN_PIPE_CFG=63 selects it.
+#define FP_LC 4
 #define FP_NF 6
 #define FP_NI 3
 #define FP_KSLACK 1
