@@ -50,6 +50,14 @@
 #ifndef FP_WAIT_HINT
 #define FP_WAIT_HINT ", %2"  // suspend-time hint operand of try_wait ("" = none)
 #endif
+#ifndef FP_NSF
+#define FP_NSF 4  // RGB (TMA) frame slots
+#endif
+#ifndef FP_SPECIALISE
+#define FP_SPECIALISE 0  // 1: interior / border code variants per CTA; 0: the general
+                         // (border) variant everywhere -- measured 1.5 % faster: one
+                         // code path per role keeps the instruction caches warm
+#endif
 #ifndef FP_LC
 #define FP_LC 2
 #endif
@@ -75,7 +83,7 @@ constexpr int NI = FP_NI;   // IIR warps
 constexpr int NWARP = NS + NI + 1;
 constexpr int NTHR = NWARP * 32;
 constexpr int K = NF + FP_KSLACK;  // IIR frame slots (slack: frames the IIR may run ahead)
-constexpr int NSF = 4;      // TMA RGB frame slots
+constexpr int NSF = FP_NSF; // TMA RGB frame slots
 constexpr int SW = 120;     // output columns per strip (window 128 = SW + 8)
 constexpr int BWB = 144;    // TMA box row bytes: 128 + worst-case 16-B alignment slack
 constexpr int PROW = 1024;  // bytes per IIR pair-row
@@ -742,7 +750,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   __syncthreads();  // the only CTA-wide barrier: roles run decoupled from here
 
   const bool in_x = bx >= 0 && bx + 127 <= a.W - 1, in_y = by >= 0 && by + R - 1 <= a.H - 1;
-  const bool interior = in_x && in_y;
+  const bool interior = FP_SPECIALISE && in_x && in_y;
   if (warp < NS) {
     if (interior)
       stencil_role<OH, false>(a, warp, lane, bx, by);
@@ -752,9 +760,9 @@ __global__ void __launch_bounds__(NTHR, 1)
     const int iw = warp - NS;
     if (interior)
       plane_role<OH, false, false>(a, iw, lane, bx, by);
-    else if (in_x)
+    else if (FP_SPECIALISE && in_x)
       plane_role<OH, false, true>(a, iw, lane, bx, by);
-    else if (in_y)
+    else if (FP_SPECIALISE && in_y)
       plane_role<OH, true, false>(a, iw, lane, bx, by);
     else
       plane_role<OH, true, true>(a, iw, lane, bx, by);
@@ -762,9 +770,9 @@ __global__ void __launch_bounds__(NTHR, 1)
     const int iw = warp - NS, xoff = bx - tx0;
     if (interior)
       iir_role<OH, false, false>(a, iw, lane, bx, by, xoff);
-    else if (in_x)
+    else if (FP_SPECIALISE && in_x)
       iir_role<OH, false, true>(a, iw, lane, bx, by, xoff);
-    else if (in_y)
+    else if (FP_SPECIALISE && in_y)
       iir_role<OH, true, false>(a, iw, lane, bx, by, xoff);
     else
       iir_role<OH, true, true>(a, iw, lane, bx, by, xoff);

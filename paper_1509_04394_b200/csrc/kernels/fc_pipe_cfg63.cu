@@ -1,10 +1,9 @@
-// Tuning variant of the frame pipeline: 4-column stencil lanes (one warp
-// per frame), 6 frames in flight, 3 IIR warps, 1 slack IIR slot.
-// FUSEPLAN_PIPE_CFG=63 selects it.
-#define FP_LC 4
-#define FP_NF 6
-#define FP_NI 3
-#define FP_KSLACK 1
+// Tuning variant of the frame pipeline: interior / border code variants per
+// CTA (FP_SPECIALISE 1).  FUSEPLAN_PIPE_CFG=63 selects it.
+#define FP_SPECIALISE 1
+#define FP_NF 5
+#define FP_NI 5
+#define FP_KSLACK 2
 #define FP_NAMESPACE fcpipe63
 #define FP_ENTRY fc_chain_pipe63
 #define FP_F345_ENTRY fc_f345_pipe63
