@@ -135,6 +135,23 @@ fp_status fp_exec_run_range(fp_exec* e, const void* video, int in_type,
                             const float* state_in, float* state_out,
                             void* stream);
 
+/* ---- K6 tracking (tracking.cpp:84-128, capi.cpp:366-381), on the GPU -----
+ * mask [frames][height][width], FP_ELEM_U8 or FP_ELEM_F32, "set" where
+ * > 127; mask_on_device != 0: a device pointer (async on `stream`, the call
+ * still returns after the points are on the host), else a host pointer.
+ * rois_xywh: n_rois x (x, y, w, h) initial ROIs, one per marker.
+ * kalman_json (nullable): {"q": 0.01, "r": 0.25, "p0": 10.0} (the reference's
+ * KalmanParams defaults).
+ * points (nullable, caller-owned, n_rois * frames * 23 doubles): per marker
+ * and frame: measured (0/1), meas_x, meas_y, est_x, est_y, est_vx, est_vy,
+ * covariance[16] row-major.
+ * csv_out (nullable): the reference's trajectory CSV text
+ * (trajectories_to_csv, tracking.cpp:130-146); free with fp_string_free. */
+fp_status fp_track_features(const void* mask, int elem_type, int mask_on_device,
+                            int width, int height, int frames, const int* rois_xywh,
+                            int n_rois, const char* kalman_json, double* points,
+                            char** csv_out, void* stream);
+
 /* JSON: the launch groups and the kernel each runs. */
 fp_status fp_exec_describe(const fp_exec* e, char** out_json);
 

@@ -41,7 +41,7 @@ HOST_SRCS = ["host/model.cpp", "host/planner.cpp", "host/video.cpp",
              "host/exec.cpp", "host/capi.cpp"]
 CUDA_SRCS = ["kernels/fc_exact.cu", "kernels/fc_fast.cu", "kernels/fc_strip.cu", "kernels/fc_pipe.cu",
              "kernels/fc_pipe_cfg63.cu",
-             "kernels/fc_f12.cu",
+             "kernels/fc_f12.cu", "kernels/fc_track.cu",
              "kernels/fc_dispatch.cu"]
 HEADERS = ["kernels/fc_pipe.cu", "host/fuseplan.hpp", "host/exec.hpp", "host/video.hpp",
            "kernels/fc_kernels.h", "kernels/fc_common.cuh"]

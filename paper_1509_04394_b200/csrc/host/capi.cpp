@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstring>
 #include <filesystem>
+#include <fstream>
 #include <iomanip>
 #include <memory>
 #include <sstream>
@@ -36,6 +37,80 @@ struct fp_exec {
 };
 
 namespace {
+
+constexpr int kTrackPts = 23;
+
+// trajectories_to_csv (tracking.cpp:130-146): same header, precision 9
+std::string trajectory_csv(const double* pts, int n_rois, int frames) {
+  std::ostringstream ss;
+  ss << "frame,marker_id,meas_x,meas_y,est_x,est_y,est_vx,est_vy\n";
+  ss << std::setprecision(9);
+  for (int m = 0; m < n_rois; ++m)
+    for (int t = 0; t < frames; ++t) {
+      const double* p = pts + (std::size_t(m) * frames + t) * kTrackPts;
+      ss << t << ',' << (m + 1) << ',';
+      if (p[0] != 0.0)
+        ss << p[1] << ',' << p[2];
+      else
+        ss << ',';
+      ss << ',' << p[3] << ',' << p[4] << ',' << p[5] << ',' << p[6] << '\n';
+    }
+  return ss.str();
+}
+
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(ErrorKind::Internal, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Runs the K6 kernel; `pts` receives n_rois * frames * kTrackPts doubles.
+void track_on_device(const void* mask, int elem_type, bool on_device, int W, int H, int F,
+                     const int* rois, int n_rois, double q, double r, double p0,
+                     std::vector<double>& pts, void* stream) {
+  require(W > 0 && H > 0 && F >= 0 && n_rois >= 1, ErrorKind::Input, "bad tracking dims");
+  require(elem_type == FP_ELEM_U8 || elem_type == FP_ELEM_F32, ErrorKind::Input,
+          "mask must be FP_ELEM_U8 or FP_ELEM_F32");
+  for (int i = 0; i < n_rois; ++i)
+    require(rois[4 * i + 2] >= 1 && rois[4 * i + 3] >= 1, ErrorKind::Input,
+            "ROI extents must be >= 1");
+  pts.assign(std::size_t(n_rois) * F * kTrackPts, 0.0);
+  if (F == 0) return;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const std::size_t mbytes = std::size_t(W) * H * F * (elem_type == FP_ELEM_U8 ? 1 : 4);
+  // grow-only per-thread device buffers (tracking runs often on short calls)
+  struct Buf {
+    void* p = nullptr;
+    std::size_t n = 0;
+    void* get(std::size_t want) {
+      if (want > n) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cuda_ok(cudaMalloc(&p, want), "cudaMalloc tracking buffer");
+        n = want;
+      }
+      return p;
+    }
+  };
+  static thread_local Buf bmask, brois, bpts;
+  const void* m = mask;
+  if (!on_device) {
+    void* dm = bmask.get(mbytes);
+    cuda_ok(cudaMemcpyAsync(dm, mask, mbytes, cudaMemcpyHostToDevice, st), "H2D mask");
+    m = dm;
+  }
+  int* drois = static_cast<int*>(brois.get(sizeof(int) * 4 * n_rois));
+  double* dpts = static_cast<double*>(bpts.get(sizeof(double) * pts.size()));
+  cuda_ok(cudaMemcpyAsync(drois, rois, sizeof(int) * 4 * n_rois, cudaMemcpyHostToDevice, st),
+          "H2D rois");
+  const int rc = fc_track_features(m, elem_type == FP_ELEM_U8 ? FC_U8 : FC_F32, W, H, F, drois,
+                                   n_rois, q, r, p0, dpts, stream);
+  cuda_ok(cudaError_t(rc), "tracking kernel");
+  cuda_ok(cudaMemcpyAsync(pts.data(), dpts, sizeof(double) * pts.size(), cudaMemcpyDeviceToHost,
+                          st),
+          "D2H points");
+  cuda_ok(cudaStreamSynchronize(st), "tracking sync");
+}
 
 thread_local std::string g_err;
 
@@ -274,8 +349,6 @@ fp_status fp_simulate(const fp_pipeline* p, const fp_device* d, const char* opti
     need(p && d && out);
     require((video_path != nullptr) != (synth_json != nullptr), ErrorKind::Input,
             "exactly one of video file / synth spec needed");
-    require(track_csv_path == nullptr, ErrorKind::Input,
-            "the tracking stage (K6) is not part of the B200 hot-path build");
     ReportFormat rf = fmt_of(format);
     PlanOptions base = parse_plan_options(options_json);
     HostVideo video = video_path ? read_fpvd_file(video_path)
@@ -338,6 +411,29 @@ fp_status fp_simulate(const fp_pipeline* p, const fp_device* d, const char* opti
     std::int64_t dev_fused = device_elems(executed, p->p);
     double reduction =
         dev_serial > 0 ? 100.0 * (1.0 - double(dev_fused) / double(dev_serial)) : 0.0;
+
+    if (track_csv_path) {  // capi.cpp:366-381: K6 on the tiled arm's mask, on the GPU
+      require(synth_json != nullptr, ErrorKind::Input,
+              "tracking output needs a synthetic scene with markers");
+      SyntheticSceneSpec spec = parse_synth_spec(synth_json);
+      require(!spec.markers.empty(), ErrorKind::Input,
+              "tracking output needs a synthetic scene with markers");
+      bool gray = pv.channels == 1;
+      for (const KernelDesc& k : p->p.kernels) gray = gray || k.stencil_op == "rgba2gray";
+      require(gray, ErrorKind::Input, "tracking needs a single-channel mask output");
+      std::vector<int> rois;
+      for (const auto& mk : spec.markers) {
+        const int side = 2 * int(std::ceil(mk.radius)) + 9;
+        rois.insert(rois.end(), {int(std::lround(mk.start_x)) - side / 2,
+                                 int(std::lround(mk.start_y)) - side / 2, side, side});
+      }
+      std::vector<double> pts;
+      track_on_device(b.data(), FP_ELEM_F32, false, pv.width, pv.height, pv.frames, rois.data(),
+                      int(spec.markers.size()), 0.01, 0.25, 10.0, pts, nullptr);
+      std::ofstream f(track_csv_path, std::ios::binary);
+      require(bool(f), ErrorKind::Input, std::string("cannot write ") + track_csv_path);
+      f << trajectory_csv(pts.data(), int(spec.markers.size()), pv.frames);
+    }
 
     std::ostringstream ss;
     if (rf == ReportFormat::Json) {
@@ -505,6 +601,32 @@ fp_status fp_exec_describe(const fp_exec* e, char** out_json) {
   return guarded([&] {
     need(e && out_json);
     *out_json = dup(e->ex->describe());
+  });
+}
+
+fp_status fp_track_features(const void* mask, int elem_type, int mask_on_device, int width,
+                            int height, int frames, const int* rois_xywh, int n_rois,
+                            const char* kalman_json, double* points, char** csv_out,
+                            void* stream) {
+  return guarded([&] {
+    need(mask && rois_xywh);
+    double q = 0.01, r = 0.25, p0 = 10.0;  // KalmanParams defaults (tracking.hpp:40-44)
+    if (kalman_json && *kalman_json) {
+      ordered_json j;
+      try {
+        j = ordered_json::parse(kalman_json);
+      } catch (const ordered_json::exception& e) {
+        throw Error(ErrorKind::Input, std::string("kalman: bad JSON: ") + e.what());
+      }
+      q = j.value("q", q);
+      r = j.value("r", r);
+      p0 = j.value("p0", p0);
+    }
+    std::vector<double> pts;
+    track_on_device(mask, elem_type, mask_on_device != 0, width, height, frames, rois_xywh,
+                    n_rois, q, r, p0, pts, stream);
+    if (points) std::memcpy(points, pts.data(), pts.size() * sizeof(double));
+    if (csv_out) *csv_out = dup(trajectory_csv(pts.data(), n_rois, frames));
   });
 }
 

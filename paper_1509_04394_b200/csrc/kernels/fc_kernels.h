@@ -111,6 +111,12 @@ int fc_hash_video_u8(uint8_t* out, fc_dims d, int channels, int t0,
  * launch on this stream's device (diagnostic; 0 if unavailable). */
 long long fc_last_recheck_count(void);
 
+/* K6 tracking: one CTA per marker (fc_track.cu).  rois_dev: n x (x, y, w, h)
+ * int32 on the device; points_dev: n x frames x 23 doubles on the device. */
+int fc_track_features(const void* mask, int elem_type, int W, int H, int F,
+                      const int* rois_dev, int n_rois, double q, double r, double p0,
+                      double* points_dev, void* stream);
+
 const char* fc_error_string(int code);
 
 #ifdef __cplusplus

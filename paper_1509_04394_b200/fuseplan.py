@@ -97,6 +97,8 @@ def lib() -> ctypes.CDLL:
         "fp_exec_run_range": ([P, P, I, P, I, I, P, P, P], I),
         "fp_exec_describe": ([P, PP], I),
         "fp_synth_hash_u8": ([P, I, I, I, I, I, ctypes.c_uint64, P], I),
+        "fp_track_features": ([P, I, I, I, I, I, ctypes.POINTER(ctypes.c_int), I, S,
+                               ctypes.POINTER(ctypes.c_double), PP, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -382,3 +384,41 @@ def spec_chain(width: int, height: int, frames: int, alpha: float = 0.5,
         ks.append({"name": "kalman_tracking", "stencil_op": "kalman_track"})
     return {"video": {"width": width, "height": height, "frames": frames, "fps": 1,
                       "channels": channels}, "kernels": ks}
+
+
+TRACK_POINT_FIELDS = ("measured", "meas_x", "meas_y", "est_x", "est_y", "est_vx", "est_vy") + \
+    tuple(f"cov{i}{j}" for i in range(4) for j in range(4))
+
+
+def track_features(mask, rois, q: float = 0.01, r: float = 0.25, p0: float = 10.0,
+                   stream=None, csv: bool = True):
+    """K6 tracking on the GPU (fp_track_features; tracking.cpp:84-128).
+
+    mask: [F, H, W] uint8 / float32, numpy (host) or a torch CUDA tensor;
+    rois: [(x, y, w, h)] initial ROI per marker.  Returns (points, csv):
+    points [n, F, 23] float64 (TRACK_POINT_FIELDS), csv the reference's
+    trajectory CSV text (None when csv=False)."""
+    F, H, W = (int(v) for v in mask.shape)
+    rois = np.ascontiguousarray(np.asarray(rois, np.int32).reshape(-1, 4))
+    n = rois.shape[0]
+    pts = np.zeros((n, F, 23), np.float64)
+    out = ctypes.c_void_p()
+    kal = json.dumps({"q": q, "r": r, "p0": p0}).encode()
+    is_torch = type(mask).__module__.startswith("torch")
+    if is_torch and mask.is_cuda:
+        torch = _torch()
+        mask = mask.contiguous()
+        elem = FP_ELEM_U8 if mask.dtype == torch.uint8 else FP_ELEM_F32
+        st = _stream_handle(torch.cuda.current_stream(mask.device) if stream is None else stream)
+        ptr, on_dev = mask.data_ptr(), 1
+    else:
+        arr = np.ascontiguousarray(mask.numpy() if is_torch else np.asarray(mask))
+        elem = FP_ELEM_U8 if arr.dtype == np.uint8 else FP_ELEM_F32
+        if elem == FP_ELEM_F32:
+            arr = arr.astype(np.float32, copy=False)
+        mask, ptr, on_dev, st = arr, arr.ctypes.data, 0, None
+    _check(lib().fp_track_features(
+        ptr, elem, on_dev, W, H, F, rois.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), n, kal,
+        pts.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+        ctypes.byref(out) if csv else None, st))
+    return pts, (_take_string(out) if csv else None)
