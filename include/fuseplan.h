@@ -135,6 +135,13 @@ fp_status fp_exec_run_range(fp_exec* e, const void* video, int in_type,
                             const float* state_in, float* state_out,
                             void* stream);
 
+/* FPVD file -> FPVD file (video.cpp:46-109), streamed through the GPU:
+ * chunks of host_chunk_frames frames are read into pinned buffers while the
+ * previous chunk runs, the IIR carried exactly between chunks, the output
+ * (1 channel: u8 mask or f32 planes) written as chunks complete -- the video
+ * never has to fit in host memory.  Synchronous. */
+fp_status fp_exec_run_file(fp_exec* e, const char* in_path, const char* out_path);
+
 /* ---- K6 tracking (tracking.cpp:84-128, capi.cpp:366-381), on the GPU -----
  * mask [frames][height][width], FP_ELEM_U8 or FP_ELEM_F32, "set" where
  * > 127; mask_on_device != 0: a device pointer (async on `stream`, the call

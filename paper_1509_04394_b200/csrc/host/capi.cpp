@@ -597,6 +597,13 @@ fp_status fp_exec_run_range(fp_exec* e, const void* video, int in_type, void* ou
   });
 }
 
+fp_status fp_exec_run_file(fp_exec* e, const char* in_path, const char* out_path) {
+  return guarded([&] {
+    need(e && in_path && out_path);
+    e->ex->run_file(in_path, out_path);
+  });
+}
+
 fp_status fp_exec_describe(const fp_exec* e, char** out_json) {
   return guarded([&] {
     need(e && out_json);

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <memory>
 #include <cmath>
 #include <cstring>
 #include <sstream>
@@ -459,6 +461,144 @@ void Executor::run_host(const void* video, int in_type, void* out) {
   cudaStreamDestroy(s_out);
   cudaFree(mem);
   if (!err.empty()) throw Error(ErrorKind::Internal, err);
+}
+
+void Executor::run_file(const std::string& in_path, const std::string& out_path) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  std::FILE* fin = std::fopen(in_path.c_str(), "rb");
+  require(fin != nullptr, ErrorKind::Input, "cannot open video file: " + in_path);
+  std::FILE* fout = nullptr;
+  std::unique_ptr<std::FILE, int (*)(std::FILE*)> in_guard(fin, &std::fclose);
+  // header: "FPVD", version, width, height, frames, channels, elem type
+  unsigned char hdr[28];
+  require(std::fread(hdr, 1, 28, fin) == 28 && std::memcmp(hdr, "FPVD", 4) == 0,
+          ErrorKind::Input, "not an FPVD video file");
+  auto u32 = [&](int i) {
+    return std::uint32_t(hdr[i]) | std::uint32_t(hdr[i + 1]) << 8 |
+           std::uint32_t(hdr[i + 2]) << 16 | std::uint32_t(hdr[i + 3]) << 24;
+  };
+  require(u32(4) == 1, ErrorKind::Input, "unsupported FPVD version");
+  require(int(u32(8)) == dims_.width && int(u32(12)) == dims_.height &&
+              int(u32(16)) == dims_.frames && int(u32(20)) == dims_.channels,
+          ErrorKind::Input, "video does not match pipeline dimensions");
+  require(u32(24) <= 1, ErrorKind::Input, "unknown FPVD element type");
+  const int in_type = u32(24) == 0 ? FC_U8 : FC_F32;
+
+  const long long hw = (long long)dims_.width * dims_.height;
+  const int C = dims_.channels, F = dims_.frames;
+  const std::size_t esz = in_type == FC_U8 ? 1 : 4;
+  const std::size_t osz = out_type_ == FC_U8 ? 1 : 4;
+  const std::size_t in_frame = std::size_t(C) * hw * esz, out_frame = std::size_t(hw) * osz;
+  const int read_planes =
+      (C == 4 && groups_.front().stages.front().op == FC_RGBA2GRAY) ? 3 : C;
+  bool temporal_window = false;
+  for (const auto& g : groups_)
+    for (const auto& st : g.stages)
+      if (st.op == FC_BOX_MEAN && st.rt > 0) temporal_window = true;
+  int chunk = opt_.host_chunk_frames;
+  if (chunk <= 0) chunk = int(std::max<long long>(1, (96LL << 20) / (long long)in_frame));
+  if (temporal_window) chunk = F;  // cannot cut a temporal window
+  chunk = std::max(1, std::min(chunk, F));
+  const int n_chunks = (F + chunk - 1) / chunk;
+
+  fout = std::fopen(out_path.c_str(), "wb");
+  require(fout != nullptr, ErrorKind::Input, "cannot write video file: " + out_path);
+  std::unique_ptr<std::FILE, int (*)(std::FILE*)> out_guard(fout, &std::fclose);
+  {
+    unsigned char oh[28];
+    std::memcpy(oh, "FPVD", 4);
+    const std::uint32_t vals[6] = {1u, std::uint32_t(dims_.width), std::uint32_t(dims_.height),
+                                   std::uint32_t(F), 1u, out_type_ == FC_U8 ? 0u : 1u};
+    for (int i = 0; i < 6; ++i)
+      for (int b = 0; b < 4; ++b) oh[4 + 4 * i + b] = (unsigned char)(vals[i] >> (8 * b));
+    require(std::fwrite(oh, 1, 28, fout) == 28, ErrorKind::Input, "write failed: " + out_path);
+  }
+  if (F == 0) return;
+
+  auto align = [](std::size_t b) { return (b + 255) & ~std::size_t(255); };
+  const std::size_t vbytes = align(std::size_t(chunk) * in_frame);
+  const std::size_t obytes = align(std::size_t(chunk) * out_frame);
+  const std::size_t sbytes = align(std::size_t(std::max(n_iir_, 1)) * hw * sizeof(float));
+  char* mem = nullptr;
+  char* pin = nullptr;
+  cuda_check(cudaMalloc(&mem, 2 * (vbytes + obytes + sbytes)), "cudaMalloc(file stream)");
+  if (cudaMallocHost(&pin, 2 * (vbytes + obytes)) != cudaSuccess) {
+    cudaFree(mem);
+    throw Error(ErrorKind::Internal, "cudaMallocHost(file stream) failed");
+  }
+  char* vb[2] = {mem, mem + vbytes};
+  char* ob[2] = {mem + 2 * vbytes, mem + 2 * vbytes + obytes};
+  float* sb[2] = {reinterpret_cast<float*>(mem + 2 * (vbytes + obytes)),
+                  reinterpret_cast<float*>(mem + 2 * (vbytes + obytes) + sbytes)};
+  char* pi[2] = {pin, pin + vbytes};
+  char* po[2] = {pin + 2 * vbytes, pin + 2 * vbytes + obytes};
+  cudaStream_t s_in, s_out;
+  cudaStream_t s_comp = static_cast<cudaStream_t>(own_stream_);
+  cuda_check(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream");
+  std::vector<cudaEvent_t> ev_in(n_chunks), ev_comp(n_chunks), ev_out(n_chunks);
+  for (int k = 0; k < n_chunks; ++k) {
+    cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming);
+  }
+  auto frames_of = [&](int k) { return std::min(chunk, F - k * chunk); };
+  auto write_chunk = [&](int k) {
+    cuda_check(cudaEventSynchronize(ev_out[k]), "sync D2H");
+    const std::size_t bytes = std::size_t(frames_of(k)) * out_frame;
+    require(std::fwrite(po[k & 1], 1, bytes, fout) == bytes, ErrorKind::Input,
+            "write failed: " + out_path);
+  };
+  std::string err;
+  ErrorKind kind = ErrorKind::Internal;
+  try {
+    for (int k = 0; k < n_chunks; ++k) {
+      const int nf = frames_of(k), b = k & 1;
+      // pinned input b is free once chunk k-2's H2D finished
+      if (k >= 2) cuda_check(cudaEventSynchronize(ev_in[k - 2]), "sync H2D");
+      const std::size_t bytes = std::size_t(nf) * in_frame;
+      require(std::fread(pi[b], 1, bytes, fin) == bytes, ErrorKind::Input,
+              "video payload size mismatch");
+      if (k >= 2) cuda_check(cudaStreamWaitEvent(s_in, ev_comp[k - 2], 0), "wait");
+      if (read_planes == C)
+        cuda_check(cudaMemcpyAsync(vb[b], pi[b], bytes, cudaMemcpyHostToDevice, s_in), "H2D");
+      else
+        cuda_check(cudaMemcpy2DAsync(vb[b], in_frame, pi[b], in_frame,
+                                     std::size_t(read_planes) * hw * esz, nf,
+                                     cudaMemcpyHostToDevice, s_in),
+                   "H2D");
+      cuda_check(cudaEventRecord(ev_in[k], s_in), "record");
+      cuda_check(cudaStreamWaitEvent(s_comp, ev_in[k], 0), "wait");
+      if (k >= 2) cuda_check(cudaStreamWaitEvent(s_comp, ev_out[k - 2], 0), "wait");
+      run_device(vb[b], in_type, ob[b], nf, 0, k == 0 || n_iir_ == 0 ? nullptr : sb[b ^ 1],
+                 n_iir_ ? sb[b] : nullptr, s_comp);
+      cuda_check(cudaEventRecord(ev_comp[k], s_comp), "record");
+      cuda_check(cudaStreamWaitEvent(s_out, ev_comp[k], 0), "wait");
+      cuda_check(cudaMemcpyAsync(po[b], ob[b], std::size_t(nf) * out_frame,
+                                 cudaMemcpyDeviceToHost, s_out),
+                 "D2H");
+      cuda_check(cudaEventRecord(ev_out[k], s_out), "record");
+      // disk write of the previous chunk overlaps this chunk's GPU work
+      if (k >= 1) write_chunk(k - 1);
+    }
+    write_chunk(n_chunks - 1);
+  } catch (const Error& e) {
+    err = e.what();
+    kind = e.kind();
+  }
+  cudaStreamSynchronize(s_in);
+  cudaStreamSynchronize(s_comp);
+  cudaStreamSynchronize(s_out);
+  for (int k = 0; k < n_chunks; ++k) {
+    cudaEventDestroy(ev_in[k]);
+    cudaEventDestroy(ev_comp[k]);
+    cudaEventDestroy(ev_out[k]);
+  }
+  cudaStreamDestroy(s_in);
+  cudaStreamDestroy(s_out);
+  cudaFreeHost(pin);
+  cudaFree(mem);
+  if (!err.empty()) throw Error(kind, err);
 }
 
 }  // namespace fuseplan

@@ -63,6 +63,13 @@ class Executor {
   // streams.  Synchronous.
   void run_host(const void* video, int in_type, void* out);
 
+  // FPVD file -> FPVD file (video.cpp:46-109 layout), streamed: chunks of
+  // frames are read from disk into pinned buffers while the previous chunk
+  // is on the GPU, the IIR carried exactly between chunks, the output
+  // (1 channel, u8 mask or f32 planes) written as chunks complete.  The
+  // video never has to fit in host memory.  Synchronous.
+  void run_file(const std::string& in_path, const std::string& out_path);
+
   std::string describe() const;  // JSON: launch groups and kernels
   std::int64_t launches_per_run() const;
 

@@ -96,6 +96,7 @@ def lib() -> ctypes.CDLL:
         "fp_exec_run": ([P, P, I, P, I, P], I),
         "fp_exec_run_range": ([P, P, I, P, I, I, P, P, P], I),
         "fp_exec_describe": ([P, PP], I),
+        "fp_exec_run_file": ([P, S, S], I),
         "fp_synth_hash_u8": ([P, I, I, I, I, I, ctypes.c_uint64, P], I),
         "fp_track_features": ([P, I, I, I, I, I, ctypes.POINTER(ctypes.c_int), I, S,
                                ctypes.POINTER(ctypes.c_double), PP, P], I),
@@ -320,6 +321,11 @@ class Executor(_Handle):
                                  out.ctypes.data, FP_EXEC_HOST_PTRS, None))
         return out
 
+    def run_file(self, in_path: str, out_path: str) -> None:
+        """FPVD file in -> FPVD file out, streamed through the GPU in chunks
+        (fp_exec_run_file); the video never has to fit in host memory."""
+        _check(lib().fp_exec_run_file(self.ptr, str(in_path).encode(), str(out_path).encode()))
+
     def run_range(self, video, n_warm: int = 0, state_in=None, state_out=None,
                   out=None, stream=None):
         """T-shard run on CUDA tensors: video [n, C, H, W] starting at the first
@@ -422,3 +428,33 @@ def track_features(mask, rois, q: float = 0.01, r: float = 0.25, p0: float = 10.
         pts.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
         ctypes.byref(out) if csv else None, st))
     return pts, (_take_string(out) if csv else None)
+
+
+def write_fpvd(path: str, video: np.ndarray) -> None:
+    """FPVD writer (video.cpp:46-62): planar [F, C, H, W] (or [F, H, W]) u8/f32."""
+    import struct
+    v = np.asarray(video)
+    if v.ndim == 3:
+        v = v[:, None]
+    F, C, H, W = v.shape
+    et = 0 if v.dtype == np.uint8 else 1
+    with open(path, "wb") as fh:
+        fh.write(b"FPVD" + struct.pack("<6I", 1, W, H, F, C, et))
+        fh.write(np.ascontiguousarray(v if et == 0 else v.astype(np.float32)).tobytes())
+
+
+def read_fpvd(path: str) -> np.ndarray:
+    """FPVD reader (video.cpp:64-94) -> planar [F, C, H, W] u8 / f32."""
+    import struct
+    with open(path, "rb") as fh:
+        hdr = fh.read(28)
+        if hdr[:4] != b"FPVD":
+            raise InputError("not an FPVD video file")
+        ver, W, H, F, C, et = struct.unpack("<6I", hdr[4:])
+        if ver != 1:
+            raise InputError("unsupported FPVD version")
+        dt = np.uint8 if et == 0 else np.float32
+        data = np.fromfile(fh, dtype=dt)
+    if data.size != F * C * H * W:
+        raise InputError("video payload size mismatch")
+    return data.reshape(F, C, H, W)
