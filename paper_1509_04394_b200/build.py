@@ -38,7 +38,8 @@ CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
              "-Wno-unused-function", f"-I{JSON_DIR}", f"-I{CUDA_HOME}/include"]
 
 HOST_SRCS = ["host/model.cpp", "host/planner.cpp", "host/video.cpp",
-             "host/exec.cpp", "host/capi.cpp"]
+             "host/exec.cpp", "host/capi.cpp",
+             "host/calibrate.cpp"]
 CUDA_SRCS = ["kernels/fc_exact.cu", "kernels/fc_fast.cu", "kernels/fc_strip.cu", "kernels/fc_pipe.cu",
              "kernels/fc_pipe_cfg63.cu",
              "kernels/fc_f12.cu", "kernels/fc_track.cu",

@@ -23,6 +23,10 @@
 using namespace fuseplan;
 using ordered_json = nlohmann::ordered_json;
 
+namespace fuseplan {
+void calibrate_csv(const std::string& text, double params[4], double* rms);  // calibrate.cpp
+}
+
 struct fp_pipeline {
   Pipeline p;
 };
@@ -503,10 +507,17 @@ fp_status fp_simulate(const fp_pipeline* p, const fp_device* d, const char* opti
 }
 
 fp_status fp_calibrate_csv(const char* measurements_csv, char** result_json) {
-  return guarded([&] {
+  return guarded([&] {  // capi.cpp:388-400
     need(measurements_csv && result_json);
-    throw Error(ErrorKind::Input,
-                "cost-model calibration is not part of the B200 hot-path build");
+    double prm[4], rms = 0.0;
+    calibrate_csv(measurements_csv, prm, &rms);
+    ordered_json j;
+    j["params"] = {{"gmem_cost_per_elem", prm[0]},
+                   {"smem_cost_per_elem", prm[1]},
+                   {"compute_cost_unit", prm[2]},
+                   {"launch_overhead", prm[3]}};
+    j["residual_rms"] = rms;
+    *result_json = dup(j.dump(2) + "\n");
   });
 }
 
