@@ -9,8 +9,10 @@ configuration (config 3: 800x600x1000 u8 RGBA, SPEC chain
 rgba2gray -> iir(0.5) -> gaussian(r2,s1) -> gradient -> threshold(128)),
 the video already resident in HBM.  N > 1 (torchrun): the video is sharded
 along T; every rank but the first warms its IIR up over 64 frames before its
-shard, then the IIR carry is exchanged with NCCL send/recv and verified
-bit-for-bit (fix-up re-run on mismatch) inside the timed region.
+shard, then every rank sends its IIR carry to the next (NCCL send/recv, all
+at once), verifies the one it received bit for bit, and one all-reduce finds
+the first wrong warm state (fix-up chain only from there) -- all inside the
+timed region.
 
 Prints ONE JSON line on rank 0.
 """
@@ -240,6 +242,12 @@ def main():
 
     host_stage = args.dist_backend == "gloo"
 
+    def first_bad(k):
+        # all-reduce MIN of "my warm state was wrong" rank indices (world = none)
+        t = torch.tensor([k], dtype=torch.int64, device="cpu" if host_stage else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return int(t.item())
+
     def send(state, dst):
         dist.send(state.cpu() if host_stage else state, dst)
 
@@ -258,7 +266,9 @@ def main():
             return
         # T-shard protocol: warm-up, shard, NCCL carry exchange + bitwise
         # verify, fix-up re-run on mismatch (paper_1509_04394_b200/sharding.py)
-        run_sharded(shard, run_shard, send, recv, torch.equal, events)
+        # world 2: the chain is one link anyway; beyond, verify in parallel
+        run_sharded(shard, run_shard, send, recv, torch.equal, events,
+                    first_bad if world > 2 else None)
 
     for _ in range(args.warmup):
         step()

@@ -7,15 +7,19 @@ earlier frame, so each rank
   1. warms the recurrence up over the W frames before its shard (restarting
      it there, like the reference does at frame 0, simulator.cpp:136-147),
   2. runs its shard from that warm state, keeping the end state,
-  3. receives the TRUE end state of rank g-1 (send/recv of one W*H float
-     plane -- the only collective of the path) and compares it bit for bit
-     with its warm state; on any mismatch it re-runs its shard from the true
-     state (the fix-up), which also corrects its own end state before it is
-     forwarded to rank g+1.
+  3. sends its end state to rank g+1 and receives rank g-1's (all ranks at
+     once: one send/recv of a W*H float plane per rank), compares it bit for
+     bit with its warm state, and the ranks agree (one all-reduce MIN) on the
+     first rank k whose warm state was wrong;
+  4. if every warm state was right (k = world), every shard started from the
+     exact state by induction (rank g's end state is exact when its start
+     state was) -- done.  Otherwise ranks >= k walk the carry in order from
+     k: each re-runs its shard from the true state (the fix-up) and forwards
+     its corrected end state.
 
-Step 3 walks the ranks in order, so every shard ends up computed from the
-exact state: the result is identical to a single-device run whatever W is;
-W only decides how often a fix-up is needed (W >= 48 gave no
+So the common case costs one exchange and one all-reduce whatever the rank
+count, and the result is identical to a single-device run whatever W is;
+W only decides how often the fix-up chain runs (W >= 48 gave no
 mismatch on 800x600 data).
 
 `run_shard` is the compute: (frames, n_warm, state_in) -> (output, state_out)
@@ -50,7 +54,8 @@ def shard_of(rank: int, world: int, frames: int, warmup: int = WARMUP_FRAMES) ->
 
 
 def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callable,
-                equal: Callable, stats: Optional[dict] = None) -> Tuple[object, object]:
+                equal: Callable, stats: Optional[dict] = None,
+                first_bad: Optional[Callable] = None) -> Tuple[object, object]:
     """Executes this rank's part of the protocol and returns (output, end_state).
 
     run_shard(first, n_frames, n_warm, state_in) -> (out, state_out): run
@@ -58,6 +63,8 @@ def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callabl
         advancing the state; state_in None = restart at `first`.
     send(state, dst) / recv(src) -> state: point-to-point state exchange.
     equal(a, b) -> bool: bitwise comparison of two state planes.
+    first_bad(k) -> int: all-reduce MIN over the ranks of k (None: the
+        sequential chain of the original protocol is used for every rank).
     """
     n_local = shard.hi - shard.lo
     if shard.warm:
@@ -67,11 +74,36 @@ def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callabl
         s_warm = None
         out, s_end = run_shard(shard.lo, n_local, 0, None)
     fixups = 0
-    # carry chain: rank r's end state is final once rank r has verified
-    for r in range(shard.world - 1):
-        if shard.rank == r:
+    world, rank = shard.world, shard.rank
+    start = 0  # first rank of the sequential fix-up chain
+    if first_bad is not None and world > 1:
+        # 3: every rank forwards its (tentative) end state at once; even /
+        # odd ordering of send and recv keeps blocking point-to-point
+        # backends deadlock-free
+        s_true = None
+        if rank % 2 == 0:
+            if rank + 1 < world:
+                send(s_end, rank + 1)
+            if rank > 0:
+                s_true = recv(rank - 1)
+        else:
+            s_true = recv(rank - 1)
+            if rank + 1 < world:
+                send(s_end, rank + 1)
+        ok = rank == 0 or (s_warm is not None and equal(s_true, s_warm))
+        start = first_bad(world if ok else rank)
+        if start >= world:  # 4: all warm states were exact
+            if stats is not None:
+                stats["fixups"] = stats.get("fixups", 0)
+            return out, s_end
+        if rank == start:  # its received state is exact (all ranks < start verified)
+            out, s_end = run_shard(shard.lo, n_local, 0, s_true)
+            fixups += 1
+    # carry chain from `start`: rank r's end state is final once r verified
+    for r in range(start, world - 1):
+        if rank == r:
             send(s_end, r + 1)
-        elif shard.rank == r + 1:
+        elif rank == r + 1:
             s_true = recv(r)
             if s_warm is None or not equal(s_true, s_warm):
                 out, s_end = run_shard(shard.lo, n_local, 0, s_true)

@@ -21,7 +21,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, frames, warmup, result_path):
+def _worker(rank, world, port, frames, warmup, result_path, parallel=False):
     import sys
     sys.path.insert(0, ROOT)
     from oracle import oracle as O
@@ -49,10 +49,15 @@ def _worker(rank, world, port, frames, warmup, result_path):
         dist.recv(t, src)
         return t.numpy()
 
+    def first_bad(k):
+        t = torch.tensor([k], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return int(t.item())
+
     stats = {}
     out, _ = run_sharded(sh, run_shard, send, recv,
                          lambda a, b: np.array_equal(a.view(np.uint32), b.view(np.uint32)),
-                         stats)
+                         stats, first_bad if parallel else None)
     # gather to rank 0
     full = [None] * world if rank == 0 else None
     dist.gather_object((sh.lo, out, stats["fixups"] if stats else 0), full, dst=0)
@@ -65,12 +70,15 @@ def _worker(rank, world, port, frames, warmup, result_path):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("parallel", [False, True])
 @pytest.mark.parametrize("world,frames,warmup,expect_fixups",
                          [(2, 40, 64, False), (2, 40, 3, True), (3, 45, 2, True),
-                          (3, 45, 48, None)])
-def test_sharded_run_is_exact(tmp_path, world, frames, warmup, expect_fixups):
+                          (3, 45, 48, None), (4, 48, 1, True), (4, 48, 30, None)])
+def test_sharded_run_is_exact(tmp_path, world, frames, warmup, expect_fixups, parallel):
+    """Sequential carry chain and the parallel verification (one exchange +
+    one all-reduce, chain only from the first failing rank)."""
     out = tmp_path / "r.npy"
-    mp.spawn(_worker, args=(world, _free_port(), frames, warmup, str(out)),
+    mp.spawn(_worker, args=(world, _free_port(), frames, warmup, str(out), parallel),
              nprocs=world, join=True)
     ok, fixups = np.load(out)
     assert ok == 1
