@@ -231,6 +231,23 @@ def main():
 
     shard = Shard(rank, world, lo, hi, warm)
     bufs = {}
+    # gray + IIR only, for the warm state the carry is verified against; it
+    # runs on a side stream while the shard's single launch (warm-up inside)
+    # runs on the main stream
+    spec12 = dict(pipe_spec, kernels=pipe_spec["kernels"][:2])
+    pipe12 = fp.Pipeline(json.dumps(spec12))
+    ex12 = fp.Executor(pipe12, fp.Plan(pipe12, fp.Device.load("b200"),
+                                       {"force_partition": "1-2"}), device=local)
+    side = torch.cuda.Stream(dev)
+    s_warm_buf = torch.empty((1, H, W), dtype=torch.float32, device=dev)
+
+    def warm_state(first, n):
+        v = video[first - (lo - warm):first - (lo - warm) + n]
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            ex12.run_range(v, n_warm=n, state_out=s_warm_buf, stream=side)
+        stream.wait_stream(side)
+        return s_warm_buf
 
     def run_shard(first, n, n_warm, state_in):
         # video holds frames [lo - warm, hi) of the full video
@@ -268,7 +285,7 @@ def main():
         # verify, fix-up re-run on mismatch (paper_1509_04394_b200/sharding.py)
         # world 2: the chain is one link anyway; beyond, verify in parallel
         run_sharded(shard, run_shard, send, recv, torch.equal, events,
-                    first_bad if world > 2 else None)
+                    first_bad if world > 2 else None, warm_state)
 
     for _ in range(args.warmup):
         step()

@@ -55,7 +55,8 @@ def shard_of(rank: int, world: int, frames: int, warmup: int = WARMUP_FRAMES) ->
 
 def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callable,
                 equal: Callable, stats: Optional[dict] = None,
-                first_bad: Optional[Callable] = None) -> Tuple[object, object]:
+                first_bad: Optional[Callable] = None,
+                warm_state: Optional[Callable] = None) -> Tuple[object, object]:
     """Executes this rank's part of the protocol and returns (output, end_state).
 
     run_shard(first, n_frames, n_warm, state_in) -> (out, state_out): run
@@ -65,9 +66,18 @@ def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callabl
     equal(a, b) -> bool: bitwise comparison of two state planes.
     first_bad(k) -> int: all-reduce MIN over the ranks of k (None: the
         sequential chain of the original protocol is used for every rank).
+    warm_state(first, n) -> state: the IIR state after n frames from a
+        fresh start at `first` (a gray+IIR-only pass).  When given, the
+        shard runs as ONE launch with its warm-up inside (n_warm = W) and the
+        warm state used for verification comes from this side computation
+        (it may run concurrently); the IIR arithmetic of both is the
+        reference's, so the two warm states are identical.
     """
     n_local = shard.hi - shard.lo
-    if shard.warm:
+    if shard.warm and warm_state is not None:
+        out, s_end = run_shard(shard.first, shard.warm + n_local, shard.warm, None)
+        s_warm = warm_state(shard.first, shard.warm)
+    elif shard.warm:
         _, s_warm = run_shard(shard.first, shard.warm, shard.warm, None)
         out, s_end = run_shard(shard.lo, n_local, 0, s_warm)
     else:

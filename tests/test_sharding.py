@@ -21,7 +21,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, frames, warmup, result_path, parallel=False):
+def _worker(rank, world, port, frames, warmup, result_path, parallel=False, single=False):
     import sys
     sys.path.insert(0, ROOT)
     from oracle import oracle as O
@@ -54,10 +54,17 @@ def _worker(rank, world, port, frames, warmup, result_path, parallel=False):
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         return int(t.item())
 
+    def warm_state(first, n):  # gray + IIR only over the warm-up frames
+        p12 = dict(pipe, kernels=pipe["kernels"][:2])
+        _, st = O.orc_chain(p12, video[first:first + n], t_out=n, return_state=True,
+                            nthreads=1)
+        return st
+
     stats = {}
     out, _ = run_sharded(sh, run_shard, send, recv,
                          lambda a, b: np.array_equal(a.view(np.uint32), b.view(np.uint32)),
-                         stats, first_bad if parallel else None)
+                         stats, first_bad if parallel else None,
+                         warm_state if single else None)
     # gather to rank 0
     full = [None] * world if rank == 0 else None
     dist.gather_object((sh.lo, out, stats["fixups"] if stats else 0), full, dst=0)
@@ -70,15 +77,16 @@ def _worker(rank, world, port, frames, warmup, result_path, parallel=False):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("parallel", [False, True])
+@pytest.mark.parametrize("parallel,single", [(False, False), (True, False), (True, True)])
 @pytest.mark.parametrize("world,frames,warmup,expect_fixups",
                          [(2, 40, 64, False), (2, 40, 3, True), (3, 45, 2, True),
                           (3, 45, 48, None), (4, 48, 1, True), (4, 48, 30, None)])
-def test_sharded_run_is_exact(tmp_path, world, frames, warmup, expect_fixups, parallel):
-    """Sequential carry chain and the parallel verification (one exchange +
-    one all-reduce, chain only from the first failing rank)."""
+def test_sharded_run_is_exact(tmp_path, world, frames, warmup, expect_fixups, parallel, single):
+    """Sequential carry chain, the parallel verification (one exchange + one
+    all-reduce, chain only from the first failing rank), and the single-launch
+    shard (warm-up inside, warm state from a gray+IIR side pass)."""
     out = tmp_path / "r.npy"
-    mp.spawn(_worker, args=(world, _free_port(), frames, warmup, str(out), parallel),
+    mp.spawn(_worker, args=(world, _free_port(), frames, warmup, str(out), parallel, single),
              nprocs=world, join=True)
     ok, fixups = np.load(out)
     assert ok == 1
