@@ -371,10 +371,13 @@ def main():
         "config": {"workload": desc, "chain": "SPEC K1..K5 (+K6 host)",
                    "partition": plan.partition, "variant": args.variant,
                    "l2": "inputs larger than L2 (1.92 GB video)",
-                   "sharding": f"T-shards, {WARMUP_FRAMES}-frame IIR warm-up"},
+                   "sharding": f"T-shards, {WARMUP_FRAMES}-frame IIR warm-up",
+                   "parallelism": f"T-shard x{world}" if world > 1 else "single GPU"},
         "mpix_per_s": fps * W * H / 1e6,
         "hbm_gbps_alg": ALG_BYTES_PER_PX * W * H * fps / 1e9,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        # rank 0's launches in the timed steps (ranks > 0 add one gray+IIR
+        # warm-state pass per step; fix-ups add a launch each)
         "gpu_launches": launches * args.steps,
         "clocks": clocks.summary(),
         "kernels": desc_ex,
