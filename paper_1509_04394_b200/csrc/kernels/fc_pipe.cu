@@ -54,9 +54,11 @@
 #define FP_NSF 4  // RGB (TMA) frame slots
 #endif
 #ifndef FP_SPECIALISE
-#define FP_SPECIALISE 0  // 1: interior / border code variants per CTA; 0: the general
-                         // (border) variant everywhere -- measured 1.5 % faster: one
-                         // code path per role keeps the instruction caches warm
+#define FP_SPECIALISE 2  // 1: interior / border variants of every role per CTA;
+                         // 0: the general (border) variant everywhere; 2: IIR /
+                         // plane roles specialised, one stencil path (measured:
+                         // 2 > 0 by 0.6 % > 1 by 1.5 % -- the stencil code must
+                         // stay single to keep the instruction caches warm)
 #endif
 #ifndef FP_LC
 #define FP_LC 2
@@ -751,14 +753,16 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   const bool in_x = bx >= 0 && bx + 127 <= a.W - 1, in_y = by >= 0 && by + R - 1 <= a.H - 1;
   const bool interior = FP_SPECIALISE && in_x && in_y;
+  // FP_SPECIALISE 2: IIR / plane roles specialised per CTA, one stencil path
+  const bool interior_iir = (FP_SPECIALISE != 0) && in_x && in_y;
   if (warp < NS) {
-    if (interior)
+    if (FP_SPECIALISE == 1 && interior)
       stencil_role<OH, false>(a, warp, lane, bx, by);
     else
       stencil_role<OH, true>(a, warp, lane, bx, by);
   } else if (warp < NS + NI && SRC_F32) {
     const int iw = warp - NS;
-    if (interior)
+    if (interior_iir)
       plane_role<OH, false, false>(a, iw, lane, bx, by);
     else if (FP_SPECIALISE && in_x)
       plane_role<OH, false, true>(a, iw, lane, bx, by);
@@ -768,7 +772,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       plane_role<OH, true, true>(a, iw, lane, bx, by);
   } else if (warp < NS + NI) {
     const int iw = warp - NS, xoff = bx - tx0;
-    if (interior)
+    if (interior_iir)
       iir_role<OH, false, false>(a, iw, lane, bx, by, xoff);
     else if (FP_SPECIALISE && in_x)
       iir_role<OH, false, true>(a, iw, lane, bx, by, xoff);

@@ -1,6 +1,7 @@
-// Tuning variant of the frame pipeline: interior / border code variants per
-// CTA (FP_SPECIALISE 1).  FUSEPLAN_PIPE_CFG=63 selects it.
-#define FP_SPECIALISE 1
+// Tuning variant of the frame pipeline: the general (border) code path in
+// every role of every CTA (FP_SPECIALISE 0).
+// FUSEPLAN_PIPE_CFG=63 selects it.
+#define FP_SPECIALISE 0
 #define FP_NF 5
 #define FP_NI 5
 #define FP_KSLACK 2
