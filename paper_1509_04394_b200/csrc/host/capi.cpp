@@ -311,33 +311,77 @@ fp_status fp_codegen(const fp_pipeline* p, const fp_device* d, const char* optio
   return guarded([&] {
     need(p && d && name && out_dir && manifest_out);
     FusionPlan fp = plan(p->p, d->d, parse_plan_options(options_json));
-    // The B200 build does not emit source text: each group maps onto a
-    // compiled sm_100a kernel; the manifest records which one.
+    // The B200 build does not generate kernel source: each group maps onto a
+    // compiled sm_100a kernel.  Per group it writes <name>_group<i>.genkernel
+    // (the reference's file name, codegen.cpp) naming that kernel, its
+    // launch-relevant plan data and the stage parameters as the kernel
+    // receives them, with the entry's __global__ signature; the manifest
+    // records the mapping.
     ordered_json m;
     m["schema_version"] = 1;
     m["name"] = name;
     m["target"] = "sm_100a";
     m["groups"] = ordered_json::array();
+    std::filesystem::create_directories(out_dir);
+    int gi = 0;
     for (const PlanGroup& g : fp.groups) {
-      std::string kernel = "host (global aggregation)";
+      ++gi;
+      std::string kernel = "fctrack::k_track (K6 centroid + Kalman, one CTA per marker)";
+      std::string src = "fc_track.cu";
+      std::vector<std::string> ops;
+      for (int id = g.first; id <= g.last; ++id)
+        ops.push_back(p->p.kernels[std::size_t(id - 1)].stencil_op);
       if (!g.global_aggregation) {
-        std::vector<std::string> ops;
-        for (int id = g.first; id <= g.last; ++id)
-          ops.push_back(p->p.kernels[std::size_t(id - 1)].stencil_op);
         using V = std::vector<std::string>;
-        if (ops == V{"rgba2gray", "iir_temporal", "gaussian", "gradient", "threshold"})
-          kernel = "fc::k_chain (F12345 streaming)";
-        else if (ops == V{"rgba2gray", "iir_temporal"})
-          kernel = "fc::k_gray_iir (F12)";
-        else if (ops == V{"gaussian", "gradient", "threshold"})
-          kernel = "fc::k_gauss_grad_thr (F345)";
-        else
-          kernel = "per-stage kernels";
+        if (ops == V{"rgba2gray", "iir_temporal", "gaussian", "gradient", "threshold"}) {
+          kernel = "fcpipe::k_chain_pipe<OH, false> (F12345 frame pipeline; exact: k_chain_exact)";
+          src = "fc_pipe.cu / fc_exact.cu";
+        } else if (ops == V{"rgba2gray", "iir_temporal"}) {
+          kernel = "k_gray_iir_stream / k_gray_iir (F12)";
+          src = "fc_f12.cu / fc_exact.cu";
+        } else if (ops == V{"gaussian", "gradient", "threshold"}) {
+          kernel = "fcpipe::k_chain_pipe<OH, true> (F345 frame pipeline; exact: k_gauss_grad_thr)";
+          src = "fc_pipe.cu / fc_exact.cu";
+        } else {
+          kernel = "per-stage kernels (k_rgba2gray, k_iir, k_gaussian<R>, k_gradient, "
+                   "k_pointwise, k_box_mean)";
+          src = "fc_exact.cu";
+        }
       }
       m["groups"].push_back({{"first", g.first}, {"last", g.last}, {"kernel", kernel}});
+      if (g.global_aggregation) continue;
+      std::ostringstream k;
+      k << "// " << name << " group " << gi << ": K" << g.first << ".." << "K" << g.last
+        << " (";
+      for (std::size_t i = 0; i < ops.size(); ++i) k << (i ? ", " : "") << ops[i];
+      k << ")\n// executed on sm_100a by " << kernel << "\n// source: "
+        << "paper_1509_04394_b200/csrc/kernels/" << src << "\n// plan: tile " << g.tile.x
+        << "x" << g.tile.y << "x" << g.tile.t << ", halo x " << g.halo.x_lo << "/"
+        << g.halo.x_hi << " y " << g.halo.y_lo << "/" << g.halo.y_hi << " t " << g.halo.t_lo
+        << "/" << g.halo.t_hi << "\n// stage parameters as passed to the kernel (fc_stage):\n"
+        << std::setprecision(9);
+      for (int id = g.first; id <= g.last; ++id) {
+        const fc_stage st = make_stage(p->p.kernels[std::size_t(id - 1)]);
+        k << "//   K" << id << " " << p->p.kernels[std::size_t(id - 1)].stencil_op;
+        if (st.op == FC_RGBA2GRAY) k << " wr=" << st.wr << " wg=" << st.wg << " wb=" << st.wb;
+        if (st.op == FC_IIR_TEMPORAL) k << " alpha=" << st.alpha;
+        if (st.op == FC_THRESHOLD)
+          k << " th=" << st.th << " white=" << st.white << " black=" << st.black;
+        if (st.op == FC_GAUSSIAN) {
+          const int dd = 2 * st.g_radius + 1;
+          k << " radius=" << st.g_radius << " taps=";
+          for (int i = 0; i < dd * dd; ++i) k << (i ? "," : "") << st.g_w[i];
+        }
+        k << "\n";
+      }
+      k << "extern \"C\" __global__ void " << name << "_group" << gi
+        << "(const void* in, void* out, int width, int height, int frames);\n";
+      write_text_file((std::filesystem::path(out_dir) /
+                       (std::string(name) + "_group" + std::to_string(gi) + ".genkernel"))
+                          .string(),
+                      k.str());
     }
     std::string text = m.dump(2) + "\n";
-    std::filesystem::create_directories(out_dir);
     write_text_file((std::filesystem::path(out_dir) / (std::string(name) + "_manifest.json"))
                         .string(),
                     text);
