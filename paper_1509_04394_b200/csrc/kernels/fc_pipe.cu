@@ -101,11 +101,32 @@ struct Args {
   unsigned off_bar, off_taps, off_queue;
   const float* state_in;
   float* state_out;
+  // Time segments (small frames): CTA b works on window b % n_windows and
+  // segment b / n_windows of seg_len output frames; chain segments s > 0
+  // restart the IIR seg_warm frames early, publish their warm state to
+  // seg_warm_out[s] and their end state to seg_end[s] for verification; a
+  // fix-up launch (fix_k != null) re-runs every window from segment *fix_k.
+  int n_windows, n_segs, seg_len, seg_warm;
+  float* seg_end;
+  float* seg_warm_out;
+  int* fix_k;
+  int* seg_k;  // main segmented launch: reset to n_segs by CTA 0 (read by verify / fix-up)
   long long* dbg;  // optional per-CTA timing (FUSEPLAN_PIPE_PROFILE), 8 slots per CTA
   int skip;        // timing experiments only (FUSEPLAN_PIPE_SKIP): 1 IIR math, 2 stencil math
   int dbg_x, dbg_y, dbg_t;  // diagnostics (FUSEPLAN_PIPE_DEBUG_PX=x,y,t): dump the
   float* dbg_px;            // recheck's 7x7 IIR neighbourhood + decision
   FastParams p;
+};
+
+// The frames one CTA processes (see Args: time segments / fix-up)
+struct Range {
+  int f0;       // first input frame (video / plane index)
+  int n;        // frames processed
+  int n_warm;   // leading warm-up frames (IIR state only)
+  int out0;     // first output frame index (relative to `out`)
+  const float* st_in;
+  float* st_out;
+  float* st_warm;  // state after the warm-up frames (segments s > 0)
 };
 
 __device__ unsigned long long g_rechecks;
@@ -192,12 +213,12 @@ __device__ __forceinline__ float2 shfl_down2(float2 v) {
 // ------------------------------------------------------------------ IIR warps
 
 template <int OH, bool BX, bool BY>
-__device__ __forceinline__ void iir_role(const Args& a, int iw, int lane, int bx, int by,
-                                         int xoff) {
+__device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw, int lane,
+                                         int bx, int by, int xoff) {
   constexpr int NP = OH + 6;               // pair-rows
   constexpr int NR = (NP + NI - 1) / NI;   // pair-rows of this warp: p = iw + NI r
   constexpr int R = 2 * OH + 6;
-  const int W = a.W, H = a.H, n = a.n_frames, n_warm = a.n_warm;
+  const int W = a.W, H = a.H, n = rg.n, n_warm = rg.n_warm;
   const int cplane = R * BWB;
   const int xl = bx + 4 * lane;
   const uint32_t k4b = a.p.k4b;
@@ -223,7 +244,7 @@ __device__ __forceinline__ void iir_role(const Args& a, int iw, int lane, int bx
 
   // exact IIR state of the lane's cells: v[r][j] = {row p, row p + OH}, col 4L + j
   float2 v[NR][4];
-  const bool fresh = a.state_in == nullptr;
+  const bool fresh = rg.st_in == nullptr;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const int p = iw + NI * r;
@@ -233,12 +254,27 @@ __device__ __forceinline__ void iir_role(const Args& a, int iw, int lane, int bx
         v[r][j] = make_float2(0.0f, 0.0f);
       } else {
         const int cx = clampi(xl + j, 0, W - 1);
-        v[r][j].x = a.state_in[(long long)clampi(by + p, 0, H - 1) * W + cx];
-        v[r][j].y = a.state_in[(long long)clampi(by + p + OH, 0, H - 1) * W + cx];
+        v[r][j].x = rg.st_in[(long long)clampi(by + p, 0, H - 1) * W + cx];
+        v[r][j].y = rg.st_in[(long long)clampi(by + p + OH, 0, H - 1) * W + cx];
       }
     }
   }
 
+  // the lane's output cells (rows 3 .. OH+2 of both halves) -> a state plane
+  auto write_state = [&](float* dst) {
+    if (!dst || lane < 1 || lane > 30 || xl >= W) return;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int p = iw + NI * r;
+      if (p < 3 || p > OH + 2) continue;  // output rows of both halves
+      const int yx = by + p, yy = by + p + OH;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (yx < H) dst[(long long)yx * W + xl + j] = v[r][j].x;
+        if (yy < H) dst[(long long)yy * W + xl + j] = v[r][j].y;
+      }
+    }
+  };
   const unsigned smem0 = smem_u32(fp_smem);
   int rslot = 0, islot = 0;
   unsigned rpar = 0, ipar = 0;
@@ -292,7 +328,10 @@ __device__ __forceinline__ void iir_role(const Args& a, int iw, int lane, int bx
       rslot = 0;
       rpar ^= 1u;
     }
-    if (t < n_warm) continue;  // warm-up frame: state only
+    if (t < n_warm) {  // warm-up frame: state only
+      if (t == n_warm - 1) write_state(rg.st_warm);
+      continue;
+    }
     if (a.dbg) {
       const long long c0 = clk();
       wait_phase(bar_iir_empty(a, islot), ipar ^ 1u);
@@ -322,29 +361,18 @@ __device__ __forceinline__ void iir_role(const Args& a, int iw, int lane, int bx
     atomicAdd(reinterpret_cast<unsigned long long*>(d + 4), (unsigned long long)w_slot);
     atomicAdd(reinterpret_cast<unsigned long long*>(d + 6), (unsigned long long)(clk() - t_begin));
   }
-  if (a.state_out && lane >= 1 && lane <= 30 && xl < W) {
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const int p = iw + NI * r;
-      if (p < 3 || p > OH + 2) continue;  // output rows of both halves
-      const int yx = by + p, yy = by + p + OH;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (yx < H) a.state_out[(long long)yx * W + xl + j] = v[r][j].x;
-        if (yy < H) a.state_out[(long long)yy * W + xl + j] = v[r][j].y;
-      }
-    }
-  }
+  write_state(rg.st_out);
 }
 
 // F345 mode: the "IIR" warps load the frame's f32 input plane window (TMA
 // slot, row-major, 512 B per row) and repack it into the pair-row layout; no
 // state.  Window cells outside the video take the clamped row / edge column.
 template <int OH, bool BX, bool BY>
-__device__ __forceinline__ void plane_role(const Args& a, int iw, int lane, int bx, int by) {
+__device__ __forceinline__ void plane_role(const Args& a, const Range& rg, int iw, int lane,
+                                           int bx, int by) {
   constexpr int NP = OH + 6;
   constexpr int NR = (NP + NI - 1) / NI;
-  const int W = a.W, H = a.H, n = a.n_frames;
+  const int W = a.W, H = a.H, n = rg.n;
   const int xl = bx + 4 * lane;
   int colb = 16 * lane, comp = -1;  // byte offset of the lane's 4 floats in a slot row
   if (BX && (xl < 0 || xl > W - 1)) {
@@ -460,10 +488,11 @@ using ic = std::integral_constant<int, N>;
 // Uncertain values are queued in shared memory (record: pair-row, lane,
 // 4 value bits) and recomputed exactly after the march.
 template <int OH, bool BORDER>
-__device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, int bx, int by) {
+__device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int sw, int lane,
+                                             int bx, int by) {
   constexpr int NP = OH + 6;
   const int W = a.W, H = a.H;
-  const int n_out = a.n_frames - a.n_warm;
+  const int n_out = rg.n - rg.n_warm;
   const long long hw = (long long)W * H;
   const float mlo = a.p.mlo_n, band = a.p.band_n;  // scaled domain (normalised taps)
   const float g0 = a.p.g0, g1 = a.p.g1;
@@ -496,7 +525,7 @@ __device__ __forceinline__ void stencil_role(const Args& a, int sw, int lane, in
       wait_phase(bar_iir_full(a, slot), par);
     }
     const unsigned base = smem0 + a.off_iir + slot * a.iir_stride;
-    unsigned char* o = a.out + (long long)u * hw;
+    unsigned char* o = a.out + (long long)(rg.out0 + u) * hw;
     unsigned char* ox = o + (long long)(by + 3) * W + xl;  // pair-row 3, top half
     unsigned char* oy = ox + (long long)OH * W;              // bottom half
     int nq = 0;                                              // queued records
@@ -726,7 +755,36 @@ __global__ void __launch_bounds__(NTHR, 1)
     k_chain_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
   constexpr int R = 2 * OH + 6;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int strip = blockIdx.x % a.strips, band = blockIdx.x / a.strips;
+  const int win = blockIdx.x % a.n_windows, seg = blockIdx.x / a.n_windows;
+  const int strip = win % a.strips, band = win / a.strips;
+  // this CTA's frames (Args: time segments / fix-up)
+  Range rg{0, a.n_frames, a.n_warm, 0, a.state_in, a.state_out, nullptr};
+  {
+    const long long hwl = (long long)a.W * a.H;
+    const int n_out = a.n_frames - a.n_warm;
+    if (a.fix_k) {  // fix-up: re-run every window from the first wrong segment
+      const int k = *a.fix_k;
+      if (k >= a.n_segs) return;  // all segment warm states were exact
+      rg.out0 = k * a.seg_len;
+      rg.f0 = rg.out0;
+      rg.n = n_out - rg.out0;
+      rg.n_warm = 0;
+      rg.st_in = a.seg_end + (long long)(k - 1) * hwl;
+    } else if (a.n_segs > 1) {
+      rg.out0 = seg * a.seg_len;
+      const int e = min(rg.out0 + a.seg_len, n_out);
+      rg.f0 = max(0, rg.out0 - a.seg_warm);
+      rg.n_warm = rg.out0 - rg.f0;
+      rg.n = e - rg.f0;
+      rg.st_in = nullptr;
+      rg.st_out = seg < a.n_segs - 1 ? (a.seg_end ? a.seg_end + (long long)seg * hwl : nullptr)
+                                     : a.state_out;
+      rg.st_warm = seg > 0 && a.seg_warm_out ? a.seg_warm_out + (long long)seg * hwl : nullptr;
+    }
+    if (rg.n <= 0) return;
+    if (a.fix_k == nullptr && a.n_segs > 1 && blockIdx.x == 0 && tid == 0 && a.seg_k)
+      *a.seg_k = a.n_segs;  // verification result slot (reset before verify runs)
+  }
   const int x0 = strip * SW, y0 = band * (2 * OH);
   const int bx = x0 - 4, by = y0 - 3;
   const int tx0 = bx >= 0 ? (bx & ~15) : -((-bx + 15) & ~15);
@@ -757,43 +815,44 @@ __global__ void __launch_bounds__(NTHR, 1)
   const bool interior_iir = (FP_SPECIALISE != 0) && in_x && in_y;
   if (warp < NS) {
     if (FP_SPECIALISE == 1 && interior)
-      stencil_role<OH, false>(a, warp, lane, bx, by);
+      stencil_role<OH, false>(a, rg, warp, lane, bx, by);
     else
-      stencil_role<OH, true>(a, warp, lane, bx, by);
+      stencil_role<OH, true>(a, rg, warp, lane, bx, by);
   } else if (warp < NS + NI && SRC_F32) {
     const int iw = warp - NS;
     if (interior_iir)
-      plane_role<OH, false, false>(a, iw, lane, bx, by);
+      plane_role<OH, false, false>(a, rg, iw, lane, bx, by);
     else if (FP_SPECIALISE && in_x)
-      plane_role<OH, false, true>(a, iw, lane, bx, by);
+      plane_role<OH, false, true>(a, rg, iw, lane, bx, by);
     else if (FP_SPECIALISE && in_y)
-      plane_role<OH, true, false>(a, iw, lane, bx, by);
+      plane_role<OH, true, false>(a, rg, iw, lane, bx, by);
     else
-      plane_role<OH, true, true>(a, iw, lane, bx, by);
+      plane_role<OH, true, true>(a, rg, iw, lane, bx, by);
   } else if (warp < NS + NI) {
     const int iw = warp - NS, xoff = bx - tx0;
     if (interior_iir)
-      iir_role<OH, false, false>(a, iw, lane, bx, by, xoff);
+      iir_role<OH, false, false>(a, rg, iw, lane, bx, by, xoff);
     else if (FP_SPECIALISE && in_x)
-      iir_role<OH, false, true>(a, iw, lane, bx, by, xoff);
+      iir_role<OH, false, true>(a, rg, iw, lane, bx, by, xoff);
     else if (FP_SPECIALISE && in_y)
-      iir_role<OH, true, false>(a, iw, lane, bx, by, xoff);
+      iir_role<OH, true, false>(a, rg, iw, lane, bx, by, xoff);
     else
-      iir_role<OH, true, true>(a, iw, lane, bx, by, xoff);
+      iir_role<OH, true, true>(a, rg, iw, lane, bx, by, xoff);
   } else if (lane == 0) {
     // producer: frame t -> RGB slot t % NSF once the IIR warps released it
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
     int slot = 0;
     unsigned par = 0;
-    for (int t = 0; t < a.n_frames; ++t) {
+    for (int t = 0; t < rg.n; ++t) {
       wait_phase(bar_rgb_empty(a, slot), par ^ 1u);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(bar_rgb_full(a, slot), a.rgb_bytes);
       if (SRC_F32)  // f32 plane window: x start bx is a multiple of 4 (16-byte aligned)
-        tma_load_3d(fp_smem + slot * a.rgb_stride, &tmap, bar_rgb_full(a, slot), bx, by, t);
+        tma_load_3d(fp_smem + slot * a.rgb_stride, &tmap, bar_rgb_full(a, slot), bx, by,
+                    rg.f0 + t);
       else
         tma_load_3d(fp_smem + slot * a.rgb_stride, &tmap, bar_rgb_full(a, slot), tx0, by,
-                    4 * t);
+                    4 * (rg.f0 + t));
       if (++slot == NSF) {
         slot = 0;
         par ^= 1u;
@@ -846,20 +905,30 @@ KernelFn kernel_for(int oh, bool src_f32) {
 }
 
 struct PipePlan {
-  int W = -1, H = -1, dev = -1;
-  int oh = 0, strips = 0, bands = 0;
+  int W = -1, H = -1, dev = -1, frames = -1, force_oh = 0, force_segs = 0;
+  bool segs_ok = false;
+  int oh = 0, strips = 0, bands = 0, n_segs = 1, seg_len = 0;
   size_t smem = 0;
 };
 
-// Every CTA marches the whole video; an SM's time is ~ (CTAs it runs) x (its
-// CTA's pair-rows).  Pick OH minimising the busiest SM's pair-rows; ties go to
-// the larger window (less halo).  FUSEPLAN_PIPE_OH forces the choice.
-bool choose(int W, int H, int dev, bool src_f32, PipePlan* pp) {
+constexpr int SEG_WARM = 64;  // IIR warm-up of a time segment (48 suffices)
+
+// Every CTA marches its frames; an SM's time is ~ (CTAs it runs) x (pair-rows
+// of a window) x (frames of a CTA, warm-up frames at ~0.4 of a full frame).
+// Small frames leave SMs idle with one CTA per window, so the frames may be
+// split into time segments (chain: restarted SEG_WARM frames early and
+// verified, see Args).  Pick (OH, segments) minimising the busiest SM's load;
+// ties go to the larger window.  FUSEPLAN_PIPE_OH / FUSEPLAN_PIPE_SEGS force.
+int env_int(const char* name, int dflt) {
+  const char* env = std::getenv(name);
+  return env ? std::atoi(env) : dflt;
+}
+
+bool choose(int W, int H, int frames, bool segs_ok, int dev, bool src_f32, int force,
+            int force_segs, PipePlan* pp) {
   int sms = 0, optin = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  int force = 0;
-  if (const char* env = std::getenv("FUSEPLAN_PIPE_OH")) force = std::atoi(env);
   const int strips = (W + SW - 1) / SW;
   double best = 1e300;
   const int ohs[] = {
@@ -868,6 +937,7 @@ bool choose(int W, int H, int dev, bool src_f32, PipePlan* pp) {
 #undef FP_ITEM
   };
   const bool dbg = std::getenv("FUSEPLAN_DEBUG") != nullptr;
+  const double warm_cost = src_f32 ? 0.0 : 0.4;
   for (int oh : ohs) {
     if (force && oh != force) continue;
     const size_t smem = layout(oh, src_f32, nullptr);
@@ -886,18 +956,46 @@ bool choose(int W, int H, int dev, bool src_f32, PipePlan* pp) {
       continue;
     }
     const long long bands = (H + 2 * oh - 1) / (2 * oh);
-    const long long ctas = strips * bands;
-    const long long per_busiest = (ctas + sms - 1) / sms;
-    const double cost = double(per_busiest) * (oh + 6) - 1e-3 * oh;
-    if (cost < best) {
-      best = cost;
-      pp->oh = oh;
-      pp->strips = strips;
-      pp->bands = int(bands);
-      pp->smem = smem;
+    const long long windows = strips * bands;
+    const int max_segs = segs_ok ? 16 : 1;
+    for (int segs = 1; segs <= max_segs; ++segs) {
+      if (force_segs && segs_ok && segs != force_segs) continue;
+      const long long L = (frames + segs - 1) / segs;
+      if (!force_segs && segs > 1 && !src_f32 && L < 2 * SEG_WARM) break;  // warm-up dominates
+      if (segs > 1 && L < 2) break;
+      const long long ctas = windows * segs;
+      const long long per_busiest = (ctas + sms - 1) / sms;
+      const double cta_frames = double(L) + (segs > 1 ? warm_cost * SEG_WARM : 0.0);
+      const double cost = double(per_busiest) * (oh + 6) * cta_frames * (1.0 - 1e-4 * oh);
+      if (cost < best) {
+        best = cost;
+        pp->oh = oh;
+        pp->strips = strips;
+        pp->bands = int(bands);
+        pp->smem = smem;
+        pp->n_segs = segs;
+        pp->seg_len = int(L);
+      }
     }
   }
+  if (dbg && best < 1e300)
+    std::fprintf(stderr, "fc_pipe choose: -> oh=%d segs=%d seg_len=%d\n", pp->oh, pp->n_segs,
+                 pp->seg_len);
   return best < 1e300;
+}
+
+// Chain segments: first segment s >= 1 whose warm state differs from the end
+// state of segment s-1 (bitwise), atomically minimised into *k.
+__global__ void k_verify_segments(const float* __restrict__ warm, const float* __restrict__ end,
+                                  long long hw, int n_segs, int* k) {
+  const long long total = (long long)(n_segs - 1) * hw;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = int(i / hw) + 1;
+    const long long px = i % hw;
+    if (__float_as_uint(warm[s * hw + px]) != __float_as_uint(end[(s - 1) * hw + px]))
+      atomicMin(k, s);
+  }
 }
 
 // Shared launcher of both modes (src_f32: F345 from f32 planes).
@@ -908,12 +1006,25 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
   cudaGetDevice(&dev);
   static thread_local PipePlan caches[2];
   PipePlan& cache = caches[src_f32 ? 1 : 0];
-  if (cache.W != d.width || cache.H != d.height || cache.dev != dev) {
+  // time segments only for self-contained launches (no carried state in,
+  // no launch-level warm-up): their CTAs may restart the IIR anywhere
+  const bool segs_ok = src_f32 || (state_in == nullptr && n_warm == 0);
+  const int force_oh = env_int("FUSEPLAN_PIPE_OH", 0);
+  const int force_segs = env_int("FUSEPLAN_PIPE_SEGS", 0);
+  if (cache.W != d.width || cache.H != d.height || cache.dev != dev ||
+      cache.frames != d.frames || cache.segs_ok != segs_ok || cache.force_oh != force_oh ||
+      cache.force_segs != force_segs) {
     PipePlan pp;
-    if (!choose(d.width, d.height, dev, src_f32, &pp)) return -1;
+    if (!choose(d.width, d.height, d.frames - n_warm, segs_ok, dev, src_f32, force_oh,
+                force_segs, &pp))
+      return -1;
+    pp.force_oh = force_oh;
+    pp.force_segs = force_segs;
     pp.W = d.width;
     pp.H = d.height;
     pp.dev = dev;
+    pp.frames = d.frames;
+    pp.segs_ok = segs_ok;
     cache = pp;
   }
   Args a;
@@ -925,6 +1036,29 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
   a.n_frames = d.frames;
   a.n_warm = n_warm;
   a.strips = cache.strips;
+  a.n_windows = cache.strips * cache.bands;
+  a.n_segs = cache.n_segs;
+  a.seg_len = cache.seg_len;
+  a.seg_warm = src_f32 ? 0 : env_int("FUSEPLAN_PIPE_SEG_WARM", SEG_WARM);
+  const long long hwl = (long long)d.width * d.height;
+  const bool verify = !src_f32 && cache.n_segs > 1;
+  if (verify) {  // per-segment end / warm state planes and the verdict slot
+    static thread_local float* seg_buf = nullptr;
+    static thread_local int* seg_k = nullptr;
+    static thread_local size_t seg_cap = 0;
+    const size_t need = size_t(2 * cache.n_segs) * size_t(hwl);
+    if (need > seg_cap) {
+      if (seg_buf) cudaFree(seg_buf);
+      seg_buf = nullptr;
+      seg_cap = 0;
+      if (cudaMalloc(&seg_buf, need * sizeof(float)) != cudaSuccess) return int(cudaGetLastError());
+      seg_cap = need;
+    }
+    if (!seg_k && cudaMalloc(&seg_k, sizeof(int)) != cudaSuccess) return int(cudaGetLastError());
+    a.seg_end = seg_buf;
+    a.seg_warm_out = seg_buf + size_t(cache.n_segs) * size_t(hwl);
+    a.seg_k = seg_k;
+  }
   a.state_in = state_in;
   a.state_out = state_out;
   a.p = fp;
@@ -942,7 +1076,7 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
   if (src_f32 ? !plane_tensor_map(&map, in, d, 128, 2 * cache.oh + 6)
               : !rgb_tensor_map(&map, in, d, BWB, 2 * cache.oh + 6))
     return -1;
-  const int grid = cache.strips * cache.bands;
+  const int grid = cache.strips * cache.bands * cache.n_segs;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool profile = std::getenv("FUSEPLAN_PIPE_PROFILE") != nullptr;
   if (profile) {
@@ -950,7 +1084,18 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
     cudaMemsetAsync(a.dbg, 0, sizeof(long long) * 8 * grid, st);
   }
   kernel_for(cache.oh, src_f32)<<<grid, NTHR, cache.smem, st>>>(map, a);
-  const int rc = int(cudaGetLastError());
+  int rc = int(cudaGetLastError());
+  if (rc == 0 && verify) {
+    // verify the segment seams, then (device-side decision) re-run every
+    // window from the first wrong segment; a no-op launch when all matched
+    k_verify_segments<<<296, 256, 0, st>>>(a.seg_warm_out, a.seg_end, hwl, cache.n_segs,
+                                           a.seg_k);
+    Args f = a;
+    f.fix_k = a.seg_k;
+    f.seg_k = nullptr;
+    kernel_for(cache.oh, src_f32)<<<cache.strips * cache.bands, NTHR, cache.smem, st>>>(map, f);
+    rc = int(cudaGetLastError());
+  }
   if (profile && a.dbg) {  // per-CTA span and per-role wait shares
     std::vector<long long> h(size_t(8) * grid);
     cudaStreamSynchronize(st);

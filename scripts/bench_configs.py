@@ -161,10 +161,10 @@ def file_config(name, W, H, F, path="/tmp/fuseplan_cfg4.fpvd"):
 def main():
     which = sys.argv[1:] or ["1", "2", "3", "4", "5"]
     if "1" in which:
-        device_config("cfg1", 192, 432, 600, "plan")
+        device_config("cfg1", 192, 432, 600, "plan", check_frames=600)
     if "2" in which:
         for part in ["1,2,3,4,5", "plan", "1-2,3-5", "1-5"]:
-            device_config("cfg2", 192, 432, 600, part)
+            device_config("cfg2", 192, 432, 600, part, check_frames=600)
         device_config("cfg2", 192, 432, 600, "1-5", variant="exact")
     if "3" in which:
         device_config("cfg3", 800, 600, 1000, "1-5")

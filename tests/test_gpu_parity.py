@@ -315,3 +315,35 @@ def test_sharding_protocol_on_device_emulated(fp, cuda, oracle, world, warmup):
     np.testing.assert_array_equal(got, oracle.orc_chain(pipe, video.cpu().numpy()))
     if warmup <= 2:
         assert fixups["fixups"] >= 1
+
+
+@pytest.mark.parametrize("part", ["1-5", "1-2,3-5"])
+@pytest.mark.parametrize("segs,seg_warm", [(0, None), (4, None), (3, 1), (7, 2), (16, 64)])
+@pytest.mark.parametrize("shape", [(192, 432, 300), (64, 48, 170)])
+def test_pipe_time_segments_exact(fp, cuda, oracle, monkeypatch, part, segs, seg_warm, shape):
+    """Time-segmented pipe launches (small frames: several CTAs per window,
+    each over its own run of frames).  All-fused segments restart the IIR
+    seg_warm frames early; a tiny seg_warm makes the seam verification fail
+    and the device-side fix-up re-run from the first wrong segment.  Output
+    and the carried end state stay bit-exact, with forced rechecks on top."""
+    import torch
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    if segs:
+        monkeypatch.setenv("FUSEPLAN_PIPE_SEGS", str(segs))
+    if seg_warm is not None:
+        monkeypatch.setenv("FUSEPLAN_PIPE_SEG_WARM", str(seg_warm))
+    monkeypatch.setenv("FUSEPLAN_PIPE_BAND_SCALE", "30")
+    W, H, F = shape
+    pipe = spec_chain(W, H, F)
+    v = hash_video_u8(F, 4, H, W, 40 + segs)
+    want = oracle.orc_chain(pipe, v)
+    p = fp.Pipeline(json.dumps(pipe))
+    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": part}),
+                     variant="fast" if part == "1-5" else "auto")
+    vt = torch.from_numpy(v).to(cuda)
+    st = torch.empty((1, H, W), device=cuda)
+    out = ex.run_range(vt[:F - 9], state_out=st)
+    tail = ex.run_range(vt[F - 9:], state_in=st)
+    torch.cuda.synchronize()
+    got = torch.cat([out, tail]).cpu().numpy().astype(np.float32)
+    np.testing.assert_array_equal(got, want)
