@@ -143,6 +143,53 @@ __global__ void __launch_bounds__(NT) k_gray_iir_stream(const __grid_constant__ 
     }
 }
 
+// Small frames: no per-CTA ring, each thread owns 4 pixels (one 32-bit word
+// per channel, float4 stores) and issues the R, G, B loads of U frames
+// before using any of them.
+constexpr int SMALL_NT = 128;
+
+template <int SMALL_U>
+__global__ void __launch_bounds__(SMALL_NT) k_gray_iir_small(Args a) {
+  const long long q = blockIdx.x * (long long)SMALL_NT + threadIdx.x;
+  const long long hw = a.hw, p = 4 * q, cs = hw / 4;
+  if (p >= hw) return;
+  const uint32_t k4b = 0x4B000000u;
+  const bool fresh = a.state_in == nullptr;
+  float st[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  if (!fresh) {
+    const float4 v = *reinterpret_cast<const float4*>(a.state_in + p);
+    st[0] = v.x, st[1] = v.y, st[2] = v.z, st[3] = v.w;
+  }
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(a.video) + q;
+  const int n = a.n_frames, ics = int(cs);  // small frames: in-batch offsets fit 32 bits
+  for (int t = 0; t < n; t += SMALL_U) {
+    uint32_t w[SMALL_U][3];
+    const uint32_t* bp = src + (long long)t * 4 * cs;
+#pragma unroll
+    for (int u = 0; u < SMALL_U; ++u)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[u][c] = t + u < n ? __ldg(bp + (u * 4 + c) * ics) : 0u;
+#pragma unroll
+    for (int u = 0; u < SMALL_U; ++u) {
+      if (t + u >= n) break;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float x = __fadd_rn(__fadd_rn(wp(w[u][0], k, a.wr, a.wrm, k4b),
+                                            wp(w[u][1], k, a.wg, a.wgm, k4b)),
+                                  wp(w[u][2], k, a.wb, a.wbm, k4b));
+        // simulator.cpp:57-62
+        st[k] = (fresh && t + u == 0) ? x
+                                       : __fadd_rn(__fmul_rn(a.alpha, x), __fmul_rn(a.beta, st[k]));
+      }
+      if (t + u >= a.n_warm)
+        *reinterpret_cast<float4*>(a.out + (long long)(t + u - a.n_warm) * hw + p) =
+            make_float4(st[0], st[1], st[2], st[3]);
+    }
+  }
+  if (a.state_out)
+    *reinterpret_cast<float4*>(a.state_out + p) = make_float4(st[0], st[1], st[2], st[3]);
+}
+
 }  // namespace fcf12
 
 using namespace fcf12;
@@ -155,19 +202,13 @@ extern "C" int fc_gray_iir_stream(const fc_stage* sg, const fc_stage* si, const 
   const long long hw = (long long)d.width * d.height;
   if (in_type != FC_U8 || hw % 16 != 0) return -1;
   if (reinterpret_cast<uintptr_t>(video) % 16 || reinterpret_cast<uintptr_t>(out) % 16) return -1;
+  if (reinterpret_cast<uintptr_t>(state_in) % 16 || reinterpret_cast<uintptr_t>(state_out) % 16)
+    return -1;
   if (std::getenv("FUSEPLAN_F12_LEGACY")) return -1;
   // Small frames (< 256 k pixels) leave each CTA a few hundred pixels and the
-  // per-frame ring handshake dominates; the per-pixel kernel is faster there
-  // (measured: 192x432 0.14 vs 0.23 ms, 800x600 0.38 ms faster here).
-  if (hw < 256 * 1024 && !std::getenv("FUSEPLAN_F12_STREAM")) return -1;
+  // per-frame ring handshake dominates (192x432: 0.23 ms vs 0.14 ms for the
+  // old per-pixel kernel): they take k_gray_iir_small instead.
   if (hw == 0 || d.frames == 0) return 0;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  long long per = (hw + sms - 1) / sms;
-  per = (per + 15) / 16 * 16;
-  if (per > MAXPX) per = MAXPX;
-  const int grid = int((hw + per - 1) / per);
   Args a;
   a.video = static_cast<const uint8_t*>(video);
   a.out = out;
@@ -176,7 +217,6 @@ extern "C" int fc_gray_iir_stream(const fc_stage* sg, const fc_stage* si, const 
   a.hw = hw;
   a.n_frames = d.frames;
   a.n_warm = n_warm;
-  a.px_per_cta = int(per);
   a.wr = sg->wr;
   a.wg = sg->wg;
   a.wb = sg->wb;
@@ -185,6 +225,24 @@ extern "C" int fc_gray_iir_stream(const fc_stage* sg, const fc_stage* si, const 
   a.wbm = -sg->wb * 8388608.0f;
   a.alpha = si->alpha;
   a.beta = 1.0f - si->alpha;  // host float arithmetic == the reference's
+  if (hw < 256 * 1024 && !std::getenv("FUSEPLAN_F12_STREAM")) {
+    const long long threads = hw / 4;
+    const int grid = int((threads + SMALL_NT - 1) / SMALL_NT);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // batch depth 16 frames (measured at 192x432x600: U = 8 / 12 / 16 / 32 ->
+    // 134 / 121 / 110 / 138 us; 2-pixel threads 142 us, the old per-pixel
+    // kernel 140 us)
+    k_gray_iir_small<16><<<grid, SMALL_NT, 0, st>>>(a);
+    return int(cudaGetLastError());
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long per = (hw + sms - 1) / sms;
+  per = (per + 15) / 16 * 16;
+  if (per > MAXPX) per = MAXPX;
+  const int grid = int((hw + per - 1) / per);
+  a.px_per_cta = int(per);
   const size_t smem = size_t(DEPTH) * 3 * MAXPX + 2 * DEPTH * 8;
   static bool attr = false;
   if (!attr) {

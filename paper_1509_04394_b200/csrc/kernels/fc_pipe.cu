@@ -129,6 +129,10 @@ struct Range {
   float* st_warm;  // state after the warm-up frames (segments s > 0)
 };
 
+// The CTA's Range lives in shared memory: the roles read each field where
+// they use it, so the segment bookkeeping costs no registers in the marches.
+__shared__ Range fp_rg;
+
 __device__ unsigned long long g_rechecks;
 extern __shared__ __align__(128) unsigned char fp_smem[];
 
@@ -807,6 +811,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     a.dbg[8 * blockIdx.x] = (long long)now;
     a.dbg[8 * blockIdx.x + 7] = (interior_flag(a, bx, by, 2 * OH + 6));
   }
+  if (tid == 0) fp_rg = rg;
   __syncthreads();  // the only CTA-wide barrier: roles run decoupled from here
 
   const bool in_x = bx >= 0 && bx + 127 <= a.W - 1, in_y = by >= 0 && by + R - 1 <= a.H - 1;
@@ -815,44 +820,45 @@ __global__ void __launch_bounds__(NTHR, 1)
   const bool interior_iir = (FP_SPECIALISE != 0) && in_x && in_y;
   if (warp < NS) {
     if (FP_SPECIALISE == 1 && interior)
-      stencil_role<OH, false>(a, rg, warp, lane, bx, by);
+      stencil_role<OH, false>(a, fp_rg, warp, lane, bx, by);
     else
-      stencil_role<OH, true>(a, rg, warp, lane, bx, by);
+      stencil_role<OH, true>(a, fp_rg, warp, lane, bx, by);
   } else if (warp < NS + NI && SRC_F32) {
     const int iw = warp - NS;
     if (interior_iir)
-      plane_role<OH, false, false>(a, rg, iw, lane, bx, by);
+      plane_role<OH, false, false>(a, fp_rg, iw, lane, bx, by);
     else if (FP_SPECIALISE && in_x)
-      plane_role<OH, false, true>(a, rg, iw, lane, bx, by);
+      plane_role<OH, false, true>(a, fp_rg, iw, lane, bx, by);
     else if (FP_SPECIALISE && in_y)
-      plane_role<OH, true, false>(a, rg, iw, lane, bx, by);
+      plane_role<OH, true, false>(a, fp_rg, iw, lane, bx, by);
     else
-      plane_role<OH, true, true>(a, rg, iw, lane, bx, by);
+      plane_role<OH, true, true>(a, fp_rg, iw, lane, bx, by);
   } else if (warp < NS + NI) {
     const int iw = warp - NS, xoff = bx - tx0;
     if (interior_iir)
-      iir_role<OH, false, false>(a, rg, iw, lane, bx, by, xoff);
+      iir_role<OH, false, false>(a, fp_rg, iw, lane, bx, by, xoff);
     else if (FP_SPECIALISE && in_x)
-      iir_role<OH, false, true>(a, rg, iw, lane, bx, by, xoff);
+      iir_role<OH, false, true>(a, fp_rg, iw, lane, bx, by, xoff);
     else if (FP_SPECIALISE && in_y)
-      iir_role<OH, true, false>(a, rg, iw, lane, bx, by, xoff);
+      iir_role<OH, true, false>(a, fp_rg, iw, lane, bx, by, xoff);
     else
-      iir_role<OH, true, true>(a, rg, iw, lane, bx, by, xoff);
+      iir_role<OH, true, true>(a, fp_rg, iw, lane, bx, by, xoff);
   } else if (lane == 0) {
     // producer: frame t -> RGB slot t % NSF once the IIR warps released it
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
     int slot = 0;
     unsigned par = 0;
-    for (int t = 0; t < rg.n; ++t) {
+    const int n = fp_rg.n, f0 = fp_rg.f0;
+    for (int t = 0; t < n; ++t) {
       wait_phase(bar_rgb_empty(a, slot), par ^ 1u);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(bar_rgb_full(a, slot), a.rgb_bytes);
       if (SRC_F32)  // f32 plane window: x start bx is a multiple of 4 (16-byte aligned)
         tma_load_3d(fp_smem + slot * a.rgb_stride, &tmap, bar_rgb_full(a, slot), bx, by,
-                    rg.f0 + t);
+                    f0 + t);
       else
         tma_load_3d(fp_smem + slot * a.rgb_stride, &tmap, bar_rgb_full(a, slot), tx0, by,
-                    4 * (rg.f0 + t));
+                    4 * (f0 + t));
       if (++slot == NSF) {
         slot = 0;
         par ^= 1u;

@@ -9,3 +9,6 @@ ncu -i gpurun_out/ev_full.ncu-rep --page raw --csv > gpurun_out/ev_full_raw.csv 
 ncu -i gpurun_out/ev_full.ncu-rep --page details --csv > gpurun_out/ev_full_details.csv 2>&1
 ncu -i gpurun_out/ev_full.ncu-rep --page source --print-source sass --csv > gpurun_out/ev_full_sass.csv 2>&1
 cat gpurun_out/ev_tests.log; tail -c 3000 gpurun_out/ev_bench.json
+timeout 900 python scripts/bench_configs.py 1 2 3 5 > gpurun_out/ev_configs.jsonl 2> gpurun_out/ev_configs.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_cfg1_launches.csv python scripts/bench_configs.py 1 > /dev/null 2>&1
+tail -c 1500 gpurun_out/ev_configs.jsonl
