@@ -7,8 +7,9 @@ frames/s and Mpixel/s of the fused chain on 800x600 video; HBM GB/s vs peak).
 One step = one pass of the chain over the whole synthetic video of the
 configuration (config 3: 800x600x1000 u8 RGBA, SPEC chain
 rgba2gray -> iir(0.5) -> gaussian(r2,s1) -> gradient -> threshold(128)),
-the video already resident in HBM.  N > 1 (torchrun): the video is sharded
-along T; every rank but the first warms its IIR up over 64 frames before its
+the video already resident in HBM.  N > 1 (torchrun): an N x 1000-frame
+video (--scaling weak, default; --scaling strong splits the 1000 frames) is
+sharded along T; every rank but the first warms its IIR up over 64 frames before its
 shard, then every rank sends its IIR carry to the next (NCCL send/recv, all
 at once), verifies the one it received bit for bit, and one all-reduce finds
 the first wrong warm state (fix-up chain only from there) -- all inside the
@@ -181,6 +182,9 @@ def main():
     ap.add_argument("--variant", default="auto", choices=["auto", "exact", "fast"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = F frames per GPU (N x F-frame video), "
+                         "strong = the F-frame video split N ways")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: carry planes staged through the host (lets N ranks "
                          "share one GPU for testing)")
@@ -207,12 +211,14 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
-    # T-shard of this rank (weak scaling would keep F per GPU; the BASELINE
-    # config fixes the video, so N GPUs split its frames: strong scaling)
-    lo, hi = rank * F // world, (rank + 1) * F // world
+    # T-shard of this rank.  weak (default): every GPU owns F frames of an
+    # N x F-frame video (per-GPU work fixed, the SPEC chain's throughput
+    # scaling); strong: the F-frame video itself is split N ways
+    FT = F * world if args.scaling == "weak" else F
+    lo, hi = rank * FT // world, (rank + 1) * FT // world
     warm = min(WARMUP_FRAMES, lo)
     n_local = hi - lo
-    pipe_spec = fp.spec_chain(W, H, F, kalman=True)
+    pipe_spec = fp.spec_chain(W, H, F, kalman=True)  # per-launch chain (run_range sizes)
     pipe = fp.Pipeline(json.dumps(pipe_spec))
     part = args.partition
     opts = None if part == "plan" else {"force_partition": part + ",6"}
@@ -306,10 +312,10 @@ def main():
         clocks.__exit__(None, None, None)
     ms = start.elapsed_time(end) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device="cpu" if host_stage else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    fps = F / (ms / 1e3)
+    fps = FT / (ms / 1e3)
 
     # dominant kernel timed alone on the launching stream (one launch = the
     # fused chain over this rank's frames)
@@ -342,6 +348,43 @@ def main():
         e2e = {"value": F / dt, "unit": "frames/s",
                "h2d_bytes_per_step": 3 * W * H * F, "d2h_bytes_per_step": W * H * F,
                "ms_per_step": dt * 1e3, "matches_device_run": bool(ok)}
+    elif world > 1 and args.e2e_steps > 0:
+        # every rank: its shard's frames (warm-up frames included) from
+        # pinned host memory, the sharded step, its mask back to the host;
+        # wall clock between barriers, max over ranks
+        host_video = torch.empty(tuple(video.shape), dtype=torch.uint8, pin_memory=True)
+        host_video.copy_(video.cpu())
+        host_mask = torch.empty(tuple(mask.shape), dtype=torch.uint8, pin_memory=True)
+        ref_mask = mask.cpu()
+
+        def e2e_step():  # whole RGBA frames: one contiguous DMA (A plane unused)
+            video.copy_(host_video, non_blocking=True)
+            step()
+            host_mask.copy_(mask, non_blocking=True)
+            torch.cuda.synchronize()
+
+        e2e_step()
+        ts = []
+        for _ in range(args.e2e_steps):
+            dist.barrier()
+            t0 = time.perf_counter()
+            e2e_step()
+            dist.barrier()
+            ts.append(time.perf_counter() - t0)
+        rdev = "cpu" if host_stage else dev
+        t = torch.tensor([float(np.median(ts))], device=rdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+        ok = torch.tensor([int(torch.equal(host_mask, ref_mask))], device=rdev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        in_frames = sum((r + 1) * FT // world - r * FT // world + min(WARMUP_FRAMES, r * FT // world)
+                        for r in range(world))
+        e2e = {"value": FT / dt, "unit": "frames/s",
+               "h2d_bytes_per_step": 4 * W * H * in_frames,
+               "d2h_bytes_per_step": W * H * FT,
+               "ms_per_step": dt * 1e3, "matches_device_run": bool(ok.item()),
+               "note": "per rank: H2D of its shard (+ warm-up frames), sharded step, "
+                       "D2H of its mask; max over ranks"}
 
     if rank != 0:
         if world > 1:
@@ -365,10 +408,13 @@ def main():
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "u8 in / f32 (FP64 gaussian recheck) / u8 mask",
         "data": "synthetic counter-hash u8 RGBA video (device-generated)",
-        "config": {"workload": desc, "chain": "SPEC K1..K5 (+K6 host)",
+        "config": {"workload": desc if world == 1 else
+                   (f"{desc} per GPU ({W}x{H}x{FT} video, T-sharded)" if args.scaling == "weak"
+                    else f"{desc} T-sharded {world} ways"),
+                   "chain": "SPEC K1..K5 (+K6 host)",
                    "partition": plan.partition, "variant": args.variant,
                    "l2": "inputs larger than L2 (1.92 GB video)",
                    "sharding": f"T-shards, {WARMUP_FRAMES}-frame IIR warm-up",
