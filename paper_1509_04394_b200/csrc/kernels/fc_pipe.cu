@@ -63,6 +63,9 @@
 #ifndef FP_LC
 #define FP_LC 2
 #endif
+#ifndef FP_IIR_TMA
+#define FP_IIR_TMA 1  // all-fused mode: the TMA producer warp is also an IIR warp
+#endif
 #ifndef FP_NF
 #define FP_NF 5
 #define FP_NI 5
@@ -82,6 +85,10 @@ constexpr int WPF = 4 / LC; // stencil warps per frame
 constexpr int NF = FP_NF;   // frames in flight in the stencil
 constexpr int NS = WPF * NF;  // stencil warps
 constexpr int NI = FP_NI;   // IIR warps
+// warps sharing the IIR rows in the all-fused mode: with FP_IIR_TMA the
+// producer warp takes rows too (lane 0 still issues the TMA copies), so the
+// slowest IIR warp has ceil(NP / (NI + 1)) pair-rows instead of ceil(NP / NI)
+constexpr int NIE = NI + (FP_IIR_TMA ? 1 : 0);
 constexpr int NWARP = NS + NI + 1;
 constexpr int NTHR = NWARP * 32;
 constexpr int K = NF + FP_KSLACK;  // IIR frame slots (slack: frames the IIR may run ahead)
@@ -218,9 +225,10 @@ __device__ __forceinline__ float2 shfl_down2(float2 v) {
 
 template <int OH, bool BX, bool BY>
 __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw, int lane,
-                                         int bx, int by, int xoff) {
+                                         int bx, int by, int xoff, const CUtensorMap* tmap,
+                                         int tx0) {
   constexpr int NP = OH + 6;               // pair-rows
-  constexpr int NR = (NP + NI - 1) / NI;   // pair-rows of this warp: p = iw + NI r
+  constexpr int NR = (NP + NIE - 1) / NIE; // pair-rows of this warp: p = iw + NIE r
   constexpr int R = 2 * OH + 6;
   const int W = a.W, H = a.H, n = rg.n, n_warm = rg.n_warm;
   const int cplane = R * BWB;
@@ -232,7 +240,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
   int rowx[NR], rowy[NR];  // RGB slot byte offsets of the two window rows
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    const int p = iw + NI * r;
+    const int p = iw + NIE * r;
     const int rx = p, ry = p + OH;
     rowx[r] = (BY ? clampi(by + rx, 0, H - 1) - by : rx) * BWB;
     rowy[r] = (BY ? clampi(by + ry, 0, H - 1) - by : ry) * BWB;
@@ -251,7 +259,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
   const bool fresh = rg.st_in == nullptr;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    const int p = iw + NI * r;
+    const int p = iw + NIE * r;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (fresh || p >= NP) {
@@ -269,7 +277,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
     if (!dst || lane < 1 || lane > 30 || xl >= W) return;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      const int p = iw + NI * r;
+      const int p = iw + NIE * r;
       if (p < 3 || p > OH + 2) continue;  // output rows of both halves
       const int yx = by + p, yy = by + p + OH;
 #pragma unroll
@@ -284,7 +292,30 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
   unsigned rpar = 0, ipar = 0;
   long long w_rgb = 0, w_slot = 0;
   const long long t_begin = clk();
+  // FP_IIR_TMA: lane 0 of warp NI keeps NSF - 1 frames of RGB in flight; the
+  // slot of frame t + NSF - 1 is that of frame t - 1, which every IIR warp
+  // (this one included) has released before this warp starts frame t
+  const bool prod = FP_IIR_TMA && iw == NI && lane == 0;
+  int pslot = 0;
+  unsigned ppar = 0;
+  const int f0 = rg.f0;
+  auto issue = [&](int tp) {
+    wait_phase(bar_rgb_empty(a, pslot), ppar ^ 1u);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar_rgb_full(a, pslot), a.rgb_bytes);
+    tma_load_3d(fp_smem + pslot * a.rgb_stride, tmap, bar_rgb_full(a, pslot), tx0, by,
+                4 * (f0 + tp));
+    if (++pslot == NSF) {
+      pslot = 0;
+      ppar ^= 1u;
+    }
+  };
+  if (prod) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+    for (int tp = 0; tp < NSF - 1 && tp < n; ++tp) issue(tp);
+  }
   for (int t = 0; t < n; ++t) {
+    if (prod && t + NSF - 1 < n) issue(t + NSF - 1);
     if (a.dbg) {
       const long long c0 = clk();
       wait_phase(bar_rgb_full(a, rslot), rpar);
@@ -297,7 +328,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
       constexpr bool FIRST = decltype(first_tag)::value;
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        if (iw + NI * r >= NP) continue;
+        if (iw + NIE * r >= NP) continue;
         uint32_t wx[3], wy[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -346,7 +377,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
     const unsigned base = smem0 + a.off_iir + islot * a.iir_stride;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      const int p = iw + NI * r;
+      const int p = iw + NIE * r;
       if (p >= NP) continue;
       sts128(base + p * PROW + so0, v[r][0], v[r][1]);
       sts128(base + p * PROW + so1, v[r][2], v[r][3]);
@@ -796,10 +827,10 @@ __global__ void __launch_bounds__(NTHR, 1)
   if (tid == 0) {
     for (int i = 0; i < NSF; ++i) {
       mbar_init(bar_rgb_full(a, i), 1);
-      mbar_init(bar_rgb_empty(a, i), NI);  // one arrive per IIR warp
+      mbar_init(bar_rgb_empty(a, i), SRC_F32 ? NI : NIE);  // one arrive per IIR warp
     }
     for (int i = 0; i < K; ++i) {
-      mbar_init(bar_iir_full(a, i), NI);
+      mbar_init(bar_iir_full(a, i), SRC_F32 ? NI : NIE);
       mbar_init(bar_iir_empty(a, i), WPF);  // the frame's stencil warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -833,16 +864,16 @@ __global__ void __launch_bounds__(NTHR, 1)
       plane_role<OH, true, false>(a, fp_rg, iw, lane, bx, by);
     else
       plane_role<OH, true, true>(a, fp_rg, iw, lane, bx, by);
-  } else if (warp < NS + NI) {
+  } else if (warp < NS + NIE && !SRC_F32) {
     const int iw = warp - NS, xoff = bx - tx0;
     if (interior_iir)
-      iir_role<OH, false, false>(a, fp_rg, iw, lane, bx, by, xoff);
+      iir_role<OH, false, false>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
     else if (FP_SPECIALISE && in_x)
-      iir_role<OH, false, true>(a, fp_rg, iw, lane, bx, by, xoff);
+      iir_role<OH, false, true>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
     else if (FP_SPECIALISE && in_y)
-      iir_role<OH, true, false>(a, fp_rg, iw, lane, bx, by, xoff);
+      iir_role<OH, true, false>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
     else
-      iir_role<OH, true, true>(a, fp_rg, iw, lane, bx, by, xoff);
+      iir_role<OH, true, true>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
   } else if (lane == 0) {
     // producer: frame t -> RGB slot t % NSF once the IIR warps released it
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
