@@ -50,6 +50,9 @@
 #ifndef FP_WAIT_HINT
 #define FP_WAIT_HINT ", %2"  // suspend-time hint operand of try_wait ("" = none)
 #endif
+#ifndef FP_WAIT_SLEEP
+#define FP_WAIT_SLEEP 0  // > 0: poll with plain try_wait + __nanosleep(ns) back-off
+#endif
 #ifndef FP_NSF
 #define FP_NSF 4  // RGB (TMA) frame slots
 #endif
@@ -164,6 +167,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Blocking wait: the suspend-time hint parks the warp in the barrier unit
 // instead of spinning through issue slots the working warps need.
 __device__ __forceinline__ void wait_phase(uint64_t* bar, unsigned phase) {
+#if FP_WAIT_SLEEP
+  // variant: plain try_wait, then a software back-off between polls
+  for (;;) {
+    unsigned ok;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (ok) return;
+    __nanosleep(FP_WAIT_SLEEP);
+  }
+#endif
   asm volatile(
       "{\n"
       ".reg .pred p;\n"

@@ -1,10 +1,10 @@
 // Tuning variant of the frame pipeline (FUSEPLAN_PIPE_CFG=63 selects it):
-// separate TMA producer warp (the IIR rows shared by the 5 IIR warps only).
+// mbarrier waits poll with a software back-off instead of the suspend hint.
 #define FP_SPECIALISE 2
 #define FP_NF 5
 #define FP_NI 5
 #define FP_KSLACK 2
-#define FP_IIR_TMA 0
+#define FP_WAIT_SLEEP 64
 #define FP_NAMESPACE fcpipe63
 #define FP_ENTRY fc_chain_pipe63
 #define FP_F345_ENTRY fc_f345_pipe63

@@ -1,0 +1,6 @@
+# one full ncu capture of the headline pipe kernel (800x600x1000) + raw / sass exports
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chain_pipe -c 1 -o gpurun_out/np_full python scripts/tile_sweep.py 800 600 1000 > /dev/null 2>&1
+ncu -i gpurun_out/np_full.ncu-rep --page raw --csv > gpurun_out/np_full_raw.csv 2>&1
+ncu -i gpurun_out/np_full.ncu-rep --page source --print-source sass --csv > gpurun_out/np_full_sass.csv 2>&1
+ls -la gpurun_out/np_full*
