@@ -49,7 +49,10 @@ extern "C" int fc_fused_chain(const fc_stage* sgray, const fc_stage* si,
                                     out_type, d, n_warm, state_in, state_out, stream)
                    : pipe(sgray, si, sg, sthr, video, in_type, gray_in, out, out_type, d,
                           n_warm, state_in, state_out, stream);
-    if (rc != -1 || variant == 2) return rc;  // -1: parameters not covered
+    if (rc != -1) return rc;  // -1: parameters not covered
+    if (variant == 2)  // frames lower than 6 rows: the certified tile march
+      return fc_chain_tile(sgray, si, sg, sthr, video, in_type, gray_in, out, out_type, d,
+                           n_warm, state_in, state_out, stream);
   }
   return fc_chain_exact(sgray, si, sg, sthr, video, in_type, gray_in, out,
                         out_type, d, n_warm, state_in, state_out, stream);

@@ -591,10 +591,15 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
     // and Sobel at pair-row p - 5 (G rows p-6..p-4) are mutually
     // independent, so the scheduler overlaps the loads and the three
     // dependency chains of a step.
-    auto step = [&](auto pm_t, auto h_t, auto v_t, auto s_t, int p) {
+    // YB: the video's top row (1: window row 3 of band 0, the first Sobel
+    // step) or bottom row (2: the last band ends at row H - 1, so it is the
+    // bottom half of the last Sobel step) may be in this step's Sobel rows;
+    // every other step needs no y clamp
+    auto step = [&](auto pm_t, auto h_t, auto v_t, auto s_t, auto yb_t, int p) {
       constexpr int PM = decltype(pm_t)::value;  // p % 6
       constexpr bool DO_H = decltype(h_t)::value, DO_V = decltype(v_t)::value;
       constexpr bool DO_S = decltype(s_t)::value;
+      constexpr int YB = decltype(yb_t)::value;
       // ---- horizontal pass of pair-row p
       if constexpr (DO_H) {
         const unsigned rb = base + p * PROW;
@@ -626,12 +631,8 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
 #pragma unroll
         for (int j = 0; j < LC; ++j) {
           float2 gm = gr[(QM + 5) % 6][j], gc = gr[QM][j], gp = gr[(QM + 1) % 6][j];
-          if (BORDER) {  // predicated selects: the step stays one basic block
-            if (yx == 0) gm.x = gc.x;
-            if (yy == 0) gm.y = gc.y;
-            if (yx == H - 1) gp.x = gc.x;
-            if (yy == H - 1) gp.y = gc.y;
-          }
+          if (YB == 1 && yx == 0) gm.x = gc.x;      // predicated selects: the step
+          if (YB == 2 && yy == H - 1) gp.y = gc.y;  // stays one basic block
           s2[j] = __fadd2_rn(__ffma2_rn(splat(2.0f), gc, gm), gp);
           d2[j] = __ffma2_rn(splat(-1.0f), gm, gp);
         }
@@ -654,8 +655,8 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
           const float2 ngx = f2(-gx.x, -gx.y), ngy = f2(-gy.x, -gy.y);
           dm[j] = __ffma2_rn(ngx, gx, __ffma2_rn(ngy, gy, splat(mlo)));
         }
-        const bool okx = outl && (!BORDER || yx < H);
-        const bool oky = outl && (!BORDER || yy < H);
+        // rows are inside the video: the last band is aligned to end at H - 1
+        const bool okx = outl, oky = outl;
         if constexpr (LC == 2) {
           if (okx) *reinterpret_cast<uint16_t*>(ox) = uint16_t(pack_neg2(dm[0].x, dm[1].x));
           if (oky) *reinterpret_cast<uint16_t*>(oy) = uint16_t(pack_neg2(dm[0].y, dm[1].y));
@@ -696,33 +697,36 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
     // Steps p = 0 .. NP + 1: H while p < NP, V for 5 <= p <= NP, Sobel for
     // 8 <= p <= NP + 1.  Prologue p < 8, a rolled loop of 6-step bodies,
     // then a compile-time tail.
-    step(ic<0>{}, T, F, F, 0);
-    step(ic<1>{}, T, F, F, 1);
-    step(ic<2>{}, T, F, F, 2);
-    step(ic<3>{}, T, F, F, 3);
-    step(ic<4>{}, T, F, F, 4);
-    step(ic<5>{}, T, T, F, 5);
-    step(ic<0>{}, T, T, F, 6);
-    step(ic<1>{}, T, T, F, 7);
+    const auto Y0 = ic<0>{};
+    step(ic<0>{}, T, F, F, Y0, 0);
+    step(ic<1>{}, T, F, F, Y0, 1);
+    step(ic<2>{}, T, F, F, Y0, 2);
+    step(ic<3>{}, T, F, F, Y0, 3);
+    step(ic<4>{}, T, F, F, Y0, 4);
+    step(ic<5>{}, T, T, F, Y0, 5);
+    step(ic<0>{}, T, T, F, Y0, 6);
+    step(ic<1>{}, T, T, F, Y0, 7);
+    step(ic<2>{}, T, T, T, ic<1>{}, 8);  // Sobel row 3: the video's top row in band 0
+    flush(3, 1);
 #pragma unroll 1
-    for (int p = 8; p + 6 <= NP; p += 6) {  // p % 6 == 2 at the top
-      step(ic<2>{}, T, T, T, p);
-      step(ic<3>{}, T, T, T, p + 1);
-      step(ic<4>{}, T, T, T, p + 2);
-      step(ic<5>{}, T, T, T, p + 3);
-      step(ic<0>{}, T, T, T, p + 4);
-      step(ic<1>{}, T, T, T, p + 5);
+    for (int p = 9; p + 6 <= NP; p += 6) {  // p % 6 == 3 at the top
+      step(ic<3>{}, T, T, T, Y0, p);
+      step(ic<4>{}, T, T, T, Y0, p + 1);
+      step(ic<5>{}, T, T, T, Y0, p + 2);
+      step(ic<0>{}, T, T, T, Y0, p + 3);
+      step(ic<1>{}, T, T, T, Y0, p + 4);
+      step(ic<2>{}, T, T, T, Y0, p + 5);
       flush(p - 5, BODY);
     }
-    constexpr int PT = 8 + 6 * ((NP - 8) / 6);  // tail: full steps PT .. NP - 1
-    if constexpr (NP - PT >= 1) step(ic<2>{}, T, T, T, PT);
-    if constexpr (NP - PT >= 2) step(ic<3>{}, T, T, T, PT + 1);
-    if constexpr (NP - PT >= 3) step(ic<4>{}, T, T, T, PT + 2);
-    if constexpr (NP - PT >= 4) step(ic<5>{}, T, T, T, PT + 3);
-    if constexpr (NP - PT >= 5) step(ic<0>{}, T, T, T, PT + 4);
+    constexpr int PT = 9 + 6 * ((NP - 9) / 6);  // tail: full steps PT .. NP - 1
+    if constexpr (NP - PT >= 1) step(ic<3>{}, T, T, T, Y0, PT);
+    if constexpr (NP - PT >= 2) step(ic<4>{}, T, T, T, Y0, PT + 1);
+    if constexpr (NP - PT >= 3) step(ic<5>{}, T, T, T, Y0, PT + 2);
+    if constexpr (NP - PT >= 4) step(ic<0>{}, T, T, T, Y0, PT + 3);
+    if constexpr (NP - PT >= 5) step(ic<1>{}, T, T, T, Y0, PT + 4);
     if constexpr (NP - PT >= 1) flush(PT - 5, NP - PT);  // <= 5 rows per record
-    step(ic<NP % 6>{}, F, T, T, NP);
-    step(ic<(NP + 1) % 6>{}, F, F, T, NP + 1);
+    step(ic<NP % 6>{}, F, T, T, Y0, NP);
+    step(ic<(NP + 1) % 6>{}, F, F, T, ic<2>{}, NP + 1);  // bottom row of the last band
     flush(NP - 5, 2);
 
     // ---- exact recheck of the queued uncertain values (rare)
@@ -838,7 +842,12 @@ __global__ void __launch_bounds__(NTHR, 1)
     if (a.fix_k == nullptr && a.n_segs > 1 && blockIdx.x == 0 && tid == 0 && a.seg_k)
       *a.seg_k = a.n_segs;  // verification result slot (reset before verify runs)
   }
-  const int x0 = strip * SW, y0 = band * (2 * OH);
+  // the last band ends exactly at row H - 1 (it overlaps the band above it;
+  // both write identical values): the y clamps of the stencil march then
+  // sit at compile-time steps (choose() keeps 2 OH <= H)
+  const int bands = a.n_windows / a.strips;
+  const int x0 = strip * SW,
+            y0 = band == bands - 1 ? max(0, a.H - 2 * OH) : band * (2 * OH);
   const int bx = x0 - 4, by = y0 - 3;
   const int tx0 = bx >= 0 ? (bx & ~15) : -((-bx + 15) & ~15);
   double* taps = reinterpret_cast<double*>(fp_smem + a.off_taps);
@@ -996,7 +1005,7 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, bool src_f32, int f
   for (int oh : ohs) {
     if (force && oh != force) continue;
     const size_t smem = layout(oh, src_f32, nullptr);
-    if (smem > size_t(optin)) continue;
+    if (smem > size_t(optin) || 2 * oh > H) continue;  // the last band must fit the video
     KernelFn fn = kernel_for(oh, src_f32);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));

@@ -347,3 +347,25 @@ def test_pipe_time_segments_exact(fp, cuda, oracle, monkeypatch, part, segs, seg
     torch.cuda.synchronize()
     got = torch.cat([out, tail]).cpu().numpy().astype(np.float32)
     np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("oh", [3, 4, 5, 8, 10, 12, 15])
+@pytest.mark.parametrize("part", ["1-5", "1-2,3-5"])
+@pytest.mark.parametrize("shape", [(256, 131, 6), (144, 31, 5), (64, 30, 4)])
+def test_pipe_every_window_height_exact(fp, cuda, oracle, monkeypatch, oh, part, shape):
+    """Every window height, on frame heights that are not multiples of it: the
+    last band is shifted up to end at the video's bottom row (overlapping the
+    band above), so the y clamps of the march sit at fixed steps.  Bit-exact
+    with widened certification bands (forced rechecks)."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    W, H, F = shape
+    if 2 * oh > H:
+        pytest.skip("window taller than the video")
+    monkeypatch.setenv("FUSEPLAN_PIPE_OH", str(oh))
+    monkeypatch.setenv("FUSEPLAN_PIPE_BAND_SCALE", "100")
+    pipe = spec_chain(W, H, F)
+    v = hash_video_u8(F, 4, H, W, 70 + oh)
+    want = oracle.orc_chain(pipe, v)
+    out, _ = run(fp, pipe, v, {"force_partition": part},
+                 variant="fast" if part == "1-5" else "auto", torch_dev=cuda)
+    np.testing.assert_array_equal(out, want)
