@@ -25,6 +25,16 @@ mismatch on 800x600 data).
 `run_shard` is the compute: (frames, n_warm, state_in) -> (output, state_out)
 on this rank.  In production it is the sm_100a executor (fp_exec_run_range
 over NCCL-backed torch.distributed); tests plug in the CPU oracle over gloo.
+
+Temporal windows (box_mean with radius_t): with R the
+chain's cumulative temporal radius, rank g also computes the R frames on each
+side of its shard (its "context"; the video itself is replicated or readable
+by every rank, so these halo frames need no transfer) and keeps only its own
+frames -- a range run clamps its temporal windows at the range ends, which is
+exact at the video's ends and only disturbs the discarded halo frames
+elsewhere.  The carried IIR state is then the one before rank g+1's context
+start (hi - R), computed by a gray+IIR-only pass (`advance`), because the
+full chain cannot be split there without clamping a temporal window.
 """
 from __future__ import annotations
 
@@ -41,22 +51,38 @@ class Shard:
     lo: int
     hi: int
     warm: int
+    frames: int = 0   # video length (0: unknown, no temporal halo)
+    t_halo: int = 0   # cumulative temporal radius R of the chain
+
+    @property
+    def ctx_lo(self) -> int:
+        """First frame whose chain output this rank computes (halo included)."""
+        return max(0, self.lo - self.t_halo)
+
+    @property
+    def ctx_hi(self) -> int:
+        return min(self.frames, self.hi + self.t_halo) if self.t_halo else self.hi
 
     @property
     def first(self) -> int:
         """First frame this rank reads (warm-up included)."""
-        return self.lo - self.warm
+        return self.ctx_lo - self.warm
 
 
-def shard_of(rank: int, world: int, frames: int, warmup: int = WARMUP_FRAMES) -> Shard:
+def shard_of(rank: int, world: int, frames: int, warmup: int = WARMUP_FRAMES,
+             t_halo: int = 0) -> Shard:
     lo, hi = rank * frames // world, (rank + 1) * frames // world
-    return Shard(rank, world, lo, hi, min(warmup, lo))
+    if t_halo and world > 1 and (frames // world) < t_halo:
+        raise ValueError("shards must be at least as long as the temporal halo")
+    ctx_lo = max(0, lo - t_halo)
+    return Shard(rank, world, lo, hi, min(warmup, ctx_lo), frames, t_halo)
 
 
 def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callable,
                 equal: Callable, stats: Optional[dict] = None,
                 first_bad: Optional[Callable] = None,
-                warm_state: Optional[Callable] = None) -> Tuple[object, object]:
+                warm_state: Optional[Callable] = None,
+                advance: Optional[Callable] = None) -> Tuple[object, object]:
     """Executes this rank's part of the protocol and returns (output, end_state).
 
     run_shard(first, n_frames, n_warm, state_in) -> (out, state_out): run
@@ -72,7 +98,12 @@ def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callabl
         warm state used for verification comes from this side computation
         (it may run concurrently); the IIR arithmetic of both is the
         reference's, so the two warm states are identical.
+    advance(first, n, state_in) -> state: gray+IIR state after n frames from
+        state_in (None = fresh); required when shard.t_halo > 0.
     """
+    if shard.t_halo:
+        return _run_sharded_halo(shard, run_shard, send, recv, equal, stats, first_bad,
+                                 advance)
     n_local = shard.hi - shard.lo
     if shard.warm and warm_state is not None:
         out, s_end = run_shard(shard.first, shard.warm + n_local, shard.warm, None)
@@ -117,6 +148,67 @@ def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callabl
             s_true = recv(r)
             if s_warm is None or not equal(s_true, s_warm):
                 out, s_end = run_shard(shard.lo, n_local, 0, s_true)
+                fixups += 1
+    if stats is not None:
+        stats["fixups"] = stats.get("fixups", 0) + fixups
+    return out, s_end
+
+
+def _run_sharded_halo(shard: Shard, run_shard: Callable, send: Callable, recv: Callable,
+                      equal: Callable, stats: Optional[dict], first_bad: Optional[Callable],
+                      advance: Callable) -> Tuple[object, object]:
+    """run_sharded for chains with temporal windows (module docstring).
+
+    advance(first, n, state_in) -> the gray+IIR state after frames
+    [first, first + n) from state_in (None: a fresh start at `first`)."""
+    if advance is None:
+        raise ValueError("temporal halos need the gray+IIR `advance` callback")
+    world, rank = shard.world, shard.rank
+    c_lo, c_hi = shard.ctx_lo, shard.ctx_hi
+    keep = slice(shard.lo - c_lo, shard.hi - c_lo)
+    # the carry point: the state before rank g+1's context start
+    nxt = shard_of(rank + 1, world, shard.frames, shard.warm, shard.t_halo) \
+        if rank + 1 < world else None
+    c_next = nxt.ctx_lo if nxt is not None else None
+
+    def compute(s_start):
+        out, _ = run_shard(c_lo, c_hi - c_lo, 0, s_start)
+        s_end = None
+        if c_next is not None:
+            s_end = advance(c_lo, c_next - c_lo, s_start) if c_next > c_lo else s_start
+        return out[keep], s_end
+
+    s_warm = advance(shard.first, shard.warm, None) if shard.warm else None
+    out, s_end = compute(s_warm)
+    fixups = 0
+    start = 0
+    if first_bad is not None and world > 1:
+        s_true = None
+        if rank % 2 == 0:
+            if rank + 1 < world:
+                send(s_end, rank + 1)
+            if rank > 0:
+                s_true = recv(rank - 1)
+        else:
+            s_true = recv(rank - 1)
+            if rank + 1 < world:
+                send(s_end, rank + 1)
+        ok = rank == 0 or (s_warm is not None and equal(s_true, s_warm))
+        start = first_bad(world if ok else rank)
+        if start >= world:
+            if stats is not None:
+                stats["fixups"] = stats.get("fixups", 0)
+            return out, s_end
+        if rank == start:
+            out, s_end = compute(s_true)
+            fixups += 1
+    for r in range(start, world - 1):
+        if rank == r:
+            send(s_end, r + 1)
+        elif rank == r + 1:
+            s_true = recv(r)
+            if s_warm is None or not equal(s_true, s_warm):
+                out, s_end = compute(s_true)
                 fixups += 1
     if stats is not None:
         stats["fixups"] = stats.get("fixups", 0) + fixups

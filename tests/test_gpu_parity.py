@@ -317,6 +317,57 @@ def test_sharding_protocol_on_device_emulated(fp, cuda, oracle, world, warmup):
         assert fixups["fixups"] >= 1
 
 
+@pytest.mark.parametrize("world,warmup", [(2, 64), (3, 2), (4, 64), (4, 1)])
+@pytest.mark.parametrize("opts", [None, {"force_partition": "1-2,3,4-6"}])
+def test_sharding_temporal_halo_on_device_emulated(fp, cuda, oracle, world, warmup, opts):
+    """T-shards of a chain with a temporal box_mean window (SURVEY 8(f)
+    rank 3) on the device executor: each rank runs its context (R = 2 halo
+    frames each side, temporal windows clamped at the range ends by the range
+    run), keeps its own frames, and carries the gray+IIR state taken before the
+    next rank's context.  Bit-exact with the whole-video reference."""
+    import torch
+    from paper_1509_04394_b200.fuseplan import hash_video_u8
+    from paper_1509_04394_b200.sharding import run_sharded, shard_of
+    W, H, F = 96, 40, 60
+    ks = [{"name": "g", "stencil_op": "rgba2gray"},
+          {"name": "i", "stencil_op": "iir_temporal", "params": {"alpha": 0.5}},
+          {"name": "b", "stencil_op": "box_mean",
+           "params": {"radius_x": 1, "radius_y": 1, "radius_t": 2}},
+          {"name": "s", "stencil_op": "gaussian", "params": {"radius": 2, "sigma": 1.0}},
+          {"name": "d", "stencil_op": "gradient"},
+          {"name": "t", "stencil_op": "threshold", "params": {"th": 24.0}}]
+    pipe = {"video": {"width": W, "height": H, "frames": F, "channels": 4}, "kernels": ks}
+    vnp = hash_video_u8(F, 4, H, W, 91)
+    video = torch.from_numpy(vnp).to(cuda)
+    p = fp.Pipeline(json.dumps(pipe))
+    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), opts))
+    p12 = fp.Pipeline(json.dumps(dict(pipe, kernels=ks[:2])))
+    ex12 = fp.Executor(p12, fp.Plan(p12, fp.Device.load("b200"), {"force_partition": "1-2"}))
+    mailbox, outs, fixups = {}, {}, {"fixups": 0}
+
+    def run_shard(first, n, n_warm, state_in):
+        return ex.run_range(video[first:first + n], n_warm=n_warm, state_in=state_in), None
+
+    def advance(first, n, state_in):
+        st = torch.empty((1, H, W), device=cuda)
+        ex12.run_range(video[first:first + n], n_warm=n, state_in=state_in, state_out=st)
+        return st
+
+    for rank in range(world):
+        sh = shard_of(rank, world, F, warmup, t_halo=2)
+        out, _ = run_sharded(sh, run_shard,
+                             lambda s, dst: mailbox.__setitem__(dst, s.clone()),
+                             lambda src: mailbox.pop(sh.rank),
+                             torch.equal, fixups, advance=advance)
+        outs[rank] = out
+    torch.cuda.synchronize()
+    got = torch.cat([outs[r] for r in range(world)]).cpu().numpy().astype(np.float32)
+    want = oracle.orc_run_sequential(pipe, vnp.astype(np.float32))[-1]
+    np.testing.assert_array_equal(got, want)
+    if warmup <= 2:
+        assert fixups["fixups"] >= 1
+
+
 @pytest.mark.parametrize("part", ["1-5", "1-2,3-5"])
 @pytest.mark.parametrize("segs,seg_warm", [(0, None), (4, None), (3, 1), (7, 2), (16, 64)])
 @pytest.mark.parametrize("shape", [(192, 432, 300), (64, 48, 170)])
