@@ -72,6 +72,13 @@ __device__ __forceinline__ float magic_r(uint32_t w, uint32_t k4b) {
   return __uint_as_float(r);
 }
 
+// magic_r with a per-lane selector (0x7440 + byte index) in a register
+__device__ __forceinline__ float magic_rs(uint32_t w, uint32_t k4b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(k4b), "r"(sel));
+  return __uint_as_float(r);
+}
+
 // 0xFF where nd < 0, else 0, for four values -> one word: PRMT's
 // sign-replicate mode (selector nibble 8 + byte) on byte 3 of each float.
 __device__ __forceinline__ uint32_t pack_neg(float a, float b, float c, float d) {

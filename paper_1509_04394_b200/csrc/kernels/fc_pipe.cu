@@ -47,6 +47,21 @@
 
 // Warp-role counts (fc_pipe_cfg*.cu re-include this file with other values
 // under another namespace / entry name for tuning comparisons).
+#ifndef FP_NF
+// the shipped layout: one stencil warp per frame (4-column lanes, 168
+// registers), 6 frames in flight, 5 IIR warps + the producer warp (12 warps),
+// 3 TMA slots, 8 IIR slots (measured 940 k vs 904 k frames/s for two 2-column
+// warps per frame, 5 frames, 16 warps at 128 registers)
+#define FP_LC 4
+#define FP_NF 6
+#define FP_NI 5
+#define FP_KSLACK 2
+#define FP_NSF 3
+#define FP_NAMESPACE fcpipe
+#define FP_ENTRY fc_chain_pipe
+#define FP_F345_ENTRY fc_f345_pipe
+#define FP_RECHECKS fc_pipe_recheck_count
+#endif
 #ifndef FP_WAIT_HINT
 #define FP_WAIT_HINT ", %2"  // suspend-time hint operand of try_wait ("" = none)
 #endif
@@ -68,15 +83,6 @@
 #endif
 #ifndef FP_IIR_TMA
 #define FP_IIR_TMA 1  // all-fused mode: the TMA producer warp is also an IIR warp
-#endif
-#ifndef FP_NF
-#define FP_NF 5
-#define FP_NI 5
-#define FP_KSLACK 2
-#define FP_NAMESPACE fcpipe
-#define FP_ENTRY fc_chain_pipe
-#define FP_F345_ENTRY fc_f345_pipe
-#define FP_RECHECKS fc_pipe_recheck_count
 #endif
 
 namespace FP_NAMESPACE {
@@ -264,11 +270,15 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
     rowy[r] = (BY ? clampi(by + ry, 0, H - 1) - by : ry) * BWB;
   }
   int coloff = xoff + 4 * lane;
-  unsigned sel = 0x3210u;
+  // magic-float PRMT selectors of the lane's 4 cells: byte j of the word, or
+  // (lanes left / right of the video) the edge byte in every cell -- a
+  // register selector, so the x clamp costs no instruction per frame
+  uint32_t msel[4] = {0x7440u, 0x7441u, 0x7442u, 0x7443u};
   if (BX && (xl < 0 || xl > W - 1)) {
     const int edge = xl < 0 ? 0 : W - 1;
     coloff = (edge & ~3) - bx + xoff;
-    sel = unsigned(edge & 3) * 0x1111u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) msel[j] = 0x7440u + unsigned(edge & 3);
   }
   const unsigned so0 = chunk_off(2 * lane), so1 = chunk_off(2 * lane + 1);
 
@@ -352,22 +362,20 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
         for (int c = 0; c < 3; ++c) {
           wx[c] = *reinterpret_cast<const uint32_t*>(f + c * cplane + rowx[r] + coloff);
           wy[c] = *reinterpret_cast<const uint32_t*>(f + c * cplane + rowy[r] + coloff);
-          if (BX) {
-            wx[c] = __byte_perm(wx[c], 0, sel);
-            wy[c] = __byte_perm(wy[c], 0, sel);
-          }
         }
+#define FP_MG(W_, J) (BX ? magic_rs(W_, k4b, msel[J]) : magic_r<J>(W_, k4b))
 #define FP_CELL(J)                                                                          \
   {                                                                                         \
     const float2 g = __fadd2_rn(                                                            \
-        __fadd2_rn(wprod(f2(magic_r<J>(wx[0], k4b), magic_r<J>(wy[0], k4b)), wr, wrm),      \
-                   wprod(f2(magic_r<J>(wx[1], k4b), magic_r<J>(wy[1], k4b)), wg, wgm)),     \
-        wprod(f2(magic_r<J>(wx[2], k4b), magic_r<J>(wy[2], k4b)), wb, wbm));                \
+        __fadd2_rn(wprod(f2(FP_MG(wx[0], J), FP_MG(wy[0], J)), wr, wrm),                    \
+                   wprod(f2(FP_MG(wx[1], J), FP_MG(wy[1], J)), wg, wgm)),                   \
+        wprod(f2(FP_MG(wx[2], J), FP_MG(wy[2], J)), wb, wbm));                              \
     /* g = 0.5 gray exactly; IIR y = fl(0.5 x + fl(0.5 y)) == FMA(0.5, y, g) */            \
     v[r][J] = FIRST ? __fadd2_rn(g, g) : __ffma2_rn(splat(0.5f), v[r][J], g);               \
   }
         FP_CELL(0) FP_CELL(1) FP_CELL(2) FP_CELL(3)
 #undef FP_CELL
+#undef FP_MG
       }
     };
     if (a.skip & 1) {

@@ -7,9 +7,11 @@ branch loop of the stencil role.
 import collections, re, subprocess, sys
 oh = sys.argv[1] if len(sys.argv) > 1 else "15"
 f32 = sys.argv[2] if len(sys.argv) > 2 else "0"
-obj = "paper_1509_04394_b200/_build/kernels_fc_pipe.cu.o"
+obj = ("paper_1509_04394_b200/_build/kernels_fc_pipe_cfg63.cu.o" if len(sys.argv) > 3
+       else "paper_1509_04394_b200/_build/kernels_fc_pipe.cu.o")
 sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
-name = f"_ZN6fcpipe12k_chain_pipeILi{oh}ELb{f32}EEEv14CUtensorMap_stNS_4ArgsE"
+ns = sys.argv[3] if len(sys.argv) > 3 else "6fcpipe"
+name = f"_ZN{ns}12k_chain_pipeILi{oh}ELb{f32}EEEv14CUtensorMap_stNS_4ArgsE"
 blk = sass.split("Function : " + name)[1].split("Function : ")[0]
 ins = []
 for line in blk.splitlines():
