@@ -345,9 +345,25 @@ def main():
             ts.append(time.perf_counter() - t0)
         dt = float(np.median(ts))
         ok = torch.equal(host_mask, mask.cpu())
+        # the host link on this box: plain pinned copies of the same bytes
+        # (H2D of the R, G, B planes, D2H of the mask), for context
+        def link(src, dst):
+            t0 = time.perf_counter()
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            return time.perf_counter() - t0
+        rgb_dev = torch.empty((F, 3, H, W), dtype=torch.uint8, device=dev)
+        rgb_host = torch.empty((F, 3, H, W), dtype=torch.uint8, pin_memory=True)
+        link(rgb_host, rgb_dev)
+        t_h2d = min(link(rgb_host, rgb_dev) for _ in range(3))
+        t_d2h = min(link(mask, host_mask) for _ in range(3))
+        del rgb_dev, rgb_host
         e2e = {"value": F / dt, "unit": "frames/s",
                "h2d_bytes_per_step": 3 * W * H * F, "d2h_bytes_per_step": W * H * F,
-               "ms_per_step": dt * 1e3, "matches_device_run": bool(ok)}
+               "ms_per_step": dt * 1e3, "matches_device_run": bool(ok),
+               "link_h2d_gbs": 3 * W * H * F / t_h2d / 1e9,
+               "link_d2h_gbs": W * H * F / t_d2h / 1e9,
+               "link_bound_fps": F / max(t_h2d, t_d2h)}
     elif world > 1 and args.e2e_steps > 0:
         # every rank: its shard's frames (warm-up frames included) from
         # pinned host memory, the sharded step, its mask back to the host;

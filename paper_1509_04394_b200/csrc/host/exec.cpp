@@ -195,6 +195,9 @@ Executor::Executor(const Pipeline& p, const FusionPlan& fp, int device,
 
 Executor::~Executor() {
   if (scratch_) cudaFree(scratch_);
+  if (stage_) cudaFree(stage_);
+  if (s_in_) cudaStreamDestroy(static_cast<cudaStream_t>(s_in_));
+  if (s_out_) cudaStreamDestroy(static_cast<cudaStream_t>(s_out_));
   if (own_stream_) cudaStreamDestroy(static_cast<cudaStream_t>(own_stream_));
 }
 
@@ -389,7 +392,7 @@ void Executor::run_host(const void* video, int in_type, void* out) {
       if (s.op == FC_BOX_MEAN && s.rt > 0) temporal_window = true;
   int chunk = opt_.host_chunk_frames;
   if (chunk <= 0)
-    chunk = int(std::max<long long>(1, (96LL << 20) / (long long)in_frame));
+    chunk = int(std::max<long long>(1, (48LL << 20) / (long long)in_frame));  // ~25 frames at 800x600
   if (temporal_window) chunk = F;  // cannot cut a temporal window
   chunk = std::min(chunk, F);
   const int n_chunks = (F + chunk - 1) / chunk;
@@ -399,16 +402,27 @@ void Executor::run_host(const void* video, int in_type, void* out) {
   std::size_t vbytes = align(std::size_t(chunk) * in_frame);
   std::size_t obytes = align(std::size_t(chunk) * out_frame);
   std::size_t sbytes = align(std::size_t(std::max(n_iir_, 1)) * hw * sizeof(float));
-  char* mem = nullptr;
-  cuda_check(cudaMalloc(&mem, 2 * (vbytes + obytes + sbytes)), "cudaMalloc(stream)");
+  if (2 * (vbytes + obytes + sbytes) > stage_bytes_) {
+    if (stage_) cuda_check(cudaFree(stage_), "cudaFree(stage)");
+    stage_ = nullptr;
+    stage_bytes_ = 0;
+    cuda_check(cudaMalloc(&stage_, 2 * (vbytes + obytes + sbytes)), "cudaMalloc(stream)");
+    stage_bytes_ = 2 * (vbytes + obytes + sbytes);
+  }
+  char* mem = static_cast<char*>(stage_);
   char* vb[2] = {mem, mem + vbytes};
   char* ob[2] = {mem + 2 * vbytes, mem + 2 * vbytes + obytes};
   float* sb[2] = {reinterpret_cast<float*>(mem + 2 * (vbytes + obytes)),
                   reinterpret_cast<float*>(mem + 2 * (vbytes + obytes) + sbytes)};
-  cudaStream_t s_in, s_out;
+  if (!s_in_) {
+    cudaStream_t a, b;
+    cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking), "stream");
+    s_in_ = a;
+    s_out_ = b;
+  }
+  cudaStream_t s_in = static_cast<cudaStream_t>(s_in_), s_out = static_cast<cudaStream_t>(s_out_);
   cudaStream_t s_comp = static_cast<cudaStream_t>(own_stream_);
-  cuda_check(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream");
-  cuda_check(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream");
   std::vector<cudaEvent_t> ev_in(n_chunks), ev_comp(n_chunks), ev_out(n_chunks);
   for (int k = 0; k < n_chunks; ++k) {
     cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
@@ -457,9 +471,6 @@ void Executor::run_host(const void* video, int in_type, void* out) {
     cudaEventDestroy(ev_comp[k]);
     cudaEventDestroy(ev_out[k]);
   }
-  cudaStreamDestroy(s_in);
-  cudaStreamDestroy(s_out);
-  cudaFree(mem);
   if (!err.empty()) throw Error(ErrorKind::Internal, err);
 }
 
@@ -532,10 +543,15 @@ void Executor::run_file(const std::string& in_path, const std::string& out_path)
                   reinterpret_cast<float*>(mem + 2 * (vbytes + obytes) + sbytes)};
   char* pi[2] = {pin, pin + vbytes};
   char* po[2] = {pin + 2 * vbytes, pin + 2 * vbytes + obytes};
-  cudaStream_t s_in, s_out;
+  if (!s_in_) {
+    cudaStream_t a, b;
+    cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking), "stream");
+    s_in_ = a;
+    s_out_ = b;
+  }
+  cudaStream_t s_in = static_cast<cudaStream_t>(s_in_), s_out = static_cast<cudaStream_t>(s_out_);
   cudaStream_t s_comp = static_cast<cudaStream_t>(own_stream_);
-  cuda_check(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream");
-  cuda_check(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream");
   std::vector<cudaEvent_t> ev_in(n_chunks), ev_comp(n_chunks), ev_out(n_chunks);
   for (int k = 0; k < n_chunks; ++k) {
     cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
@@ -594,9 +610,7 @@ void Executor::run_file(const std::string& in_path, const std::string& out_path)
     cudaEventDestroy(ev_comp[k]);
     cudaEventDestroy(ev_out[k]);
   }
-  cudaStreamDestroy(s_in);
-  cudaStreamDestroy(s_out);
-  cudaFreeHost(pin);
+  cudaFreeHost(pin);  // (the copy streams are the executor's, kept)
   cudaFree(mem);
   if (!err.empty()) throw Error(kind, err);
 }

@@ -84,6 +84,13 @@ class Executor {
   void* scratch_ = nullptr;
   std::size_t scratch_bytes_ = 0;
   void* own_stream_ = nullptr;
+  // host-pointer streaming (run_host): device staging and copy streams kept
+  // across calls (a per-call cudaMalloc / cudaFree of the staging buffers
+  // cost tens to hundreds of ms and made end-to-end times erratic)
+  void* stage_ = nullptr;
+  std::size_t stage_bytes_ = 0;
+  void* s_in_ = nullptr;
+  void* s_out_ = nullptr;
 };
 
 // fc_stage for one kernel descriptor, parameters converted as the
