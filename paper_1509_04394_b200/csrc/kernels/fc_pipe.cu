@@ -57,6 +57,8 @@
 #define FP_NI 5
 #define FP_KSLACK 2
 #define FP_NSF 3
+#define FP_SPECIALISE 0  // one code path: 978 k vs 950 k (per-CTA variants slow
+                         // the SMs around them -- instruction caches)
 #define FP_NAMESPACE fcpipe
 #define FP_ENTRY fc_chain_pipe
 #define FP_F345_ENTRY fc_f345_pipe
@@ -1197,6 +1199,17 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
                      "iir wait rgb %.2f slot %.2f\n",
                      names[k], cls[k][0], cls[k][1] / cls[k][0], cls[k][5],
                      cls[k][2] / cls[k][0], cls[k][3] / cls[k][0], cls[k][4] / cls[k][0]);
+    if (std::getenv("FUSEPLAN_PIPE_PROFILE")[0] == '2') {  // every CTA: start, span, waits
+      for (int b = 0; b < grid; ++b) {
+        const long long* r = &h[size_t(b) * 8];
+        std::fprintf(stderr, "  cta %4d win(%d,%d) class %lld start %+.2f us span %.1f us  "
+                     "stencil wait %.3f  iir rgb %.3f slot %.3f\n",
+                     b, b % cache.strips, (b / cache.strips) % cache.bands, r[7] & 3,
+                     double(r[0] - t0) / 1e3, double(r[1] - r[0]) / 1e3,
+                     double(r[2]) / double(r[5]), double(r[3]) / double(r[6]),
+                     double(r[4]) / double(r[6]));
+      }
+    }
   }
   if (a.dbg_px) {
     float h[64];

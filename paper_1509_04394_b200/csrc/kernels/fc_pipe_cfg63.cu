@@ -1,6 +1,7 @@
 // Tuning variant of the frame pipeline (FUSEPLAN_PIPE_CFG=63 selects it):
-// the previous layout -- two 2-column stencil warps per frame, 5 frames in
-// flight, 16 warps at 128 registers, 4 TMA slots -- kept for A/B runs.
+// the earlier 16-warp layout -- two 2-column stencil warps per frame, 5
+// frames in flight, 128 registers, 4 TMA slots, IIR code specialised per
+// window -- kept for A/B runs.
 #define FP_SPECIALISE 2
 #define FP_LC 2
 #define FP_NF 5
