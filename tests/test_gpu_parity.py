@@ -420,3 +420,27 @@ def test_pipe_every_window_height_exact(fp, cuda, oracle, monkeypatch, oh, part,
     out, _ = run(fp, pipe, v, {"force_partition": part},
                  variant="fast" if part == "1-5" else "auto", torch_dev=cuda)
     np.testing.assert_array_equal(out, want)
+
+
+@pytest.mark.parametrize("shape", [(128, 64, 1), (128, 64, 2), (256, 30, 3), (1024, 12, 7)])
+@pytest.mark.parametrize("segs", [0, 2, 5])
+def test_pipe_tiny_frame_counts_exact(fp, cuda, oracle, monkeypatch, shape, segs):
+    """1-7 frames (single-frame launches, more segments than frames asked
+    for, one-band videos): bit-exact, carried end state included."""
+    import torch
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    if segs:
+        monkeypatch.setenv("FUSEPLAN_PIPE_SEGS", str(segs))
+    W, H, F = shape
+    pipe = spec_chain(W, H, F + 3, th=40.0)
+    v = hash_video_u8(F + 3, 4, H, W, 500 + F)
+    want = oracle.orc_chain(pipe, v)
+    p = fp.Pipeline(json.dumps(pipe))
+    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": "1-5"}),
+                     variant="fast")
+    vt = torch.from_numpy(v).to(cuda)
+    st = torch.empty((1, H, W), device=cuda)
+    a = ex.run_range(vt[:F], state_out=st)
+    b = ex.run_range(vt[F:], state_in=st)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(torch.cat([a, b]).cpu().numpy().astype(np.float32), want)
