@@ -203,6 +203,13 @@ __device__ __forceinline__ void wait_phase(uint64_t* bar, unsigned phase) {
 
 __device__ __forceinline__ long long clk() { return clock64(); }
 
+__device__ __forceinline__ void st_pred_u32(void* p, uint32_t v, bool on) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.global.b32 [%0], %1;\n}\n" ::"l"(p),
+      "r"(v), "r"(unsigned(on))
+      : "memory");
+}
+
 // Byte offset of chunk k (columns 2k, 2k+1; 16 bytes) inside a pair-row:
 // even chunks at positions 0..31, odd chunks at 32 + ((k >> 1) + 4) % 32.
 // IIR lanes store chunks 2L and 2L+1 (each store: 32 consecutive positions);
@@ -671,10 +678,10 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
           if (okx) *reinterpret_cast<uint16_t*>(ox) = uint16_t(pack_neg2(dm[0].x, dm[1].x));
           if (oky) *reinterpret_cast<uint16_t*>(oy) = uint16_t(pack_neg2(dm[0].y, dm[1].y));
         } else {
-          if (okx)
-            *reinterpret_cast<uint32_t*>(ox) = pack_neg(dm[0].x, dm[1].x, dm[2].x, dm[3].x);
-          if (oky)
-            *reinterpret_cast<uint32_t*>(oy) = pack_neg(dm[0].y, dm[1].y, dm[2].y, dm[3].y);
+          // predicated stores (no branch: the next step's shuffles then need
+          // no reconvergence / divergence checks)
+          st_pred_u32(ox, pack_neg(dm[0].x, dm[1].x, dm[2].x, dm[3].x), okx);
+          st_pred_u32(oy, pack_neg(dm[0].y, dm[1].y, dm[2].y, dm[3].y), oky);
         }
         ox += W;  // running row pointers
         oy += W;
