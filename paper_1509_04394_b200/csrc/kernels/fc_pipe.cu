@@ -203,6 +203,14 @@ __device__ __forceinline__ void wait_phase(uint64_t* bar, unsigned phase) {
 
 __device__ __forceinline__ long long clk() { return clock64(); }
 
+__device__ __forceinline__ void sts_pred_u32(uint32_t* p, uint32_t v, bool on) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.shared.b32 [%0], %1;\n}\n" ::"r"(
+          smem_u32(p)),
+      "r"(v), "r"(unsigned(on))
+      : "memory");
+}
+
 __device__ __forceinline__ void st_pred_u32(void* p, uint32_t v, bool on) {
   asm volatile(
       "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.global.b32 [%0], %1;\n}\n" ::"l"(p),
@@ -699,10 +707,9 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
       const bool amb = outl && amin <= band;
       const unsigned ballot = __ballot_sync(0xffffffffu, amb);
       if (ballot) {
-        if (amb) {
-          const int i = nq + __popc(ballot & lt_mask);
-          if (i < QC) queue[i] = (unsigned(q0) << 16) | (lane << 8) | unsigned(nstep);
-        }
+        const int i = nq + __popc(ballot & lt_mask);
+        sts_pred_u32(queue + min(i, QC - 1),
+                     (unsigned(q0) << 16) | (lane << 8) | unsigned(nstep), amb && i < QC);
         nq += __popc(ballot);  // nq > QC: overflow, handled after the march
         amin = __int_as_float(0x7f800000);
       }
