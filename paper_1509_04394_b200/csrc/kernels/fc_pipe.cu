@@ -171,6 +171,14 @@ __device__ __forceinline__ uint64_t* bar_iir_empty(const Args& a, int i) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// one arrive per warp (lane 0) without a divergent branch
+__device__ __forceinline__ void mbar_arrive_lane0(uint64_t* bar, int lane) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.eq.u32 q, %1, 0;\n@q mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::
+          "r"(smem_u32(bar)),
+      "r"(unsigned(lane))
+      : "memory");
+}
 
 // Blocking wait: the suspend-time hint parks the warp in the barrier unit
 // instead of spinning through issue slots the working warps need.
@@ -401,7 +409,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
     else
       body(std::false_type{});
     __syncwarp();  // the warp's RGB reads are done (values in registers)
-    if (lane == 0) mbar_arrive(bar_rgb_empty(a, rslot));
+    mbar_arrive_lane0(bar_rgb_empty(a, rslot), lane);
     if (++rslot == NSF) {
       rslot = 0;
       rpar ^= 1u;
@@ -426,7 +434,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
       sts128(base + p * PROW + so1, v[r][2], v[r][3]);
     }
     __syncwarp();  // the warp's IIR stores precede the release arrive
-    if (lane == 0) mbar_arrive(bar_iir_full(a, islot));
+    mbar_arrive_lane0(bar_iir_full(a, islot), lane);
     if (++islot == K) {
       islot = 0;
       ipar ^= 1u;
@@ -486,7 +494,7 @@ __device__ __forceinline__ void plane_role(const Args& a, const Range& rg, int i
       v[r][3] = f2(qx.w, qy.w);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(bar_rgb_empty(a, rslot));
+    mbar_arrive_lane0(bar_rgb_empty(a, rslot), lane);
     if (++rslot == NSF) {
       rslot = 0;
       rpar ^= 1u;
@@ -501,7 +509,7 @@ __device__ __forceinline__ void plane_role(const Args& a, const Range& rg, int i
       sts128(base + p * PROW + so1, v[r][2], v[r][3]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(bar_iir_full(a, islot));
+    mbar_arrive_lane0(bar_iir_full(a, islot), lane);
     if (++islot == K) {
       islot = 0;
       ipar ^= 1u;
@@ -806,7 +814,7 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
     }
     }
     __syncwarp();  // the warp's slot reads (and rechecks) are done
-    if (lane == 0) mbar_arrive(bar_iir_empty(a, slot));
+    mbar_arrive_lane0(bar_iir_empty(a, slot), lane);
     slot += NF;
     if (slot >= K) {
       slot -= K;
