@@ -142,6 +142,30 @@ def cpu_reference_rate(W, H, sample_frames, seed=1234):
     return sample_frames / dt, cores, kind, f"{W}x{H}x{sample_frames} u8 hash video"
 
 
+def check_parity(pipe_spec, video, mask, warm, chunk=100):
+    """Every frame of the timed mask against the streaming C restatement of
+    run_sequential (oracle/fusechain_oracle.c, pinned to the reference build by
+    tests/test_oracle.py), chunked with the IIR state carried.  The checker
+    only: it never feeds the measured path."""
+    from oracle import oracle as O
+    if warm:  # a shard that does not start at frame 0 has no oracle state
+        return {"frames_checked": 0, "mismatches": None, "note": "shard starts mid-video"}
+    t0 = time.perf_counter()
+    F = int(mask.shape[0])
+    state, bad, bad_frames = None, 0, 0
+    for a in range(0, F, chunk):
+        b = min(F, a + chunk)
+        want, state = O.orc_chain(pipe_spec, video[a:b].cpu().numpy(), state_in=state,
+                                  return_state=True)
+        diff = mask[a:b].cpu().numpy().astype(np.float32) != want
+        bad += int(np.count_nonzero(diff))
+        bad_frames += int(np.count_nonzero(diff.reshape(b - a, -1).any(axis=1)))
+    return {"frames_checked": F, "mismatches": bad, "mismatching_frames": bad_frames,
+            "checker": "oracle/fusechain_oracle.c (streaming restatement of "
+                       "simulator.cpp:158-177, pinned to oracle/_ref)",
+            "seconds": round(time.perf_counter() - t0, 1)}
+
+
 def run_reference_arm(args, W, H, F, desc):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -182,6 +206,8 @@ def main():
     ap.add_argument("--variant", default="auto", choices=["auto", "exact", "fast"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the oracle check of the timed output")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak = F frames per GPU (N x F-frame video), "
                          "strong = the F-frame video split N ways")
@@ -402,6 +428,13 @@ def main():
                "note": "per rank: H2D of its shard (+ warm-up frames), sharded step, "
                        "D2H of its mask; max over ranks"}
 
+    # parity of the exact output the timed steps produced (rank 0's shard, which
+    # starts the recurrence at frame 0): every frame against the oracle, run in
+    # chunks with its IIR state carried -- a checker, outside the timed region
+    parity = None
+    if rank == 0 and not args.no_parity:
+        parity = check_parity(pipe_spec, video, mask, warm)
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -445,6 +478,7 @@ def main():
         "clocks": clocks.summary(),
         "kernels": desc_ex,
         "carry_fixups": events["fixups"],
+        "parity": parity,
     }
     print(json.dumps(line))
     if world > 1:
