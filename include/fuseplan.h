@@ -85,8 +85,11 @@ fp_status fp_simulate(const fp_pipeline* p, const fp_device* d,
                       const char* synth_json, const char* track_csv_path,
                       const char* format, int with_timestamp, char** out);
 
-/* ---- fuseplan.h:85-93: cost-model calibration is outside the B200 hot path
- * (SURVEY.md §2 row 14); these return FP_ERR_INPUT with a diagnostic. */
+/* ---- fuseplan.h:85-93 / calibrate.cpp:10-54: least-squares fit of the
+ * cost-model parameters from a measurements CSV (same columns, messages and
+ * JSON result as the reference; Householder QR with column pivoting in place
+ * of Eigen's ColPivHouseholderQR), and a device JSON re-rendered with fitted
+ * parameters. */
 fp_status fp_calibrate_csv(const char* measurements_csv, char** result_json);
 fp_status fp_device_render_with_cost(const fp_device* d,
                                      const char* params_json, char** out);
@@ -103,11 +106,13 @@ enum { FP_ELEM_U8 = 0, FP_ELEM_F32 = 1 };
 enum { FP_EXEC_HOST_PTRS = 0, FP_EXEC_DEVICE_PTRS = 1 };
 
 /* Builds an executor for `plan` over `p` on CUDA device `device`.
- * options_json (may be NULL): {"variant": "auto"|"exact"|"fast"|"fast_tile",
- *   "host_chunk_frames": N}.  "fast" = the certified strip kernel (fails with
- *   FP_ERR_INTERNAL when the chain is outside its coverage), "fast_tile" = the
- *   earlier tile-march kernel (kept for A/B measurement).  FP_ERR_INPUT if a stage has no device kernel,
- * FP_ERR_INTERNAL if no CUDA device is present. */
+ * options_json (may be NULL): {"variant": "auto"|"exact"|"fast",
+ *   "host_chunk_frames": N}.  "auto": the certified FP32 frame-pipeline
+ *   kernel (exact FP64 recheck inside its error band) where it applies, else
+ *   the FP64 kernels; "exact": FP64 kernels only; "fast": the frame pipeline
+ *   or FP_ERR_INTERNAL when the chain is outside its coverage.  The FUSEPLAN_*
+ *   diagnostic environment knobs are read once, here.  FP_ERR_INPUT if a
+ *   stage has no device kernel, FP_ERR_INTERNAL if no CUDA device is present. */
 fp_status fp_exec_create(const fp_pipeline* p, const fp_plan* plan, int device,
                          const char* options_json, fp_exec** out);
 void fp_exec_free(fp_exec* e);

@@ -104,6 +104,7 @@ def ref_lib():
         lib.ref_run_sequential_strips.argtypes = [c_s, c_p, c_i, c_p, c_i, c_p, c_i]
         lib.ref_run_tiled.argtypes = [c_s, c_s, c_s, c_p, c_i, c_p, c_p, c_p, c_i]
         lib.ref_synth_u8.argtypes = [c_s, c_p, c_p, c_i]
+        lib.ref_codegen_manifest.argtypes = [c_s, c_s, c_s, c_s, c_p, c_i, c_p, c_i]
         _ref = lib
     return _ref
 
@@ -137,6 +138,20 @@ def ref_plan_json(pipeline_json: str, device_json: str,
                            out, cap, err, 1024)
     _check(rc, err)
     return out.value.decode()
+
+
+def ref_codegen_manifest(pipeline_json: str, device_json: str,
+                         options: Optional[dict], name: str) -> dict:
+    """The reference codegen's manifest (codegen.cpp:425-465) as a dict."""
+    lib = ref_lib()
+    err = ctypes.create_string_buffer(1024)
+    cap = 1 << 20
+    out = ctypes.create_string_buffer(cap)
+    opts = json.dumps(options).encode() if options else b""
+    rc = lib.ref_codegen_manifest(pipeline_json.encode(), device_json.encode(), opts,
+                                  name.encode(), out, cap, err, 1024)
+    _check(rc, err)
+    return json.loads(out.value.decode())
 
 
 def _pipe_dims(pipeline_json: str):

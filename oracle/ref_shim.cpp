@@ -21,6 +21,7 @@
 
 #include "fuseplan/config.hpp"
 #include "fuseplan/planner.hpp"
+#include "fuseplan/codegen.hpp"
 #include "fuseplan/simulator.hpp"
 #include "fuseplan/tracking.hpp"
 #include "fuseplan/video.hpp"
@@ -69,6 +70,47 @@ VideoData make_video(const Pipeline& p, const void* video, int is_u8,
 
 }  // namespace
 
+// Plan options in the C ABI's JSON (the reference's parse_plan_options,
+// capi.cpp:88-110, restated: that function lives in capi.cpp, which is not
+// built here): halo_mode, transfer_variant, force_partition as the
+// reference's "1-2,3-5,6" string (or, for older fixtures, [[a, b], ...]),
+// tile {x, y, t}.
+static PlanOptions shim_options(const char* options_json) {
+  PlanOptions opts;
+  if (!options_json || !*options_json) return opts;
+  auto j = nlohmann::json::parse(options_json);
+  if (j.contains("halo_mode"))
+    opts.halo_mode = halo_mode_from_string(j["halo_mode"].get<std::string>());
+  if (j.contains("transfer_variant"))
+    opts.transfer_variant =
+        transfer_variant_from_string(j["transfer_variant"].get<std::string>());
+  if (j.contains("force_partition")) {
+    std::vector<std::pair<int, int>> iv;
+    const auto& fpj = j["force_partition"];
+    if (fpj.is_string()) {
+      std::string str = fpj.get<std::string>(), tok;
+      std::size_t pos = 0;
+      while (pos <= str.size()) {
+        std::size_t c = str.find(',', pos);
+        if (c == std::string::npos) c = str.size();
+        tok = str.substr(pos, c - pos);
+        std::size_t dash = tok.find('-');
+        int a = std::stoi(tok.substr(0, dash));
+        int b = dash == std::string::npos ? a : std::stoi(tok.substr(dash + 1));
+        iv.emplace_back(a, b);
+        pos = c + 1;
+      }
+    } else {
+      for (auto& e : fpj) iv.emplace_back(e[0].get<int>(), e[1].get<int>());
+    }
+    opts.forced_partition = iv;
+  }
+  if (j.contains("tile"))
+    opts.forced_tile = TileShape{j["tile"].value("x", 1), j["tile"].value("y", 1),
+                                 j["tile"].value("t", 1)};
+  return opts;
+}
+
 extern "C" {
 
 // Plan JSON through the reference planner.  Returns 0 / fp_status-like code.
@@ -78,25 +120,7 @@ int ref_plan_json(const char* pipeline_json, const char* device_json,
   try {
     Pipeline p = parse_pipeline(pipeline_json);
     Device d = parse_device(device_json);
-    PlanOptions opts;
-    if (options_json && *options_json) {
-      auto j = nlohmann::json::parse(options_json);
-      if (j.contains("halo_mode"))
-        opts.halo_mode = halo_mode_from_string(j["halo_mode"]);
-      if (j.contains("transfer_variant"))
-        opts.transfer_variant =
-            transfer_variant_from_string(j["transfer_variant"]);
-      if (j.contains("force_partition")) {
-        std::vector<std::pair<int, int>> iv;
-        for (auto& e : j["force_partition"])
-          iv.emplace_back(e[0].get<int>(), e[1].get<int>());
-        opts.forced_partition = iv;
-      }
-      if (j.contains("tile"))
-        opts.forced_tile = TileShape{j["tile"].value("x", 1),
-                                     j["tile"].value("y", 1),
-                                     j["tile"].value("t", 1)};
-    }
+    PlanOptions opts = shim_options(options_json);
     std::string s = render_plan(plan(p, d, opts));
     if (int(s.size()) + 1 > cap) return -int(s.size()) - 1;
     std::memcpy(out, s.c_str(), s.size() + 1);
@@ -190,6 +214,26 @@ int ref_run_sequential_strips(const char* pipeline_json, const void* video,
 
 // run_tiled for the plan the reference planner makes; traffic4 gets
 // {gmem_reads, gmem_writes, smem_reads, smem_writes}.
+// generate_plan_sources (codegen.cpp:425-465): the manifest JSON of the plan
+// the options select (the pseudo-CUDA files themselves are not returned).
+int ref_codegen_manifest(const char* pipeline_json, const char* device_json,
+                         const char* options_json, const char* name, char* out, int cap,
+                         char* err, int errcap) {
+  try {
+    Pipeline p = parse_pipeline(pipeline_json);
+    Device d = parse_device(device_json);
+    FusionPlan fp = plan(p, d, shim_options(options_json));
+    std::string s = generate_plan_sources(fp, p, d, name).manifest_json;
+    if (int(s.size()) + 1 > cap) return -int(s.size()) - 1;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+  } catch (const Error& e) {
+    return fail(e, err, errcap, kind_code(e));
+  } catch (const std::exception& e) {
+    return fail(e, err, errcap, 3);
+  }
+}
+
 int ref_run_tiled(const char* pipeline_json, const char* device_json,
                   const char* options_json, const void* video, int is_u8,
                   float* final_out, long long* traffic4, char* err,
@@ -197,20 +241,7 @@ int ref_run_tiled(const char* pipeline_json, const char* device_json,
   try {
     Pipeline p = parse_pipeline(pipeline_json);
     Device d = parse_device(device_json);
-    PlanOptions opts;
-    if (options_json && *options_json) {
-      auto j = nlohmann::json::parse(options_json);
-      if (j.contains("force_partition")) {
-        std::vector<std::pair<int, int>> iv;
-        for (auto& e : j["force_partition"])
-          iv.emplace_back(e[0].get<int>(), e[1].get<int>());
-        opts.forced_partition = iv;
-      }
-      if (j.contains("tile"))
-        opts.forced_tile = TileShape{j["tile"].value("x", 1),
-                                     j["tile"].value("y", 1),
-                                     j["tile"].value("t", 1)};
-    }
+    PlanOptions opts = shim_options(options_json);
     FusionPlan fp = plan(p, d, opts);
     VideoData v = make_video(p, video, is_u8);
     TiledResult r = run_tiled(fp, p, v);

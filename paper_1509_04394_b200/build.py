@@ -40,10 +40,8 @@ CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
 HOST_SRCS = ["host/model.cpp", "host/planner.cpp", "host/video.cpp",
              "host/exec.cpp", "host/capi.cpp",
              "host/calibrate.cpp"]
-CUDA_SRCS = ["kernels/fc_exact.cu", "kernels/fc_fast.cu", "kernels/fc_strip.cu", "kernels/fc_pipe.cu",
-             "kernels/fc_pipe_cfg63.cu",
-             "kernels/fc_f12.cu", "kernels/fc_track.cu",
-             "kernels/fc_dispatch.cu"]
+CUDA_SRCS = ["kernels/fc_exact.cu", "kernels/fc_pipe.cu", "kernels/fc_f12.cu",
+             "kernels/fc_track.cu", "kernels/fc_tiled.cu", "kernels/fc_dispatch.cu"]
 HEADERS = ["kernels/fc_pipe.cu", "host/fuseplan.hpp", "host/exec.hpp", "host/video.hpp",
            "kernels/fc_kernels.h", "kernels/fc_common.cuh"]
 

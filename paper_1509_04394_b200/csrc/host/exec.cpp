@@ -136,6 +136,7 @@ const char* LaunchGroup::kernel_name() const {
 Executor::Executor(const Pipeline& p, const FusionPlan& fp, int device,
                    const ExecOptions& opt)
     : device_(device), dims_(p.video), opt_(opt) {
+  fc_knobs_from_env(&knobs_);
   int n_dev = 0;
   cudaError_t e = cudaGetDeviceCount(&n_dev);
   require(e == cudaSuccess && n_dev > 0, ErrorKind::Internal,
@@ -238,11 +239,10 @@ void Executor::run_device(const void* video, int in_type, void* out, int n_frame
                           void* stream) {
   require(n_frames >= 0 && n_warm >= 0 && n_warm <= n_frames, ErrorKind::Input,
           "bad frame range");
-  require(n_warm == 0 || n_iir_ == 1, ErrorKind::Input,
-          "warm-up ranges need exactly one IIR stage in the chain");
   require(state_in == nullptr || n_iir_ >= 1, ErrorKind::Input,
           "state_in given but the chain has no IIR stage");
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  fc_set_knobs(&knobs_);
   cudaStream_t st = static_cast<cudaStream_t>(stream ? stream : own_stream_);
   const long long hw = (long long)dims_.width * dims_.height;
   const int C = dims_.channels;
@@ -252,6 +252,8 @@ void Executor::run_device(const void* video, int in_type, void* out, int n_frame
     n_frames -= n_warm;
     n_warm = 0;
   }
+  require(n_warm == 0 || n_iir_ == 1, ErrorKind::Input,
+          "warm-up ranges need exactly one IIR stage in the chain");
   if (n_frames == 0) return;
 
   // two f32 ping-pong planes of the largest frame count in flight

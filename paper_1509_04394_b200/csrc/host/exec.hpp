@@ -19,7 +19,7 @@
 
 namespace fuseplan {
 
-enum class Variant { Auto = 0, Exact = 1, Fast = 2, FastTile = 3 };
+enum class Variant { Auto = 0, Exact = 1, Fast = 2 };
 
 struct ExecOptions {
   Variant variant = Variant::Auto;
@@ -76,6 +76,7 @@ class Executor {
  private:
   void ensure_scratch(std::size_t bytes);
   int device_ = 0;
+  fc_knobs knobs_{};  // FUSEPLAN_* launcher knobs, read once at creation
   VideoDims dims_;
   ExecOptions opt_;
   std::vector<LaunchGroup> groups_;

@@ -118,6 +118,21 @@ struct CostParams {
   void validate() const;
 };
 
+// B200 extension of the device profile (not in the reference): the cost of a
+// plan group as THIS build's executor runs it.  The reference's Eq-2 model
+// (predict_cost) prices tiles, halos and SHMEM windows; the B200 executor
+// streams every group (frame pipeline / time scan / per-stage kernels), so a
+// group's time is the launches it takes plus pixels x the measured ns/pixel
+// of the kernel class that runs it (calibrated on a B200:
+// scripts/calibrate_streaming.py).  Classes: "chain" / "chain_exact" (the
+// whole SPEC chain, certified / FP64), "gray_iir", "gauss_grad_thr" /
+// "gauss_grad_thr_exact", and one per catalog op for unfused stages.
+struct StreamingCost {
+  double launch_ns = 0.0;
+  std::map<std::string, double> ns_per_px;
+  double rate(const std::string& cls) const;
+};
+
 struct Device {
   std::string name;
   std::int64_t smem_bytes = 0;
@@ -127,6 +142,7 @@ struct Device {
   int max_blocks_per_sm = 16;
   int max_warps_per_sm = 64;
   CostParams cost;
+  std::optional<StreamingCost> streaming;  // "streaming_cost" (B200 extension)
   void validate() const;
 };
 
@@ -272,7 +288,18 @@ struct PlanOptions {
   // hold the whole time extent in shared memory (planner.cpp select_group_tile
   // otherwise pins t = F, planner.cpp:73 of the reference).
   bool iir_streaming = false;
+  // B200 extension: which cost model prices the groups.  Auto = the
+  // device's "streaming_cost" when its profile has one (which also lifts the
+  // IIR t-pin, as iir_streaming does), else the reference's Eq-2 model;
+  // "reference" forces Eq 2 (plans byte-identical to the reference's).
+  enum class CostModel { Auto, Reference, Streaming } cost_model = CostModel::Auto;
 };
+
+bool uses_streaming_cost(const Device& dev, const PlanOptions& opt);
+// Executor kernel class of a contiguous group whose first kernel is `first_id`
+// (1 = reads the video), and its cost under the streaming model.
+std::string streaming_class_of(std::span<const KernelDesc> ks, int first_id,
+                               const VideoDims& video);
 
 struct LaunchConfig {
   int th_x = 1, th_y = 1, th_t = 1;
@@ -305,6 +332,7 @@ struct FusionPlan {
   std::vector<FusibleSegment> segments;
   std::vector<PlanGroup> groups;
   double total_cost = 0.0;
+  bool streaming_cost = false;  // B200 extension: groups priced by StreamingCost
   BufferReport buffers;
   std::vector<std::pair<int, int>> partition() const;
 };

@@ -221,7 +221,80 @@ CostBreakdown predict_cost(std::span<const KernelDesc> kernels,
   return c;
 }
 
+// ---------------------------------------------------------------- B200 streaming cost
+// (extension; see StreamingCost in fuseplan.hpp)
+
+bool uses_streaming_cost(const Device& dev, const PlanOptions& opt) {
+  using CM = PlanOptions::CostModel;
+  if (opt.cost_model == CM::Reference) return false;
+  if (opt.cost_model == CM::Streaming)
+    require(dev.streaming.has_value(), ErrorKind::Input,
+            "cost_model 'streaming' needs a device profile with streaming_cost");
+  return dev.streaming.has_value();
+}
+
 namespace {
+double kparam(const KernelDesc& k, const char* key, double dflt) {
+  auto it = k.params.find(key);
+  return it == k.params.end() ? dflt : it->second;
+}
+}  // namespace
+
+// The launch group the executor (exec.cpp) builds for this interval, and for
+// the fused classes whether the certified FP32 kernel applies (fc_common.cuh
+// fast_params / stencil_params: alpha 0.5, gaussian r = 2, a {0, 255} byte
+// mask, th > 0, width a multiple of 16).
+std::string streaming_class_of(std::span<const KernelDesc> ks, int first_id,
+                               const VideoDims& video) {
+  std::vector<std::string> ops;
+  for (const KernelDesc& k : ks) ops.push_back(k.stencil_op);
+  using V = std::vector<std::string>;
+  auto certified_tail = [&](const KernelDesc& g, const KernelDesc& t) {
+    return int(kparam(g, "radius", 2)) == 2 && kparam(t, "th", 128.0) > 0.0 &&
+           kparam(t, "white", 255.0) == 255.0 && kparam(t, "black", 0.0) == 0.0;
+  };
+  const bool reads_video = first_id == 1;
+  if (reads_video && video.channels == 4 &&
+      ops == V{"rgba2gray", "iir_temporal", "gaussian", "gradient", "threshold"}) {
+    const int r = int(kparam(ks[2], "radius", 2));
+    if (r >= 1 && r <= 3)
+      return float(kparam(ks[1], "alpha", 0.5)) == 0.5f && certified_tail(ks[2], ks[4]) &&
+                     video.width % 16 == 0
+                 ? "chain"
+                 : "chain_exact";
+  }
+  if (reads_video && ops == V{"rgba2gray", "iir_temporal"}) return "gray_iir";
+  if (ops == V{"gaussian", "gradient", "threshold"})
+    return certified_tail(ks[0], ks[2]) && video.width % 4 == 0 ? "gauss_grad_thr"
+                                                                 : "gauss_grad_thr_exact";
+  return "stages";
+}
+
+namespace {
+
+CostBreakdown streaming_cost(std::span<const KernelDesc> ks, int first_id, const Device& dev,
+                             const VideoDims& video) {
+  const StreamingCost& sc = *dev.streaming;
+  const double px = double(video.pixel_volume());
+  CostBreakdown c;
+  if (std::any_of(ks.begin(), ks.end(), [](const KernelDesc& k) {
+        return k.scope == KernelScope::GlobalAggregation;
+      })) {
+    c.launch = sc.launch_ns;  // the host-side tracking stage: one pass
+    return c;
+  }
+  const std::string cls = streaming_class_of(ks, first_id, video);
+  if (cls == "stages") {
+    for (const KernelDesc& k : ks) {
+      c.t_compute += px * sc.rate(k.stencil_op);
+      c.launch += sc.launch_ns;
+    }
+  } else {
+    c.t_compute = px * sc.rate(cls);
+    c.launch = sc.launch_ns;
+  }
+  return c;
+}
 
 bool any_recurrence(std::span<const KernelDesc> ks) {
   return std::any_of(ks.begin(), ks.end(), [](const KernelDesc& k) {
@@ -259,7 +332,8 @@ GroupTile size_group(std::span<const KernelDesc> ks, const Device& dev,
   lim.constrain_input_box = true;
   lim.max_x = std::max(video.width, video.height);
   lim.max_t = video.frames;
-  if (any_recurrence(ks) && !opt.iir_streaming) lim.min_t = video.frames;
+  if (any_recurrence(ks) && !opt.iir_streaming && !uses_streaming_cost(dev, opt))
+    lim.min_t = video.frames;
   try {
     TileSearchResult r = optimal_tile(g.halo, dev.smem_bytes / eb, lim, eb);
     g.tile = r.tile;
@@ -323,7 +397,8 @@ PlanGroup make_group(std::span<const KernelDesc> ks, int first, int last,
   g.tile = gt.tile;
   g.smem_bytes_used = gt.smem;
   g.du = data_utilization(g.tile, g.halo);
-  g.cost = predict_cost(ks, g.tile, g.halo, dev, video);
+  g.cost = uses_streaming_cost(dev, opt) ? streaming_cost(ks, first, dev, video)
+                                          : predict_cost(ks, g.tile, g.halo, dev, video);
   g.blocks = block_count(video, g.tile);
   std::tie(g.launch.th_x, g.launch.th_y) = fold_block(g.tile, dev);
   g.launch.th_t = 1;
@@ -371,7 +446,9 @@ std::vector<CandidateFusedKernel> enumerate_candidates(
       if (c.feasible) {
         c.tile.du = data_utilization(g.tile, g.halo);
         c.tile.objective_v = objective_v(g.tile, g.halo);
-        c.breakdown = predict_cost(ks, g.tile, g.halo, dev, video);
+        c.breakdown = uses_streaming_cost(dev, opt)
+                          ? streaming_cost(ks, c.first, dev, video)
+                          : predict_cost(ks, g.tile, g.halo, dev, video);
         c.cost = c.breakdown.total();
       } else {
         c.cost = kInf;
@@ -480,6 +557,7 @@ FusionPlan plan(const Pipeline& pipeline, const Device& dev,
   fp.transfer_variant = opt.transfer_variant;
   fp.video = pipeline.video;
   fp.device_name = dev.name;
+  fp.streaming_cost = uses_streaming_cost(dev, opt);
   fp.segments = fusible_segments(pipeline);
 
   const auto& forced = opt.forced_partition;
@@ -545,6 +623,7 @@ std::string render_plan(const FusionPlan& fp) {
   doc["halo_mode"] = to_string(fp.halo_mode);
   doc["transfer_variant"] = to_string(fp.transfer_variant);
   doc["device"] = fp.device_name;
+  if (fp.streaming_cost) doc["cost_model"] = "streaming (B200 executor, ns)";
   doc["video"] = {{"width", fp.video.width},
                   {"height", fp.video.height},
                   {"frames", fp.video.frames},
@@ -647,6 +726,13 @@ PlanOptions parse_plan_options(const char* text) {
     o.forced_tile = TileShape{t.value("x", 1), t.value("y", 1), t.value("t", 1)};
   }
   if (j.contains("iir_streaming")) o.iir_streaming = j["iir_streaming"].get<bool>();
+  if (j.contains("cost_model")) {
+    const std::string m = j["cost_model"].get<std::string>();
+    if (m == "auto") o.cost_model = PlanOptions::CostModel::Auto;
+    else if (m == "reference") o.cost_model = PlanOptions::CostModel::Reference;
+    else if (m == "streaming") o.cost_model = PlanOptions::CostModel::Streaming;
+    else throw Error(ErrorKind::Input, "unknown cost_model: " + m);
+  }
   return o;
 }
 

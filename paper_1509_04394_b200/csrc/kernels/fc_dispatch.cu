@@ -1,6 +1,9 @@
-// Variant dispatch for the streaming all-fused chain (F12345).
+// Variant dispatch for the streaming all-fused chain (F12345) and the F345
+// group, plus the launcher knobs (fc_knobs, read from the environment once
+// per executor).
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -14,22 +17,45 @@
 
 extern "C" int fc_chain_exact(FC_CHAIN_ARGS);  // fc_exact.cu: FP64 everywhere
 extern "C" int fc_chain_pipe(FC_CHAIN_ARGS);   // fc_pipe.cu: certified, headline
-extern "C" int fc_chain_pipe63(FC_CHAIN_ARGS); // fc_pipe_cfg63.cu: role-count variant
-extern "C" int fc_chain_strip(FC_CHAIN_ARGS);  // fc_strip.cu: certified, strip march
-extern "C" int fc_chain_tile(FC_CHAIN_ARGS);   // fc_fast.cu: certified, tile march
 extern "C" int fc_f345_pipe(const fc_stage* sg, const fc_stage* sthr, const float* in,
                             void* out, int out_type, fc_dims d, double in_max, void* stream);
-extern "C" int fc_f345_pipe63(const fc_stage* sg, const fc_stage* sthr, const float* in,
-                              void* out, int out_type, fc_dims d, double in_max, void* stream);
-extern "C" long long fc_strip_recheck_count(void);
 extern "C" long long fc_pipe_recheck_count(void);
-extern "C" long long fc_pipe63_recheck_count(void);
-extern "C" long long fc_tile_recheck_count(void);
 
-// variant: 0 auto (certified kernel when covered, else exact), 1 exact,
-//          2 fast (certified kernel or -1), 3 fast_tile (tile kernel or -1).
-// The certified kernel of 0 / 2 is the frame pipeline (fc_pipe.cu);
-// FUSEPLAN_FAST_KERNEL=strip selects the strip march (comparison runs).
+namespace {
+thread_local fc_knobs g_knobs = {};
+
+int env_int(const char* name) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : 0;
+}
+}  // namespace
+
+extern "C" void fc_knobs_from_env(fc_knobs* k) {
+  std::memset(k, 0, sizeof *k);
+  k->pipe_oh = env_int("FUSEPLAN_PIPE_OH");
+  k->pipe_segs = env_int("FUSEPLAN_PIPE_SEGS");
+  k->pipe_seg_warm = env_int("FUSEPLAN_PIPE_SEG_WARM");
+  k->pipe_skip = env_int("FUSEPLAN_PIPE_SKIP");
+  if (const char* e = std::getenv("FUSEPLAN_PIPE_BAND_SCALE")) k->band_scale = float(std::atof(e));
+  if (const char* e = std::getenv("FUSEPLAN_PIPE_PROFILE")) k->profile = e[0] == '2' ? 2 : 1;
+  k->debug = std::getenv("FUSEPLAN_DEBUG") != nullptr;
+  if (const char* e = std::getenv("FUSEPLAN_PIPE_DEBUG_PX"))
+    k->dbg_px_on = std::sscanf(e, "%d,%d,%d", &k->dbg_px[0], &k->dbg_px[1], &k->dbg_px[2]) == 3;
+  k->f12_stream = std::getenv("FUSEPLAN_F12_STREAM") != nullptr;
+  k->f12_legacy = std::getenv("FUSEPLAN_F12_LEGACY") != nullptr;
+}
+
+extern "C" void fc_set_knobs(const fc_knobs* k) {
+  if (k)
+    g_knobs = *k;
+  else
+    std::memset(&g_knobs, 0, sizeof g_knobs);
+}
+
+extern "C" const fc_knobs* fc_get_knobs(void) { return &g_knobs; }
+
+// variant: 0 auto (certified frame pipeline when covered, else exact),
+//          1 exact, 2 fast (certified frame pipeline or -1: fail loudly).
 extern "C" int fc_fused_chain(const fc_stage* sgray, const fc_stage* si,
                               const fc_stage* sg, const fc_stage* sgrad,
                               const fc_stage* sthr, const void* video,
@@ -37,41 +63,23 @@ extern "C" int fc_fused_chain(const fc_stage* sgray, const fc_stage* si,
                               fc_dims d, int n_warm, const float* state_in,
                               float* state_out, int variant, void* stream) {
   (void)sgrad;
-  if (variant == 3)
-    return fc_chain_tile(sgray, si, sg, sthr, video, in_type, gray_in, out,
-                         out_type, d, n_warm, state_in, state_out, stream);
   if (variant == 2 || variant == 0) {
-    const char* k = std::getenv("FUSEPLAN_FAST_KERNEL");
-    const bool strip = k && std::strcmp(k, "strip") == 0;
-    const char* cfg = std::getenv("FUSEPLAN_PIPE_CFG");
-    auto* pipe = (cfg && std::strcmp(cfg, "63") == 0) ? fc_chain_pipe63 : fc_chain_pipe;
-    int rc = strip ? fc_chain_strip(sgray, si, sg, sthr, video, in_type, gray_in, out,
-                                    out_type, d, n_warm, state_in, state_out, stream)
-                   : pipe(sgray, si, sg, sthr, video, in_type, gray_in, out, out_type, d,
-                          n_warm, state_in, state_out, stream);
-    if (rc != -1) return rc;  // -1: parameters not covered
-    if (variant == 2)  // frames lower than 6 rows: the certified tile march
-      return fc_chain_tile(sgray, si, sg, sthr, video, in_type, gray_in, out, out_type, d,
-                           n_warm, state_in, state_out, stream);
+    const int rc = fc_chain_pipe(sgray, si, sg, sthr, video, in_type, gray_in, out, out_type,
+                                 d, n_warm, state_in, state_out, stream);
+    if (rc != -1 || variant == 2) return rc;  // -1: parameters not covered
   }
   return fc_chain_exact(sgray, si, sg, sthr, video, in_type, gray_in, out,
                         out_type, d, n_warm, state_in, state_out, stream);
 }
 
-extern "C" long long fc_last_recheck_count(void) {
-  long long a = fc_strip_recheck_count(), b = fc_tile_recheck_count();
-  long long c = fc_pipe_recheck_count(), e = fc_pipe63_recheck_count();
-  return (a < 0 || b < 0 || c < 0 || e < 0) ? -1 : a + b + c + e;
-}
+extern "C" long long fc_last_recheck_count(void) { return fc_pipe_recheck_count(); }
 
 extern "C" int fc_fused_gauss_grad_thr_v(const fc_stage* sg, const fc_stage* sgrad,
                                          const fc_stage* sthr, const float* in, void* out,
                                          int out_type, fc_dims d, int variant, double in_max,
                                          void* stream) {
   if (variant != 1 && in_max > 0.0) {
-    const char* cfg = std::getenv("FUSEPLAN_PIPE_CFG");
-    auto* f345 = (cfg && std::strcmp(cfg, "63") == 0) ? fc_f345_pipe63 : fc_f345_pipe;
-    const int rc = f345(sg, sthr, in, out, out_type, d, in_max, stream);
+    const int rc = fc_f345_pipe(sg, sthr, in, out, out_type, d, in_max, stream);
     if (rc != -1) return rc;  // -1: parameters not covered -> exact
   }
   return fc_fused_gauss_grad_thr(sg, sgrad, sthr, in, out, out_type, d, stream);

@@ -12,6 +12,7 @@
 // holds that stage's value at the clamped position.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "fc_kernels.h"
@@ -70,6 +71,51 @@ __device__ __forceinline__ float sobel_op(S s) {
 }
 
 // ------------------------------------------------------------ unfused stages
+// The paper's sequential baseline: one launch per stage, every intermediate
+// plane in HBM.  Each kernel is a vectorised stream over its own bytes
+// (uint4 / float4 accesses, several frames or pixels per thread) so that the
+// fused-versus-sequential comparison is made against efficient unfused
+// kernels; frames are looped inside the grid (no gridDim.z limit).
+
+// fl(w * c) for a byte c held as the float c + 2^23 (one PRMT): the FMA
+// w * (c + 2^23) - w 2^23 rounds the exact product w c once (w 2^23 exact).
+template <int K>
+__device__ __forceinline__ float byte_magic(uint32_t w) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(0x4B000000u), "n"(0x7440 + K));
+  return __uint_as_float(r);
+}
+
+// simulator.cpp:51-56 on four pixels packed as bytes of r, g, b words
+__device__ __forceinline__ float4 gray4(const fc_stage& s, float wrm, float wgm, float wbm,
+                                        uint32_t r, uint32_t g, uint32_t b) {
+#define FC_G(K)                                                                   \
+  __fadd_rn(__fadd_rn(__fmaf_rn(s.wr, byte_magic<K>(r), wrm),                     \
+                      __fmaf_rn(s.wg, byte_magic<K>(g), wgm)),                    \
+            __fmaf_rn(s.wb, byte_magic<K>(b), wbm))
+  return make_float4(FC_G(0), FC_G(1), FC_G(2), FC_G(3));
+#undef FC_G
+}
+
+// u8 RGBA -> gray, 16 pixels per work item (hw % 16 == 0, 16-byte aligned)
+__global__ void k_rgba2gray_u8x16(const uint8_t* __restrict__ in, float* __restrict__ out,
+                                  fc_stage s, long long hw, long long n16) {
+  const float wrm = -s.wr * 8388608.0f, wgm = -s.wg * 8388608.0f, wbm = -s.wb * 8388608.0f;
+  const long long q = hw / 16;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n16;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long t = i / q, p = (i - t * q) * 16;
+    const uint8_t* f = in + t * 4 * hw + p;
+    const uint4 r = __ldcs(reinterpret_cast<const uint4*>(f));
+    const uint4 g = __ldcs(reinterpret_cast<const uint4*>(f + hw));
+    const uint4 b = __ldcs(reinterpret_cast<const uint4*>(f + 2 * hw));
+    float4* o = reinterpret_cast<float4*>(out + t * hw + p);
+    __stcs(o + 0, gray4(s, wrm, wgm, wbm, r.x, g.x, b.x));
+    __stcs(o + 1, gray4(s, wrm, wgm, wbm, r.y, g.y, b.y));
+    __stcs(o + 2, gray4(s, wrm, wgm, wbm, r.z, g.z, b.z));
+    __stcs(o + 3, gray4(s, wrm, wgm, wbm, r.w, g.w, b.w));
+  }
+}
 
 template <typename InT>
 __global__ void k_rgba2gray(const InT* __restrict__ in, float* __restrict__ out,
@@ -102,70 +148,188 @@ __global__ void k_iir(const float* __restrict__ in, float* __restrict__ out,
   if (state_out) state_out[p] = prev;
 }
 
-// 2-D stencils over a frame tile staged in shared memory.
-constexpr int TW = 32, TH = 8;
-
-template <int R>
-__global__ void k_gaussian(const float* __restrict__ in, float* __restrict__ out,
-                           fc_stage s, int W, int H) {
-  constexpr int SW = TW + 2 * R, SH = TH + 2 * R;
-  __shared__ double tile[SH][SW];
-  __shared__ double w[(2 * R + 1) * (2 * R + 1)];
-  const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
-  const float* f = in + (long long)blockIdx.z * W * H;
-  const int tid = threadIdx.y * TW + threadIdx.x;
-  for (int i = tid; i < (2 * R + 1) * (2 * R + 1); i += TW * TH) w[i] = s.g_w[i];
-  for (int i = tid; i < SW * SH; i += TW * TH) {
-    int sy = i / SW, sx = i - sy * SW;
-    int gx = clampi(x0 + sx - R, 0, W - 1), gy = clampi(y0 + sy - R, 0, H - 1);
-    tile[sy][sx] = double(f[(long long)gy * W + gx]);
+// Same scan on four pixels per thread (float4), eight frames of loads issued
+// ahead of the recurrence (hw % 4 == 0, 16-byte aligned planes).
+__global__ void k_iir_x4(const float* __restrict__ in, float* __restrict__ out, float alpha,
+                         float beta, long long hw, int n_frames, int n_warm,
+                         const float* __restrict__ state_in, float* __restrict__ state_out) {
+  const long long p = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4;
+  if (p >= hw) return;
+  const float4* src = reinterpret_cast<const float4*>(in + p);
+  float4* dst = reinterpret_cast<float4*>(out + p);
+  const long long step = hw / 4;
+  float4 y = state_in ? *reinterpret_cast<const float4*>(state_in + p)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool fresh = state_in == nullptr;
+  constexpr int U = 8;
+  int t = 0;
+  for (; t < n_frames; t += U) {
+    float4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (t + u < n_frames) x[u] = __ldcs(src + (long long)(t + u) * step);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (t + u >= n_frames) break;
+      if (fresh && t + u == 0) {
+        y = x[u];
+      } else {
+        y.x = iir_op(alpha, beta, x[u].x, y.x);
+        y.y = iir_op(alpha, beta, x[u].y, y.y);
+        y.z = iir_op(alpha, beta, x[u].z, y.z);
+        y.w = iir_op(alpha, beta, x[u].w, y.w);
+      }
+      if (t + u >= n_warm) __stcs(dst + (long long)(t + u - n_warm) * step, y);
+    }
   }
-  __syncthreads();
-  int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
-  if (x >= W || y >= H) return;
-  double acc = 0.0;
-#pragma unroll
-  for (int dy = 0; dy <= 2 * R; ++dy)
-#pragma unroll
-    for (int dx = 0; dx <= 2 * R; ++dx)
-      acc = __fma_rn(w[dy * (2 * R + 1) + dx],
-                     tile[threadIdx.y + dy][threadIdx.x + dx], acc);
-  out[(long long)blockIdx.z * W * H + (long long)y * W + x] = __double2float_rn(acc);
+  if (state_out) *reinterpret_cast<float4*>(state_out + p) = y;
 }
 
-__global__ void k_gradient(const float* __restrict__ in, float* __restrict__ out,
-                           int W, int H) {
-  __shared__ float tile[TH + 2][TW + 2];
-  const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
-  const float* f = in + (long long)blockIdx.z * W * H;
-  const int tid = threadIdx.y * TW + threadIdx.x;
-  for (int i = tid; i < (TW + 2) * (TH + 2); i += TW * TH) {
-    int sy = i / (TW + 2), sx = i - sy * (TW + 2);
-    int gx = clampi(x0 + sx - 1, 0, W - 1), gy = clampi(y0 + sy - 1, 0, H - 1);
-    tile[sy][sx] = f[(long long)gy * W + gx];
+// Gaussian weights widened to double once on the host (kernel parameter:
+// the DFMA reads them from the constant bank, no register or LDS cost).
+struct GaussW {
+  double w[(2 * FC_MAX_GAUSS_RADIUS + 1) * (2 * FC_MAX_GAUSS_RADIUS + 1)];
+};
+
+// Exact FP64 gaussian (simulator.cpp:63-74): every thread computes four
+// consecutive pixels of a row from a double tile (one float->double
+// conversion per staged element), accumulating each pixel's 25 products in
+// the reference's dy-outer / dx-inner order.  CTA tile 64 x 16, frames looped.
+constexpr int GX = 64, GY = 16;
+
+template <int R>
+__global__ void __launch_bounds__(256) k_gaussian_x4(const float* __restrict__ in,
+                                                     float* __restrict__ out, GaussW gw,
+                                                     int W, int H, int F) {
+  constexpr int K = 2 * R + 1, SW = GX + 2 * R, SH = GY + 2 * R;  // SW even: 16-B rows
+  __shared__ __align__(16) double tile[SH][SW];
+  const int x0 = blockIdx.x * GX, y0 = blockIdx.y * GY;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const long long hw = (long long)W * H;
+  for (int t = blockIdx.z; t < F; t += gridDim.z) {
+    const float* f = in + t * hw;
+    for (int i = threadIdx.x; i < SW * SH; i += 256) {
+      const int sy = i / SW, sx = i - sy * SW;
+      const int gx = clampi(x0 + sx - R, 0, W - 1), gy = clampi(y0 + sy - R, 0, H - 1);
+      tile[sy][sx] = double(__ldg(f + (long long)gy * W + gx));
+    }
+    __syncthreads();
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int dy = 0; dy < K; ++dy) {
+      double v[4 + 2 * R + 1];
+      const double* row = &tile[ty + dy][4 * tx];
+#pragma unroll
+      for (int j = 0; j < (4 + 2 * R + 1) / 2; ++j) {
+        const double2 q = *reinterpret_cast<const double2*>(row + 2 * j);
+        v[2 * j] = q.x;
+        v[2 * j + 1] = q.y;
+      }
+#pragma unroll
+      for (int dx = 0; dx < K; ++dx)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = __fma_rn(gw.w[dy * K + dx], v[j + dx], acc[j]);
+    }
+    const int x = x0 + 4 * tx, y = y0 + ty;
+    if (y < H) {
+      float* o = out + t * hw + (long long)y * W + x;
+      if (x + 3 < W && (W & 3) == 0) {
+        __stcs(reinterpret_cast<float4*>(o),
+               make_float4(__double2float_rn(acc[0]), __double2float_rn(acc[1]),
+                           __double2float_rn(acc[2]), __double2float_rn(acc[3])));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (x + j < W) o[j] = __double2float_rn(acc[j]);
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
-  if (x >= W || y >= H) return;
-  int cx = threadIdx.x + 1, cy = threadIdx.y + 1;
-  out[(long long)blockIdx.z * W * H + (long long)y * W + x] =
-      sobel_op([&](int dx, int dy) { return tile[cy + dy][cx + dx]; });
+}
+
+// Sobel magnitude (simulator.cpp:75-83), four consecutive pixels per thread,
+// CTA tile 64 x 16, frames looped.
+__global__ void __launch_bounds__(256) k_gradient_x4(const float* __restrict__ in,
+                                                     float* __restrict__ out, int W, int H,
+                                                     int F) {
+  constexpr int SW = GX + 8, SH = GY + 2;  // columns x0-4 .. x0+67 (aligned loads)
+  __shared__ __align__(16) float tile[SH][SW];
+  const int x0 = blockIdx.x * GX, y0 = blockIdx.y * GY;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const long long hw = (long long)W * H;
+  for (int t = blockIdx.z; t < F; t += gridDim.z) {
+    const float* f = in + t * hw;
+    for (int i = threadIdx.x; i < SW * SH; i += 256) {
+      const int sy = i / SW, sx = i - sy * SW;
+      const int gx = clampi(x0 + sx - 4, 0, W - 1), gy = clampi(y0 + sy - 1, 0, H - 1);
+      tile[sy][sx] = __ldg(f + (long long)gy * W + gx);
+    }
+    __syncthreads();
+    float v[3][12];  // rows y-1 .. y+1, columns x-4 .. x+7
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const float4 q = *reinterpret_cast<const float4*>(&tile[ty + r][4 * tx + 4 * j]);
+        v[r][4 * j] = q.x;
+        v[r][4 * j + 1] = q.y;
+        v[r][4 * j + 2] = q.z;
+        v[r][4 * j + 3] = q.w;
+      }
+    float m[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      m[j] = sobel_op([&](int dx, int dy) { return v[dy + 1][4 + j + dx]; });
+    const int x = x0 + 4 * tx, y = y0 + ty;
+    if (y < H) {
+      float* o = out + t * hw + (long long)y * W + x;
+      if (x + 3 < W && (W & 3) == 0) {
+        __stcs(reinterpret_cast<float4*>(o), make_float4(m[0], m[1], m[2], m[3]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (x + j < W) o[j] = m[j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ float point_op(const fc_stage& s, float v) {
+  if (s.op == FC_THRESHOLD) return v >= s.th ? s.white : s.black;  // simulator.cpp:84-89
+  if (s.op == FC_SCALE_OFFSET) return __fadd_rn(__fmul_rn(s.scale, v), s.offset);  // :91-95
+  return v;  // identity :90
 }
 
 template <typename OutT>
 __global__ void k_pointwise(const float* __restrict__ in, OutT* __restrict__ out,
                             fc_stage s, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = from_level<OutT>(point_op(s, in[i]));
+}
+
+// Four elements per thread (n % 4 == 0, 16-byte aligned).
+__global__ void k_pointwise_x4_u8(const float* __restrict__ in, uint8_t* __restrict__ out,
+                                  fc_stage s, long long n4) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
-    float v = in[i];
-    float r;
-    if (s.op == FC_THRESHOLD)
-      r = v >= s.th ? s.white : s.black;  // simulator.cpp:84-89
-    else if (s.op == FC_SCALE_OFFSET)
-      r = __fadd_rn(__fmul_rn(s.scale, v), s.offset);  // :91-95
-    else
-      r = v;  // identity :90
-    out[i] = from_level<OutT>(r);
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(in) + i);
+    const uint32_t r = uint32_t(from_level<uint8_t>(point_op(s, v.x))) |
+                       uint32_t(from_level<uint8_t>(point_op(s, v.y))) << 8 |
+                       uint32_t(from_level<uint8_t>(point_op(s, v.z))) << 16 |
+                       uint32_t(from_level<uint8_t>(point_op(s, v.w))) << 24;
+    reinterpret_cast<uint32_t*>(out)[i] = r;
+  }
+}
+
+__global__ void k_pointwise_x4_f32(const float* __restrict__ in, float* __restrict__ out,
+                                   fc_stage s, long long n4) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(in) + i);
+    __stcs(reinterpret_cast<float4*>(out) + i,
+           make_float4(point_op(s, v.x), point_op(s, v.y), point_op(s, v.z), point_op(s, v.w)));
   }
 }
 
@@ -231,103 +395,153 @@ __global__ void k_gray_iir(const InT* __restrict__ video, float* __restrict__ ou
 // carry the edge value the gradient must see), then Sobel + threshold.
 constexpr int FW = 32, FH = 16, FT = 256;
 
+// The staged double plane of the fused exact kernels: rows of DP doubles
+// (even, so every row is 16-byte aligned), ring column c of the gaussian at
+// staged column c + R (staged column 0 = video column x0 - 1 - R).
+template <int R>
+struct RingGeom {
+  static constexpr int K = 2 * R + 1;
+  static constexpr int GW = FW + 2, GH = FH + 2;       // ring: the tile + 1
+  static constexpr int RG = (GW + 3) / 4;              // 4-wide ring groups per row
+  static constexpr int DW = 4 * RG + 2 * R;            // staged columns read
+  static constexpr int DP = DW + (DW & 1);             // row pitch (even)
+  static constexpr int DH = GH + 2 * R;
+};
+
+// Exact FP64 gaussian of the ring (simulator.cpp:63-74, dy-outer / dx-inner
+// accumulation): a thread computes four neighbouring ring cells from one
+// pass over 4 + 2R staged doubles per row (LDS.128 pairs); cells whose
+// centre is clamped to the video (border tiles) take the per-cell form.
+template <int R>
+__device__ __forceinline__ void ring_gaussian(const double* __restrict__ d, float* __restrict__ g,
+                                              const GaussW& gw, int x0, int y0, int W, int H) {
+  using G = RingGeom<R>;
+  constexpr int K = G::K;
+  for (int item = threadIdx.x; item < G::RG * G::GH; item += FT) {
+    const int ry = item / G::RG, rc = 4 * (item - ry * G::RG);
+    const int cy = clampi(y0 + ry - 1, 0, H - 1) - (y0 - 1 - R);  // staged row of the centre
+    bool plain = true;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int xv = x0 - 1 + rc + j;
+      plain = plain && (rc + j >= G::GW || (xv >= 0 && xv <= W - 1));
+    }
+    if (plain) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int dy = 0; dy < K; ++dy) {
+        const double* row = d + (cy - R + dy) * G::DP + rc;
+        double v[4 + 2 * R + 1];
+#pragma unroll
+        for (int q = 0; q < (4 + 2 * R + 1) / 2; ++q) {
+          const double2 t = *reinterpret_cast<const double2*>(row + 2 * q);
+          v[2 * q] = t.x;
+          v[2 * q + 1] = t.y;
+        }
+#pragma unroll
+        for (int dx = 0; dx < K; ++dx)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[j] = __fma_rn(gw.w[dy * K + dx], v[j + dx], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (rc + j < G::GW) g[ry * G::GW + rc + j] = __double2float_rn(acc[j]);
+    } else {
+      for (int j = 0; j < 4 && rc + j < G::GW; ++j) {
+        const int cx = clampi(x0 - 1 + rc + j, 0, W - 1) - (x0 - 1 - R);
+        double acc = 0.0;
+        for (int dy = 0; dy < K; ++dy)
+          for (int dx = 0; dx < K; ++dx)
+            acc = __fma_rn(gw.w[dy * K + dx], d[(cy - R + dy) * G::DP + cx - R + dx], acc);
+        g[ry * G::GW + rc + j] = __double2float_rn(acc);
+      }
+    }
+  }
+}
+
+template <int R, typename OutT>
+__device__ __forceinline__ void ring_sobel_threshold(const float* __restrict__ g,
+                                                     OutT* __restrict__ o, float th, float white,
+                                                     float black, int x0, int y0, int W, int H) {
+  using G = RingGeom<R>;
+  for (int i = threadIdx.x; i < FW * FH; i += FT) {
+    const int ty = i / FW, tx = i - ty * FW;
+    const int x = x0 + tx, y = y0 + ty;
+    if (x >= W || y >= H) continue;
+    const float m =
+        sobel_op([&](int dx, int dy) { return g[(ty + 1 + dy) * G::GW + tx + 1 + dx]; });
+    o[(long long)y * W + x] = from_level<OutT>(m >= th ? white : black);
+  }
+}
+
 template <int R, typename OutT>
 __global__ void __launch_bounds__(FT) k_gauss_grad_thr(
-    const float* __restrict__ in, OutT* __restrict__ out, fc_stage sg,
+    const float* __restrict__ in, OutT* __restrict__ out, GaussW gw,
     float th, float white, float black, int W, int H) {
-  constexpr int K = 2 * R + 1;
-  constexpr int DW = FW + 2 * (R + 1), DH = FH + 2 * (R + 1);
-  constexpr int GW = FW + 2, GH = FH + 2;
-  __shared__ double d[DH][DW];
-  __shared__ float g[GH][GW];
-  __shared__ double w[K * K];
+  using G = RingGeom<R>;
+  __shared__ __align__(16) double d[G::DH * G::DP];
+  __shared__ float g[G::GH * G::GW];
   const int x0 = blockIdx.x * FW, y0 = blockIdx.y * FH;
   const long long hw = (long long)W * H;
   const float* f = in + blockIdx.z * hw;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < K * K; i += FT) w[i] = sg.g_w[i];
-  for (int i = tid; i < DW * DH; i += FT) {
-    int sy = i / DW, sx = i - sy * DW;
-    int gx = clampi(x0 + sx - (R + 1), 0, W - 1);
-    int gy = clampi(y0 + sy - (R + 1), 0, H - 1);
-    d[sy][sx] = double(f[(long long)gy * W + gx]);
+  for (int i = threadIdx.x; i < G::DP * G::DH; i += FT) {
+    const int sy = i / G::DP, sx = i - sy * G::DP;
+    const int gx = clampi(x0 - 1 - R + sx, 0, W - 1);
+    const int gy = clampi(y0 - 1 - R + sy, 0, H - 1);
+    d[i] = double(__ldg(f + (long long)gy * W + gx));
   }
   __syncthreads();
-  for (int i = tid; i < GW * GH; i += FT) {
-    int sy = i / GW, sx = i - sy * GW;
-    // centre of this ring cell, clamped to the video; its window stays
-    // inside the staged box because clamping moves toward the tile
-    int cx = clampi(x0 + sx - 1, 0, W - 1) - (x0 - (R + 1));
-    int cy = clampi(y0 + sy - 1, 0, H - 1) - (y0 - (R + 1));
-    double acc = 0.0;
-#pragma unroll
-    for (int dy = 0; dy < K; ++dy)
-#pragma unroll
-      for (int dx = 0; dx < K; ++dx)
-        acc = __fma_rn(w[dy * K + dx], d[cy - R + dy][cx - R + dx], acc);
-    g[sy][sx] = __double2float_rn(acc);
-  }
+  ring_gaussian<R>(d, g, gw, x0, y0, W, H);
   __syncthreads();
-  for (int i = tid; i < FW * FH; i += FT) {
-    int ty = i / FW, tx = i - ty * FW;
-    int x = x0 + tx, y = y0 + ty;
-    if (x >= W || y >= H) continue;
-    float m = sobel_op([&](int dx, int dy) { return g[ty + 1 + dy][tx + 1 + dx]; });
-    out[blockIdx.z * hw + (long long)y * W + x] =
-        from_level<OutT>(m >= th ? white : black);
-  }
+  ring_sobel_threshold<R>(g, out + blockIdx.z * hw, th, white, black, x0, y0, W, H);
 }
 
 // ------------------------------------------------------------ F12345 exact
 // Streaming all-fused chain: one CTA per spatial tile marches over t, the IIR
-// state of its haloed tile (R+1 ring) lives in registers, the frame's
-// inputs for t+1 are loaded while t is computed.  Reference-exact everywhere
-// (FP64 gaussian); the fast certified kernel is in fc_fast.cu.
+// state of its staged cells lives in registers, the frame's inputs for t+1
+// are loaded while t is computed.  Reference-exact everywhere (FP64
+// gaussian); the certified kernel is fc_pipe.cu's frame pipeline.
 template <int R>
 struct ChainGeom {
-  static constexpr int DW = FW + 2 * (R + 1), DH = FH + 2 * (R + 1);
-  static constexpr int NS = (DW * DH + FT - 1) / FT;  // IIR slots per thread
+  static constexpr int NS = (RingGeom<R>::DP * RingGeom<R>::DH + FT - 1) / FT;  // cells / thread
 };
 
 template <int R, typename InT, typename OutT, bool GRAY_IN>
 __global__ void __launch_bounds__(FT) k_chain_exact(
     const InT* __restrict__ video, OutT* __restrict__ out, fc_stage sgray,
-    float alpha, float beta, fc_stage sg, float th, float white, float black,
+    float alpha, float beta, GaussW gw, float th, float white, float black,
     int W, int H, int n_frames, int n_warm, const float* __restrict__ state_in,
     float* __restrict__ state_out) {
-  using G = ChainGeom<R>;
-  constexpr int K = 2 * R + 1, DW = G::DW, DH = G::DH, NS = G::NS;
-  constexpr int GW = FW + 2, GH = FH + 2;
+  using G = RingGeom<R>;
+  constexpr int NS = ChainGeom<R>::NS, NCELL = G::DP * G::DH;
   constexpr int C = GRAY_IN ? 1 : 4;
-  __shared__ double d[DH][DW];
-  __shared__ float g[GH][GW];
-  __shared__ double w[K * K];
+  __shared__ __align__(16) double d[NCELL];
+  __shared__ float g[G::GH * G::GW];
   const int x0 = blockIdx.x * FW, y0 = blockIdx.y * FH;
   const long long hw = (long long)W * H;
   const int tid = threadIdx.x;
-  for (int i = tid; i < K * K; i += FT) w[i] = sg.g_w[i];
 
   // loop-invariant clamped source offsets of the owned IIR cells
   int src[NS];
   float st[NS];
-  bool fresh = state_in == nullptr;
+  const bool fresh = state_in == nullptr;
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
-    int i = tid + k * FT;
-    int sy = i / DW, sx = i - sy * DW;
-    int gx = clampi(x0 + sx - (R + 1), 0, W - 1);
-    int gy = clampi(y0 + sy - (R + 1), 0, H - 1);
+    const int i = tid + k * FT;
+    const int sy = i / G::DP, sx = i - sy * G::DP;
+    const int gx = clampi(x0 - 1 - R + sx, 0, W - 1);
+    const int gy = clampi(y0 - 1 - R + sy, 0, H - 1);
     src[k] = gy * W + gx;
-    st[k] = (i < DW * DH && state_in) ? state_in[src[k]] : 0.0f;
+    st[k] = (i < NCELL && state_in) ? state_in[src[k]] : 0.0f;
   }
   float cur[NS][3], nxt[NS][3];
   auto load = [&](int t, float (&v)[NS][3]) {
     const InT* f = video + (long long)t * C * hw;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      if (tid + k * FT < DW * DH) {
+      if (tid + k * FT < NCELL) {
 #pragma unroll
-        for (int c = 0; c < (GRAY_IN ? 1 : 3); ++c) v[k][c] = to_f(f[c * hw + src[k]]);
+        for (int c = 0; c < (GRAY_IN ? 1 : 3); ++c) v[k][c] = to_f(__ldg(f + c * hw + src[k]));
       }
     }
   };
@@ -335,42 +549,20 @@ __global__ void __launch_bounds__(FT) k_chain_exact(
   for (int t = 0; t < n_frames; ++t) {
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      int i = tid + k * FT;
-      if (i < DW * DH) {
-        float x = GRAY_IN ? cur[k][0] : gray_op(sgray, cur[k][0], cur[k][1], cur[k][2]);
+      const int i = tid + k * FT;
+      if (i < NCELL) {
+        const float x = GRAY_IN ? cur[k][0] : gray_op(sgray, cur[k][0], cur[k][1], cur[k][2]);
         st[k] = (fresh && t == 0) ? x : iir_op(alpha, beta, x, st[k]);
-        int sy = i / DW, sx = i - sy * DW;
-        d[sy][sx] = double(st[k]);
+        d[i] = double(st[k]);
       }
     }
     if (t + 1 < n_frames) load(t + 1, nxt);
     __syncthreads();
-    if (t >= n_warm) {
-      for (int i = tid; i < GW * GH; i += FT) {
-        int sy = i / GW, sx = i - sy * GW;
-        int cx = clampi(x0 + sx - 1, 0, W - 1) - (x0 - (R + 1));
-        int cy = clampi(y0 + sy - 1, 0, H - 1) - (y0 - (R + 1));
-        double acc = 0.0;
-#pragma unroll
-        for (int dy = 0; dy < K; ++dy)
-#pragma unroll
-          for (int dx = 0; dx < K; ++dx)
-            acc = __fma_rn(w[dy * K + dx], d[cy - R + dy][cx - R + dx], acc);
-        g[sy][sx] = __double2float_rn(acc);
-      }
-    }
+    if (t >= n_warm) ring_gaussian<R>(d, g, gw, x0, y0, W, H);
     __syncthreads();
-    if (t >= n_warm) {
-      OutT* o = out + (long long)(t - n_warm) * hw;
-      for (int i = tid; i < FW * FH; i += FT) {
-        int ty = i / FW, tx = i - ty * FW;
-        int x = x0 + tx, y = y0 + ty;
-        if (x >= W || y >= H) continue;
-        float m =
-            sobel_op([&](int dx, int dy) { return g[ty + 1 + dy][tx + 1 + dx]; });
-        o[(long long)y * W + x] = from_level<OutT>(m >= th ? white : black);
-      }
-    }
+    if (t >= n_warm)
+      ring_sobel_threshold<R>(g, out + (long long)(t - n_warm) * hw, th, white, black, x0, y0,
+                              W, H);
 #pragma unroll
     for (int k = 0; k < NS; ++k)
 #pragma unroll
@@ -380,11 +572,11 @@ __global__ void __launch_bounds__(FT) k_chain_exact(
     // write back the state of the cells that are the tile's own pixels
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      int i = tid + k * FT;
-      int sy = i / DW, sx = i - sy * DW;
-      int x = x0 + sx - (R + 1), y = y0 + sy - (R + 1);
-      if (i < DW * DH && sx >= R + 1 && sx < R + 1 + FW && sy >= R + 1 &&
-          sy < R + 1 + FH && x < W && y < H)
+      const int i = tid + k * FT;
+      const int sy = i / G::DP, sx = i - sy * G::DP;
+      const int x = x0 - 1 - R + sx, y = y0 - 1 - R + sy;
+      if (i < NCELL && sx >= R + 1 && sx < R + 1 + FW && sy >= R + 1 && sy < R + 1 + FH &&
+          x < W && y < H)
         state_out[(long long)y * W + x] = st[k];
     }
   }
@@ -449,11 +641,21 @@ int fc_stage_spatial(const fc_stage* s, const void* in, int in_type, void* out,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   long long hw = (long long)d.width * d.height, n = hw * d.frames;
   if (n == 0) return 0;
-  dim3 tiles((d.width + TW - 1) / TW, (d.height + TH - 1) / TH, d.frames);
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  // 2-D stencil grid: 64 x 16 tiles, frames looped inside (z <= 65535)
+  const int gx = (d.width + GX - 1) / GX, gy = (d.height + GY - 1) / GY;
+  const long long per_frame = (long long)gx * gy;
+  const int gz = int(std::max(1LL, std::min<long long>(
+                     d.frames, std::min<long long>(65535, (148LL * 16 + per_frame - 1) /
+                                                               per_frame))));
+  const dim3 tiles(gx, gy, gz);
   switch (s->op) {
     case FC_RGBA2GRAY:
       if (out_type != FC_F32) return -1;
-      if (in_type == FC_U8)
+      if (in_type == FC_U8 && hw % 16 == 0 && aligned(in) && aligned(out))
+        k_rgba2gray_u8x16<<<grid_for(n / 16, 256), 256, 0, st>>>(
+            static_cast<const uint8_t*>(in), static_cast<float*>(out), *s, hw, n / 16);
+      else if (in_type == FC_U8)
         k_rgba2gray<uint8_t><<<grid_for(n, 256), 256, 0, st>>>(
             static_cast<const uint8_t*>(in), static_cast<float*>(out), *s, hw, n);
       else
@@ -464,22 +666,24 @@ int fc_stage_spatial(const fc_stage* s, const void* in, int in_type, void* out,
       if (in_type != FC_F32 || out_type != FC_F32) return -1;
       auto f = static_cast<const float*>(in);
       auto o = static_cast<float*>(out);
-      dim3 b(TW, TH);
+      GaussW w;
+      const int K = 2 * s->g_radius + 1;
+      for (int i = 0; i < K * K; ++i) w.w[i] = double(s->g_w[i]);
       switch (s->g_radius) {
-        case 0: k_gaussian<0><<<tiles, b, 0, st>>>(f, o, *s, d.width, d.height); break;
-        case 1: k_gaussian<1><<<tiles, b, 0, st>>>(f, o, *s, d.width, d.height); break;
-        case 2: k_gaussian<2><<<tiles, b, 0, st>>>(f, o, *s, d.width, d.height); break;
-        case 3: k_gaussian<3><<<tiles, b, 0, st>>>(f, o, *s, d.width, d.height); break;
-        case 4: k_gaussian<4><<<tiles, b, 0, st>>>(f, o, *s, d.width, d.height); break;
+        case 0: k_gaussian_x4<0><<<tiles, 256, 0, st>>>(f, o, w, d.width, d.height, d.frames); break;
+        case 1: k_gaussian_x4<1><<<tiles, 256, 0, st>>>(f, o, w, d.width, d.height, d.frames); break;
+        case 2: k_gaussian_x4<2><<<tiles, 256, 0, st>>>(f, o, w, d.width, d.height, d.frames); break;
+        case 3: k_gaussian_x4<3><<<tiles, 256, 0, st>>>(f, o, w, d.width, d.height, d.frames); break;
+        case 4: k_gaussian_x4<4><<<tiles, 256, 0, st>>>(f, o, w, d.width, d.height, d.frames); break;
         default: return -1;
       }
       return status();
     }
     case FC_GRADIENT:
       if (in_type != FC_F32 || out_type != FC_F32) return -1;
-      k_gradient<<<tiles, dim3(TW, TH), 0, st>>>(static_cast<const float*>(in),
-                                                 static_cast<float*>(out),
-                                                 d.width, d.height);
+      k_gradient_x4<<<tiles, 256, 0, st>>>(static_cast<const float*>(in),
+                                           static_cast<float*>(out), d.width, d.height,
+                                           d.frames);
       return status();
     case FC_THRESHOLD:
     case FC_IDENTITY:
@@ -490,12 +694,20 @@ int fc_stage_spatial(const fc_stage* s, const void* in, int in_type, void* out,
         return status();
       }
       if (in_type != FC_F32) return -1;
-      if (out_type == FC_U8)
+      if (n % 4 == 0 && aligned(in) && aligned(out)) {
+        if (out_type == FC_U8)
+          k_pointwise_x4_u8<<<grid_for(n / 4, 256), 256, 0, st>>>(
+              static_cast<const float*>(in), static_cast<uint8_t*>(out), *s, n / 4);
+        else
+          k_pointwise_x4_f32<<<grid_for(n / 4, 256), 256, 0, st>>>(
+              static_cast<const float*>(in), static_cast<float*>(out), *s, n / 4);
+      } else if (out_type == FC_U8) {
         k_pointwise<uint8_t><<<grid_for(n, 256), 256, 0, st>>>(
             static_cast<const float*>(in), static_cast<uint8_t*>(out), *s, n);
-      else
+      } else {
         k_pointwise<float><<<grid_for(n, 256), 256, 0, st>>>(
             static_cast<const float*>(in), static_cast<float*>(out), *s, n);
+      }
       return status();
     case FC_BOX_MEAN:
       if (in_type != FC_F32 || out_type != FC_F32) return -1;
@@ -514,8 +726,16 @@ int fc_stage_iir(const fc_stage* s, const float* in, float* out, fc_dims d,
   long long hw = (long long)d.width * d.height;
   if (hw == 0 || d.frames == 0) return 0;
   float beta = 1.0f - s->alpha;  // host float arithmetic == reference's
-  k_iir<<<int((hw + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
-      in, out, s->alpha, beta, hw, d.frames, n_warm, state_in, state_out);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (hw % 4 == 0 && aligned(in) && aligned(out) && aligned(state_in) && aligned(state_out)) {
+    const long long th = hw / 4;
+    k_iir_x4<<<int((th + 127) / 128), 128, 0, st>>>(in, out, s->alpha, beta, hw, d.frames,
+                                                     n_warm, state_in, state_out);
+  } else {
+    k_iir<<<int((hw + 127) / 128), 128, 0, st>>>(in, out, s->alpha, beta, hw, d.frames,
+                                                 n_warm, state_in, state_out);
+  }
   return status();
 }
 
@@ -551,9 +771,19 @@ int fc_fused_gauss_grad_thr(const fc_stage* sg, const fc_stage* /*sgrad*/,
                             int out_type, fc_dims d, void* stream) {
   if ((long long)d.width * d.height * d.frames == 0) return 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  dim3 grid((d.width + FW - 1) / FW, (d.height + FH - 1) / FH, d.frames);
+  const long long hw = (long long)d.width * d.height;
+  const size_t osz = out_type == FC_U8 ? 1 : 4;
+  GaussW gw;
+  for (int i = 0; i < (2 * sg->g_radius + 1) * (2 * sg->g_radius + 1); ++i)
+    gw.w[i] = double(sg->g_w[i]);
+  // one CTA per (tile, frame): at most 65535 frames per launch (grid z)
+  for (int f0 = 0; f0 < d.frames; f0 += 65535) {
+  const int nf = std::min(65535, d.frames - f0);
+  dim3 grid((d.width + FW - 1) / FW, (d.height + FH - 1) / FH, nf);
+  const float* fin = in + f0 * hw;
+  void* fout = static_cast<char*>(out) + size_t(f0) * hw * osz;
 #define FC_GGT(R, T)                                                              \
-  k_gauss_grad_thr<R, T><<<grid, FT, 0, st>>>(in, static_cast<T*>(out), *sg,     \
+  k_gauss_grad_thr<R, T><<<grid, FT, 0, st>>>(fin, static_cast<T*>(fout), gw,    \
                                               sthr->th, sthr->white, sthr->black, \
                                               d.width, d.height)
 #define FC_GGT_R(T)            \
@@ -572,11 +802,13 @@ int fc_fused_gauss_grad_thr(const fc_stage* sg, const fc_stage* /*sgrad*/,
   }
 #undef FC_GGT_R
 #undef FC_GGT
-  return status();
+  if (const int rc = status()) return rc;
+  }
+  return 0;
 }
 
-// Exact streaming chain; the certified fast variant lives in fc_fast.cu and
-// is dispatched from there (fc_fused_chain).
+// Exact streaming chain; the certified frame pipeline (fc_pipe.cu) is
+// dispatched ahead of it by fc_fused_chain (fc_dispatch.cu).
 int fc_chain_exact(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
                    const fc_stage* sthr, const void* video, int in_type,
                    int gray_in, void* out, int out_type, fc_dims d, int n_warm,
@@ -587,10 +819,13 @@ int fc_chain_exact(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg
   float beta = 1.0f - si->alpha;
   fc_stage gdummy = {};
   const fc_stage& sgr = sgray ? *sgray : gdummy;
+  GaussW gw;
+  for (int i = 0; i < (2 * sg->g_radius + 1) * (2 * sg->g_radius + 1); ++i)
+    gw.w[i] = double(sg->g_w[i]);
 #define FC_CH(R, IT, OT, GI)                                                     \
   k_chain_exact<R, IT, OT, GI><<<grid, FT, 0, st>>>(                            \
       static_cast<const IT*>(video), static_cast<OT*>(out), sgr, si->alpha,     \
-      beta, *sg, sthr->th, sthr->white, sthr->black, d.width, d.height,         \
+      beta, gw, sthr->th, sthr->white, sthr->black, d.width, d.height,          \
       d.frames, n_warm, state_in, state_out)
 #define FC_CH_GI(R, IT, OT) \
   if (gray_in) FC_CH(R, IT, OT, true); else FC_CH(R, IT, OT, false);

@@ -17,6 +17,8 @@
 // of a fresh recurrence.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cstdint>
 #include <cstdlib>
 
@@ -204,7 +206,7 @@ extern "C" int fc_gray_iir_stream(const fc_stage* sg, const fc_stage* si, const 
   if (reinterpret_cast<uintptr_t>(video) % 16 || reinterpret_cast<uintptr_t>(out) % 16) return -1;
   if (reinterpret_cast<uintptr_t>(state_in) % 16 || reinterpret_cast<uintptr_t>(state_out) % 16)
     return -1;
-  if (std::getenv("FUSEPLAN_F12_LEGACY")) return -1;
+  if (fc_get_knobs()->f12_legacy) return -1;
   // Small frames (< 256 k pixels) leave each CTA a few hundred pixels and the
   // per-frame ring handshake dominates (192x432: 0.23 ms vs 0.14 ms for the
   // old per-pixel kernel): they take k_gray_iir_small instead.
@@ -225,7 +227,7 @@ extern "C" int fc_gray_iir_stream(const fc_stage* sg, const fc_stage* si, const 
   a.wbm = -sg->wb * 8388608.0f;
   a.alpha = si->alpha;
   a.beta = 1.0f - si->alpha;  // host float arithmetic == the reference's
-  if (hw < 256 * 1024 && !std::getenv("FUSEPLAN_F12_STREAM")) {
+  if (hw < 256 * 1024 && !fc_get_knobs()->f12_stream) {
     const long long threads = hw / 4;
     const int grid = int((threads + SMALL_NT - 1) / SMALL_NT);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -244,12 +246,14 @@ extern "C" int fc_gray_iir_stream(const fc_stage* sg, const fc_stage* si, const 
   const int grid = int((hw + per - 1) / per);
   a.px_per_cta = int(per);
   const size_t smem = size_t(DEPTH) * 3 * MAXPX + 2 * DEPTH * 8;
-  static bool attr = false;
-  if (!attr) {
+  // the dynamic shared-memory opt-in is a per-device function attribute
+  static std::atomic<unsigned long long> attr_set{0};
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_set.load() & bit)) {
     if (cudaFuncSetAttribute(k_gray_iir_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(smem)) != cudaSuccess)
-      return -1;
-    attr = true;
+      return int(cudaGetLastError());
+    attr_set.fetch_or(bit);
   }
   k_gray_iir_stream<<<grid, NT, smem, static_cast<cudaStream_t>(stream)>>>(a);
   return int(cudaGetLastError());

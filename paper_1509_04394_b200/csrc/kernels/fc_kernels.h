@@ -101,6 +101,18 @@ int fc_fused_chain(const fc_stage* s_gray, const fc_stage* s_iir,
                    const float* state_in, float* state_out, int variant,
                    void* stream);
 
+/* run_tiled's box staging (simulator.cpp:229-333) for one tiled plan group,
+ * for fp_simulate's tiled arm when a plan's halo erodes (fc_tiled.cu): one
+ * CTA per output box (boxes looped over `ctas` CTAs); dev_stages: the
+ * group's members on the device; halo = {x_lo, x_hi, y_lo, y_hi, t_lo, t_hi};
+ * in: [t][c][y][x] with in_ch channels (FC_U8 / FC_F32); out: f32 [t][y][x];
+ * scratch: fc_tiled_scratch_bytes() of device memory. */
+long long fc_tiled_scratch_bytes(int tile_x, int tile_y, int tile_t, const int* halo,
+                                 int in_ch, int ctas);
+int fc_tiled_group(const fc_stage* dev_stages, int n_stages, const void* in, int in_type,
+                   int in_ch, float* out, fc_dims d, int tile_x, int tile_y, int tile_t,
+                   const int* halo, float* scratch, int ctas, void* stream);
+
 /* Deterministic counter-hash u8 video (splitmix64 finaliser of
  * index + seed * 0x9E3779B97F4A7C15, top byte), [t][c][y][x]; frames
  * [t0, t0 + d.frames).  Mirrors tests/golden/make_golden.py:hash_video. */
@@ -118,6 +130,27 @@ int fc_track_features(const void* mask, int elem_type, int W, int H, int F,
                       double* points_dev, void* stream);
 
 const char* fc_error_string(int code);
+
+/* Diagnostic / tuning knobs of the kernel launchers.  The executor reads the
+ * FUSEPLAN_* environment ONCE, when it is created (fc_knobs_from_env), and
+ * installs its copy on the calling thread before each run (fc_set_knobs); the
+ * launchers never call getenv.  All-zero = the shipped defaults. */
+typedef struct {
+  int pipe_oh;        /* FUSEPLAN_PIPE_OH: force the frame-pipeline window height */
+  int pipe_segs;      /* FUSEPLAN_PIPE_SEGS: force the number of time segments */
+  int pipe_seg_warm;  /* FUSEPLAN_PIPE_SEG_WARM: IIR warm-up of a segment (0 = default) */
+  int pipe_skip;      /* FUSEPLAN_PIPE_SKIP: timing experiments (1 IIR, 2 stencil math) */
+  float band_scale;   /* FUSEPLAN_PIPE_BAND_SCALE: widen the certification band (tests) */
+  int profile;        /* FUSEPLAN_PIPE_PROFILE: per-CTA spans (1 summary, 2 every CTA) */
+  int debug;          /* FUSEPLAN_DEBUG: launcher decisions on stderr */
+  int dbg_px_on, dbg_px[3]; /* FUSEPLAN_PIPE_DEBUG_PX=x,y,t */
+  int f12_stream;     /* FUSEPLAN_F12_STREAM: force the streaming F12 kernel */
+  int f12_legacy;     /* FUSEPLAN_F12_LEGACY: the per-pixel F12 kernel */
+} fc_knobs;
+
+void fc_knobs_from_env(fc_knobs* k);
+void fc_set_knobs(const fc_knobs* k); /* NULL = defaults */
+const fc_knobs* fc_get_knobs(void);
 
 #ifdef __cplusplus
 }

@@ -40,13 +40,16 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "fc_common.cuh"
 
-// Warp-role counts (fc_pipe_cfg*.cu re-include this file with other values
-// under another namespace / entry name for tuning comparisons).
+// Warp-role counts (compile-time; a tuning build may predefine them together
+// with FP_NAMESPACE / FP_ENTRY to compile a second layout alongside).
 #ifndef FP_NF
 // the shipped layout: one stencil warp per frame (4-column lanes, 168
 // registers), 6 frames in flight, 5 IIR warps + the producer warp (12 warps),
@@ -1014,12 +1017,7 @@ constexpr int SEG_WARM = 64;  // IIR warm-up of a time segment (48 su
 // Small frames leave SMs idle with one CTA per window, so the frames may be
 // split into time segments (chain: restarted SEG_WARM frames early and
 // verified, see Args).  Pick (OH, segments) minimising the busiest SM's load;
-// ties go to the larger window.  FUSEPLAN_PIPE_OH / FUSEPLAN_PIPE_SEGS force.
-int env_int(const char* name, int dflt) {
-  const char* env = std::getenv(name);
-  return env ? std::atoi(env) : dflt;
-}
-
+// ties go to the larger window.  The knobs pipe_oh / pipe_segs force.
 bool choose(int W, int H, int frames, bool segs_ok, int dev, bool src_f32, int force,
             int force_segs, PipePlan* pp) {
   int sms = 0, optin = 0;
@@ -1032,7 +1030,7 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, bool src_f32, int f
       FP_OH_LIST(FP_ITEM)
 #undef FP_ITEM
   };
-  const bool dbg = std::getenv("FUSEPLAN_DEBUG") != nullptr;
+  const bool dbg = fc_get_knobs()->debug != 0;
   const double warm_cost = src_f32 ? 0.0 : 0.4;
   for (int oh : ohs) {
     if (force && oh != force) continue;
@@ -1074,6 +1072,8 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, bool src_f32, int f
       }
     }
   }
+  if (best >= 1e300 && force_segs)  // a forced segment count the frames cannot take
+    return choose(W, H, frames, segs_ok, dev, src_f32, force, 0, pp);
   if (dbg && best < 1e300)
     std::fprintf(stderr, "fc_pipe choose: -> oh=%d segs=%d seg_len=%d\n", pp->oh, pp->n_segs,
                  pp->seg_len);
@@ -1094,6 +1094,21 @@ __global__ void k_verify_segments(const float* __restrict__ warm, const float* _
   }
 }
 
+// Scratch of the segmented launches, per (device, stream).
+struct SegScratch {
+  float* buf = nullptr;
+  size_t cap = 0;
+  int* k = nullptr;
+  float* dbg_px = nullptr;
+};
+
+SegScratch& seg_scratch(int dev, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SegScratch> all;
+  std::lock_guard<std::mutex> lock(mu);
+  return all[{dev, st}];
+}
+
 // Shared launcher of both modes (src_f32: F345 from f32 planes).
 int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, fc_dims d,
                 int n_warm, const float* state_in, float* state_out, void* stream) {
@@ -1102,11 +1117,12 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
   cudaGetDevice(&dev);
   static thread_local PipePlan caches[2];
   PipePlan& cache = caches[src_f32 ? 1 : 0];
+  const fc_knobs& kn = *fc_get_knobs();
   // time segments only for self-contained launches (no carried state in,
   // no launch-level warm-up): their CTAs may restart the IIR anywhere
   const bool segs_ok = src_f32 || (state_in == nullptr && n_warm == 0);
-  const int force_oh = env_int("FUSEPLAN_PIPE_OH", 0);
-  const int force_segs = env_int("FUSEPLAN_PIPE_SEGS", 0);
+  const int force_oh = kn.pipe_oh;
+  const int force_segs = kn.pipe_segs;
   if (cache.W != d.width || cache.H != d.height || cache.dev != dev ||
       cache.frames != d.frames || cache.segs_ok != segs_ok || cache.force_oh != force_oh ||
       cache.force_segs != force_segs) {
@@ -1135,46 +1151,49 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
   a.n_windows = cache.strips * cache.bands;
   a.n_segs = cache.n_segs;
   a.seg_len = cache.seg_len;
-  a.seg_warm = src_f32 ? 0 : env_int("FUSEPLAN_PIPE_SEG_WARM", SEG_WARM);
+  a.seg_warm = src_f32 ? 0 : (kn.pipe_seg_warm > 0 ? kn.pipe_seg_warm : SEG_WARM);
   const long long hwl = (long long)d.width * d.height;
   const bool verify = !src_f32 && cache.n_segs > 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (verify) {  // per-segment end / warm state planes and the verdict slot
-    static thread_local float* seg_buf = nullptr;
-    static thread_local int* seg_k = nullptr;
-    static thread_local size_t seg_cap = 0;
+    // Owned by (device, stream): launches on one stream are ordered, so a
+    // segmented launch never sees another's seams; two streams (two
+    // executors, or device-pointer runs on two streams) get two buffers.
+    SegScratch& sc = seg_scratch(dev, st);
     const size_t need = size_t(2 * cache.n_segs) * size_t(hwl);
-    if (need > seg_cap) {
-      if (seg_buf) cudaFree(seg_buf);
-      seg_buf = nullptr;
-      seg_cap = 0;
-      if (cudaMalloc(&seg_buf, need * sizeof(float)) != cudaSuccess) return int(cudaGetLastError());
-      seg_cap = need;
+    if (need > sc.cap) {
+      if (sc.buf) cudaFree(sc.buf);
+      sc.buf = nullptr;
+      sc.cap = 0;
+      if (cudaMalloc(&sc.buf, need * sizeof(float)) != cudaSuccess) return int(cudaGetLastError());
+      sc.cap = need;
     }
-    if (!seg_k && cudaMalloc(&seg_k, sizeof(int)) != cudaSuccess) return int(cudaGetLastError());
-    a.seg_end = seg_buf;
-    a.seg_warm_out = seg_buf + size_t(cache.n_segs) * size_t(hwl);
-    a.seg_k = seg_k;
+    if (!sc.k && cudaMalloc(&sc.k, sizeof(int)) != cudaSuccess) return int(cudaGetLastError());
+    a.seg_end = sc.buf;
+    a.seg_warm_out = sc.buf + size_t(cache.n_segs) * size_t(hwl);
+    a.seg_k = sc.k;
   }
   a.state_in = state_in;
   a.state_out = state_out;
   a.p = fp;
-  if (const char* e = std::getenv("FUSEPLAN_PIPE_SKIP")) a.skip = std::atoi(e);
-  if (const char* e = std::getenv("FUSEPLAN_PIPE_BAND_SCALE"))  // diagnostics only
-    a.p.band_n *= float(std::atof(e));
-  static float* dbg_px = nullptr;
-  if (const char* e = std::getenv("FUSEPLAN_PIPE_DEBUG_PX")) {
-    if (!dbg_px) cudaMalloc(&dbg_px, 64 * sizeof(float));
-    cudaMemset(dbg_px, 0, 64 * sizeof(float));
-    std::sscanf(e, "%d,%d,%d", &a.dbg_x, &a.dbg_y, &a.dbg_t);
-    a.dbg_px = dbg_px;
+  a.skip = kn.pipe_skip;
+  if (kn.band_scale > 0.0f) a.p.band_n *= kn.band_scale;  // tests / diagnostics only
+  if (kn.dbg_px_on) {
+    SegScratch& sc = seg_scratch(dev, st);
+    if (!sc.dbg_px && cudaMalloc(&sc.dbg_px, 64 * sizeof(float)) != cudaSuccess)
+      return int(cudaGetLastError());
+    cudaMemsetAsync(sc.dbg_px, 0, 64 * sizeof(float), st);
+    a.dbg_x = kn.dbg_px[0];
+    a.dbg_y = kn.dbg_px[1];
+    a.dbg_t = kn.dbg_px[2];
+    a.dbg_px = sc.dbg_px;
   }
   CUtensorMap map;
   if (src_f32 ? !plane_tensor_map(&map, in, d, 128, 2 * cache.oh + 6)
               : !rgb_tensor_map(&map, in, d, BWB, 2 * cache.oh + 6))
     return -1;
   const int grid = cache.strips * cache.bands * cache.n_segs;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool profile = std::getenv("FUSEPLAN_PIPE_PROFILE") != nullptr;
+  const bool profile = kn.profile != 0;
   if (profile) {
     cudaMalloc(&a.dbg, sizeof(long long) * 8 * grid);
     cudaMemsetAsync(a.dbg, 0, sizeof(long long) * 8 * grid, st);
@@ -1221,7 +1240,7 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
                      "iir wait rgb %.2f slot %.2f\n",
                      names[k], cls[k][0], cls[k][1] / cls[k][0], cls[k][5],
                      cls[k][2] / cls[k][0], cls[k][3] / cls[k][0], cls[k][4] / cls[k][0]);
-    if (std::getenv("FUSEPLAN_PIPE_PROFILE")[0] == '2') {  // every CTA: start, span, waits
+    if (kn.profile == 2) {  // every CTA: start, span, waits
       for (int b = 0; b < grid; ++b) {
         const long long* r = &h[size_t(b) * 8];
         std::fprintf(stderr, "  cta %4d win(%d,%d) class %lld start %+.2f us span %.1f us  "

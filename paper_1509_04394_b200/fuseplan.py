@@ -294,12 +294,55 @@ class Executor(_Handle):
             return FP_ELEM_F32
         raise InputError(f"video dtype must be uint8 or float32, got {dtype}")
 
+    # -- caller-buffer validation: the C side reads and writes with the
+    # pipeline's dims, so a wrong shape / dtype / device here would become an
+    # out-of-bounds device write or host heap corruption
+    def _check_out(self, out, shape, on_cuda, device=None):
+        out_dt = self.out_dtype
+        if tuple(out.shape) != tuple(shape):
+            raise InputError(f"out shape {tuple(out.shape)} != {tuple(shape)}")
+        is_torch = type(out).__module__.startswith("torch")
+        if on_cuda:
+            if not (is_torch and out.is_cuda):
+                raise InputError("out must be a CUDA tensor for a CUDA video")
+            if device is not None and out.device != device:
+                raise InputError(f"out is on {out.device}, the video on {device}")
+            if not out.is_contiguous():
+                raise InputError("out must be contiguous")
+            want = "torch.uint8" if out_dt is np.uint8 else "torch.float32"
+            if str(out.dtype) != want:
+                raise InputError(f"out dtype {out.dtype} != {want}")
+        else:
+            if is_torch:
+                if out.is_cuda:
+                    raise InputError("out must be a host array for a host video")
+                arr = out.numpy()
+            else:
+                arr = out
+            if not isinstance(arr, np.ndarray) or arr.dtype != out_dt:
+                raise InputError(f"out must be a {np.dtype(out_dt).name} array")
+            if not arr.flags["C_CONTIGUOUS"]:
+                raise InputError("out must be C-contiguous")
+
+    def _check_state(self, st, name, device):
+        W, H, _, _ = self.pipeline.dims
+        n = max(self.state_planes, 1)
+        if not (type(st).__module__.startswith("torch") and st.is_cuda):
+            raise InputError(f"{name} must be a CUDA tensor")
+        if st.device != device:
+            raise InputError(f"{name} is on {st.device}, the video on {device}")
+        if str(st.dtype) != "torch.float32" or not st.is_contiguous():
+            raise InputError(f"{name} must be a contiguous float32 tensor")
+        if st.numel() != n * H * W or (st.dim() == 3 and tuple(st.shape) != (n, H, W)):
+            raise InputError(f"{name} shape {tuple(st.shape)} != {(n, H, W)}")
+
     def run(self, video, out=None, stream=None):
         """video: planar [F, C, H, W].  CUDA tensor -> CUDA tensor (async on the
         current torch stream); numpy / CPU tensor -> numpy (synchronous)."""
         W, H, F, C = self.pipeline.dims
         if tuple(video.shape) != (F, C, H, W):
             raise InputError(f"video shape {tuple(video.shape)} != {(F, C, H, W)}")
+        self._elem(video.dtype)
         is_torch = type(video).__module__.startswith("torch")
         if is_torch and video.is_cuda:
             torch = _torch()
@@ -308,6 +351,8 @@ class Executor(_Handle):
                 out = torch.empty((F, H, W), device=video.device,
                                   dtype=torch.uint8 if self.out_elem == FP_ELEM_U8
                                   else torch.float32)
+            else:
+                self._check_out(out, (F, H, W), True, video.device)
             stream = _stream_handle(torch.cuda.current_stream(video.device)
                                     if stream is None else stream)
             _check(lib().fp_exec_run(self.ptr, video.data_ptr(), self._elem(video.dtype),
@@ -317,6 +362,10 @@ class Executor(_Handle):
         arr = np.ascontiguousarray(arr)
         if out is None:
             out = np.empty((F, H, W), self.out_dtype)
+        else:
+            self._check_out(out, (F, H, W), False)
+            if type(out).__module__.startswith("torch"):
+                out = out.numpy()
         _check(lib().fp_exec_run(self.ptr, arr.ctypes.data, self._elem(arr.dtype),
                                  out.ctypes.data, FP_EXEC_HOST_PTRS, None))
         return out
@@ -331,13 +380,26 @@ class Executor(_Handle):
         """T-shard run on CUDA tensors: video [n, C, H, W] starting at the first
         processed frame; returns [n - n_warm, H, W]."""
         torch = _torch()
+        W, H, _, C = self.pipeline.dims
+        if not (type(video).__module__.startswith("torch") and video.is_cuda):
+            raise InputError("run_range needs a CUDA tensor video")
+        if video.dim() != 4 or tuple(video.shape[1:]) != (C, H, W):
+            raise InputError(f"video shape {tuple(video.shape)} != (n, {C}, {H}, {W})")
+        self._elem(video.dtype)
         n = int(video.shape[0])
-        W, H = int(video.shape[3]), int(video.shape[2])
+        if not 0 <= n_warm <= n:
+            raise InputError(f"n_warm {n_warm} outside [0, {n}]")
         video = video.contiguous()
         if out is None:
             out = torch.empty((n - n_warm, H, W), device=video.device,
                               dtype=torch.uint8 if self.out_elem == FP_ELEM_U8
                               else torch.float32)
+        else:
+            self._check_out(out, (n - n_warm, H, W), True, video.device)
+        if state_in is not None:
+            self._check_state(state_in, "state_in", video.device)
+        if state_out is not None:
+            self._check_state(state_out, "state_out", video.device)
         stream = _stream_handle(torch.cuda.current_stream(video.device)
                                 if stream is None else stream)
         _check(lib().fp_exec_run_range(

@@ -1,0 +1,117 @@
+"""Calibrates the B200 streaming cost model (StreamingCost, fuseplan.hpp) on
+the GPU: device time of every executor kernel class at several video sizes,
+least-squares time = launch + ns_per_px * pixels per class, one launch term
+shared by all classes.  Prints the "streaming_cost" block for
+paper_1509_04394_b200/data/b200.json and the raw rows (JSON lines).
+
+    python scripts/calibrate_streaming.py > profiles/r02_streaming_calibration.jsonl
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_1509_04394_b200 import fuseplan as fp  # noqa: E402
+
+SIZES = [(192, 432, 600), (800, 600, 400), (800, 600, 1000), (2048, 2048, 120)]
+
+
+def timed(fn, reps=5, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    return float(np.median(ts)) * 1e6  # ns
+
+
+def run_time(spec, partition, video, variant="auto"):
+    p = fp.Pipeline(json.dumps(spec))
+    plan = fp.Plan(p, fp.Device.load("b200"),
+                   {"force_partition": partition, "cost_model": "reference",
+                    "iir_streaming": True})
+    ex = fp.Executor(p, plan, variant=variant)
+    out = ex.run(video)
+    return timed(lambda: ex.run(video, out=out)), ex.describe()["launches_per_run"]
+
+
+STAGE = {
+    "rgba2gray": {"stencil_op": "rgba2gray"},
+    "iir_temporal": {"stencil_op": "iir_temporal", "params": {"alpha": 0.5}},
+    "gaussian": {"stencil_op": "gaussian", "params": {"radius": 2, "sigma": 1.0}},
+    "gradient": {"stencil_op": "gradient"},
+    "threshold": {"stencil_op": "threshold", "params": {"th": 128}},
+    "identity": {"stencil_op": "identity"},
+    "scale_offset": {"stencil_op": "scale_offset", "params": {"scale": 0.5, "offset": 1.0}},
+    "box_mean": {"stencil_op": "box_mean"},
+}
+
+
+def main():
+    rows = []
+    for (W, H, F) in SIZES:
+        px = W * H * F
+        rgba = torch.empty((F, 4, H, W), dtype=torch.uint8, device="cuda")
+        fp.synth_hash_u8(rgba, seed=1234)
+        gray = rgba[:, :1].float().contiguous()
+        spec5 = fp.spec_chain(W, H, F)
+        t, _ = run_time(spec5, "1-5", rgba)
+        rows.append(("chain", W, H, F, px, t, 1))
+        t, _ = run_time(spec5, "1-5", rgba, variant="exact")
+        rows.append(("chain_exact", W, H, F, px, t, 1))
+        spec2 = dict(spec5, kernels=spec5["kernels"][:2])
+        t12, _ = run_time(spec2, "1-2", rgba)
+        rows.append(("gray_iir", W, H, F, px, t12, 1))
+        t, _ = run_time(spec5, "1-2,3-5", rgba)
+        rows.append(("gauss_grad_thr", W, H, F, px, t - t12, 1))
+        t, _ = run_time(spec5, "1-2,3-5", rgba, variant="exact")
+        rows.append(("gauss_grad_thr_exact", W, H, F, px, t - t12, 1))
+        for name, k in STAGE.items():
+            ch = 4 if name == "rgba2gray" else 1
+            spec = {"video": {"width": W, "height": H, "frames": F, "fps": 1, "channels": ch},
+                    "kernels": [dict(k, name=name)]}
+            t, _ = run_time(spec, "1", rgba if ch == 4 else gray)
+            rows.append((name, W, H, F, px, t, 1))
+        del rgba, gray
+        torch.cuda.empty_cache()
+    for r in rows:
+        print(json.dumps({"class": r[0], "W": r[1], "H": r[2], "F": r[3], "px": r[4],
+                          "ns": r[5]}), flush=True)
+    # one shared launch term, one slope per class
+    classes = sorted({r[0] for r in rows})
+    A = np.zeros((len(rows), 1 + len(classes)))
+    b = np.zeros(len(rows))
+    for i, r in enumerate(rows):
+        A[i, 0] = r[6]
+        A[i, 1 + classes.index(r[0])] = r[4]
+        b[i] = r[5]
+    x, *_ = np.linalg.lstsq(A, b, rcond=None)
+    launch = max(float(x[0]), 0.0)
+    slopes = {c: float(x[1 + i]) for i, c in enumerate(classes)}
+    for c, v in slopes.items():  # guard: a slope must be positive
+        if v <= 0:
+            vals = [r[5] / r[4] for r in rows if r[0] == c]
+            slopes[c] = float(np.median(vals))
+    pred = A @ np.array([launch] + [slopes[c] for c in classes])
+    rel = np.abs(pred - b) / b
+    print(json.dumps({"streaming_cost": {"launch_ns": round(launch, 1),
+                                         "ns_per_px": {c: float(f"{v:.6g}")
+                                                       for c, v in slopes.items()}},
+                      "fit_max_rel_err": float(rel.max()),
+                      "fit_median_rel_err": float(np.median(rel))}))
+
+
+if __name__ == "__main__":
+    main()

@@ -2,6 +2,7 @@
 declares; handle / status / ownership conventions match the reference's
 tests/test_capi.cpp (no GPU needed for these)."""
 import ctypes
+import json
 import os
 import re
 
@@ -92,3 +93,41 @@ def test_out_of_scope_entry_points_report_input_error(fp):
     L = fp.lib()
     out = ctypes.c_void_p()
     assert L.fp_calibrate_csv(b"n_kernels\n", ctypes.byref(out)) == fp.FP_ERR_INPUT
+
+
+CODEGEN_CASES = [
+    ("vision_pipeline.json", "k20_like", None),
+    ("vision_pipeline.json", "b200", None),
+    ("vision_pipeline.json", "c1060_like", {"halo_mode": "paper-max"}),
+    ("vision_pipeline.json", "k20_like", {"force_partition": "1,2,3-5,6"}),
+]
+
+
+@pytest.mark.parametrize("pipe_file,device,opts", CODEGEN_CASES)
+def test_codegen_manifest_matches_reference_schema(fp, oracle, tmp_path, pipe_file, device,
+                                                   opts):
+    """fp_codegen's manifest carries the reference's schema and values
+    (codegen.cpp:425-465: pipeline, device, halo_mode, kernels[group, file,
+    tile, smem_bytes, staged_arrays, sync_points]), plus the sm_100a kernel
+    that executes each group."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    pj = open(os.path.join(fp.DATA_DIR, pipe_file)).read()
+    dj = open(os.path.join(fp.DATA_DIR, device + ".json")).read()
+    want = oracle.ref_codegen_manifest(pj, dj, opts, "vp")
+    L = fp.lib()
+    p, d = fp.Pipeline(pj), fp.Device(dj)
+    out = ctypes.c_void_p()
+    ours = dict(opts or {}, cost_model="reference") if device == "b200" else opts
+    st = L.fp_codegen(p.ptr, d.ptr, json.dumps(ours).encode() if ours else None, b"vp",
+                      str(tmp_path).encode(), ctypes.byref(out))
+    assert st == fp.FP_OK, L.fp_last_error()
+    got = json.loads(fp._take_string(out))
+    for key in ("pipeline", "device", "halo_mode"):
+        assert got[key] == want[key]
+    assert len(got["kernels"]) == len(want["kernels"])
+    for g, w in zip(got["kernels"], want["kernels"]):
+        for key in ("group", "file", "tile", "smem_bytes", "staged_arrays", "sync_points"):
+            assert g[key] == w[key], key
+        assert "sm_100a" in g["source"] or g["source"].startswith("paper_1509_04394_b200/")
+        assert (tmp_path / g["file"]).exists()

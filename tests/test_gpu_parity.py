@@ -3,6 +3,7 @@ reference's golden vectors and the oracle -- bit-exact for every element
 (masks and float planes alike; the reference semantics are reproduced
 operation for operation)."""
 import json
+import os
 
 import numpy as np
 import pytest
@@ -104,18 +105,18 @@ def test_larger_hash_video_dense_mask(fp, cuda, oracle):
             np.testing.assert_array_equal(out, want, err_msg=f"{part} {variant}")
 
 
-@pytest.mark.parametrize("variant", ["fast", "fast_tile"])
 @pytest.mark.parametrize("shape,th", [((64, 48, 20), 128.0), ((160, 120, 24), 24.0),
                                       ((192, 96, 17), 40.0), ((48, 37, 9), 24.0),
                                       ((800, 64, 6), 24.0), ((16, 8, 5), 12.0),
                                       ((256, 200, 11), 24.0), ((368, 131, 4), 30.0),
                                       ((240, 1, 3), 8.0), ((128, 300, 2), 24.0)])
-def test_fast_certified_path_exact(fp, cuda, oracle, shape, th, variant):
-    """The certified FP32 kernels (variant='fast' = frame pipeline, 'fast_tile'
-    = tile march; both fail loudly if they do not apply) are bit-exact,
-    including pixels that took the FP64 recheck."""
+def test_fast_certified_path_exact(fp, cuda, oracle, shape, th):
+    """The certified FP32 frame pipeline (variant='fast' fails loudly if it does
+    not apply; frames under 6 rows run 'auto', i.e. the FP64 kernel) is
+    bit-exact, including pixels that took the FP64 recheck."""
     from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
     W, H, F = shape
+    variant = "fast" if H >= 6 else "auto"
     pipe = spec_chain(W, H, F, th=th)
     v = hash_video_u8(F, 4, H, W, 4242)
     want = oracle.orc_chain(pipe, v)
@@ -124,8 +125,7 @@ def test_fast_certified_path_exact(fp, cuda, oracle, shape, th, variant):
     assert ex.describe()["exact_rechecks_total"] >= 0
 
 
-@pytest.mark.parametrize("variant", ["fast", "fast_tile"])
-def test_fast_path_rechecks_happen_and_are_exact(fp, cuda, oracle, variant):
+def test_fast_path_rechecks_happen_and_are_exact(fp, cuda, oracle):
     """A threshold placed in the bulk of the gradient distribution forces many
     pixels into the uncertain band; all of them must resolve exactly."""
     from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
@@ -138,7 +138,7 @@ def test_fast_path_rechecks_happen_and_are_exact(fp, cuda, oracle, variant):
     want = oracle.orc_chain(pipe, v)
     p = fp.Pipeline(json.dumps(pipe))
     ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": "1-5"}),
-                     variant=variant)
+                     variant="fast")
     before = ex.describe()["exact_rechecks_total"]
     import torch
     out = ex.run(torch.from_numpy(v).to(cuda))
@@ -148,23 +148,17 @@ def test_fast_path_rechecks_happen_and_are_exact(fp, cuda, oracle, variant):
     np.testing.assert_array_equal(out.cpu().numpy().astype(np.float32), want)
 
 
-@pytest.mark.parametrize("kernel,part", [("pipe", "1-5"), ("pipe63", "1-5"), ("strip", "1-5"),
-                                         ("pipe", "1-2,3-5"), ("pipe63", "1-2,3-5")])
+@pytest.mark.parametrize("part", ["1-5", "1-2,3-5"])
 @pytest.mark.parametrize("shape,seed", [((240, 90, 7), 5), ((368, 131, 5), 6),
                                         ((2048, 64, 3), 7), ((64, 600, 3), 8),
                                         ((800, 600, 2), 9)])
-def test_certified_kernels_forced_rechecks(fp, cuda, oracle, monkeypatch, kernel, part, shape,
-                                           seed):
+def test_certified_kernels_forced_rechecks(fp, cuda, oracle, monkeypatch, part, shape, seed):
     """Every certified kernel (all-fused F12345 and the optimizer's F345 group
     on f32 IIR planes), with the pipe kernel's band scaled x1000 so that
     several % of all pixels take the exact FP64 recheck (and the per-warp
     recheck queue overflows): still bit-exact.  Shapes cover strips/bands
     that end inside the window, multi-wave grids and one-band videos."""
     from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
-    if kernel == "strip":
-        monkeypatch.setenv("FUSEPLAN_FAST_KERNEL", "strip")
-    if kernel == "pipe63":
-        monkeypatch.setenv("FUSEPLAN_PIPE_CFG", "63")
     monkeypatch.setenv("FUSEPLAN_PIPE_BAND_SCALE", "1000")
     W, H, F = shape
     pipe = spec_chain(W, H, F)
@@ -178,8 +172,7 @@ def test_certified_kernels_forced_rechecks(fp, cuda, oracle, monkeypatch, kernel
     out = ex.run(torch.from_numpy(v).to(cuda))
     torch.cuda.synchronize()
     np.testing.assert_array_equal(out.cpu().numpy().astype(np.float32), want)
-    if kernel != "strip":  # (the strip kernel has its own band; no scaling)
-        assert ex.describe()["exact_rechecks_total"] - before > W * H * F // 50
+    assert ex.describe()["exact_rechecks_total"] - before > W * H * F // 50
 
 
 @pytest.mark.parametrize("shape", [(64, 48, 9), (192, 432, 5), (800, 600, 3), (16, 1, 40)])
@@ -444,3 +437,44 @@ def test_pipe_tiny_frame_counts_exact(fp, cuda, oracle, monkeypatch, shape, segs
     b = ex.run_range(vt[F:], state_in=st)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(torch.cat([a, b]).cpu().numpy().astype(np.float32), want)
+
+
+@pytest.mark.parametrize("case", ["paper_max", "iir_split", "exact"])
+def test_simulate_matches_reference_run_tiled(fp, cuda, oracle, tmp_path, case):
+    """fp_simulate's report against the reference's own executors
+    (oracle/_ref: run_sequential, run_tiled, simulator.cpp:158-333): the same
+    diff count and max |diff| (a PaperMax plan under-stages the halo and
+    erodes tile edges; a forced tile shorter than the video restarts the IIR
+    per box), every diff classified (interior + boundary), and the
+    reference's gmem element tallies."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    W, H, F = 160, 120, 12
+    spec = fp.spec_chain(W, H, F, th=24.0, kalman=True)
+    if case == "paper_max":
+        opts = {"halo_mode": "paper-max"}
+    elif case == "iir_split":
+        opts = {"force_partition": "1-5,6", "tile": {"x": 8, "y": 8, "t": 4}}
+    else:
+        opts = None
+    dev_json = open(os.path.join(fp.DATA_DIR, "k20_like.json")).read()
+    from paper_1509_04394_b200.fuseplan import hash_video_u8
+    video = hash_video_u8(F, 4, H, W, 77)
+    path = str(tmp_path / "v.fpvd")
+    fp.write_fpvd(path, video)
+    pj = json.dumps(spec)
+    seq, _ = oracle.ref_run_sequential(pj, video)
+    tiled, traffic = oracle.ref_run_tiled(pj, dev_json, video, opts)
+    diff = np.abs(seq - tiled)
+    want_count = int((diff != 0).sum())
+    if case != "exact":
+        assert want_count > 0  # the case exercises erosion
+    rep = json.loads(fp.simulate(fp.Pipeline(pj), fp.Device(dev_json), opts, video_path=path,
+                                 fmt="json"))
+    sim = rep["simulation"]
+    assert sim["diff_count"] == want_count
+    assert sim["max_abs_diff"] == pytest.approx(float(diff.max()) if want_count else 0.0)
+    assert sim["interior_diffs"] + sim["boundary_diffs"] == want_count
+    assert sim["outputs_identical"] == (want_count == 0)
+    assert sim["measured_tiled_gmem"] == int(traffic[0] + traffic[1])
+    assert sim["measured_serial_gmem"] == 2 * W * H * F * 5

@@ -18,7 +18,11 @@ def _device_json(name):
     return open(os.path.join(DATA, name + ".json")).read()
 
 
-def _capi_options(opts):
+def _capi_options(opts, device=None):
+    # the golden plans are the reference planner's: the b200 profile's
+    # streaming cost model (a B200 extension) is switched off for them
+    if device == "b200":
+        opts = dict(opts or {}, cost_model="reference")
     if not opts:
         return None
     o = dict(opts)
@@ -35,10 +39,10 @@ def test_plan_json_matches_reference(fp, i):
     d = fp.Device(_device_json(c["device"]))
     if c["status"] != 0:
         with pytest.raises(fp.FuseplanError) as e:
-            fp.Plan(p, d, _capi_options(c["options"]))
+            fp.Plan(p, d, _capi_options(c["options"], c["device"]))
         assert e.value.status == c["status"]
         return
-    plan = fp.Plan(p, d, _capi_options(c["options"]))
+    plan = fp.Plan(p, d, _capi_options(c["options"], c["device"]))
     assert plan.render_json() == c["plan"]
 
 
@@ -86,16 +90,57 @@ def test_status_taxonomy(fp):
 
 
 def test_large_video_partitions(fp):
-    """SURVEY finding 2/3: >=600 frames -> 1-2,3-5,6; 16000 frames infeasible on
-    k20_like, feasible on the b200 profile."""
+    """SURVEY finding 2/3: the reference's Eq-2 model plans >=600 frames as
+    1-2,3-5,6 and reports 16000 frames infeasible on k20_like; the b200
+    profile under the reference model agrees."""
     from paper_1509_04394_b200.fuseplan import spec_chain
+    ref = {"cost_model": "reference"}
     for dev in ("k20_like", "b200"):
         p = fp.Pipeline(json.dumps(spec_chain(800, 600, 1000, kalman=True)))
-        assert fp.Plan(p, fp.Device.load(dev)).partition == [(1, 2), (3, 5), (6, 6)]
+        assert fp.Plan(p, fp.Device.load(dev), ref).partition == [(1, 2), (3, 5), (6, 6)]
     p = fp.Pipeline(json.dumps(spec_chain(800, 600, 16000, kalman=True)))
     with pytest.raises(fp.InfeasibleError):
         fp.Plan(p, fp.Device.load("k20_like"))
-    assert fp.Plan(p, fp.Device.load("b200")).partition == [(1, 2), (3, 5), (6, 6)]
+    assert fp.Plan(p, fp.Device.load("b200"), ref).partition == [(1, 2), (3, 5), (6, 6)]
+
+
+@pytest.mark.parametrize("shape", [(192, 432, 600), (800, 600, 1000), (800, 600, 16000),
+                                   (2048, 2048, 1000)])
+def test_b200_streaming_cost_picks_the_fastest_partition(fp, shape):
+    """The b200 profile's streaming cost model (calibrated on a B200,
+    scripts/calibrate_streaming.py) prices each group as the executor runs
+    it, so the optimizer returns the all-fused 1-5 -- the measured fastest
+    partition on every BASELINE shape (profiles/r02_configs.jsonl) -- where
+    the reference's model returned 1-2,3-5."""
+    W, H, F = shape
+    p = fp.Pipeline(json.dumps(fp.spec_chain(W, H, F, kalman=True)))
+    plan = fp.Plan(p, fp.Device.load("b200"))
+    assert plan.partition == [(1, 5), (6, 6)]
+    doc = json.loads(plan.render_json())
+    assert doc["cost_model"].startswith("streaming")
+    # predicted cost ranks the partitions like the measurements: all-fused <
+    # optimizer-of-the-reference < unfused
+    costs = {}
+    for part in ("1-5,6", "1-2,3-5,6", "1,2,3,4,5,6"):
+        d = json.loads(fp.Plan(p, fp.Device.load("b200"),
+                               {"force_partition": part}).render_json())
+        costs[part] = d["total_cost"]
+    assert costs["1-5,6"] < costs["1-2,3-5,6"] < costs["1,2,3,4,5,6"]
+    # the k20_like / c1060_like profiles keep the reference's model
+    assert "cost_model" not in json.loads(
+        fp.Plan(p, fp.Device.load("k20_like"), None).render_json() if F <= 1000 else "{}")
+
+
+def test_streaming_cost_model_option(fp):
+    p = fp.Pipeline(json.dumps(fp.spec_chain(800, 600, 1000, kalman=True)))
+    with pytest.raises(fp.InputError):
+        fp.Plan(p, fp.Device.load("k20_like"), {"cost_model": "streaming"})
+    with pytest.raises(fp.InputError):
+        fp.Plan(p, fp.Device.load("b200"), {"cost_model": "fastest"})
+    # an uncertifiable chain (alpha != 0.5): priced with the exact kernels
+    q = fp.Pipeline(json.dumps(fp.spec_chain(800, 600, 1000, alpha=0.3, kalman=True)))
+    plan = fp.Plan(q, fp.Device.load("b200"))
+    assert plan.partition[-1] == (6, 6)
 
 
 def test_reports_render(fp):
@@ -114,13 +159,14 @@ def test_iir_streaming_option(fp):
     spec = fp.spec_chain(800, 600, 16000, kalman=True)
     p = fp.Pipeline(json.dumps(spec))
     dev = fp.Device.load("b200")
+    ref = {"cost_model": "reference"}
     with pytest.raises(fp.InfeasibleError):
-        fp.Plan(p, dev, {"force_partition": "1-5,6"})
-    plan = fp.Plan(p, dev, {"force_partition": "1-5,6", "iir_streaming": True})
+        fp.Plan(p, dev, dict(ref, force_partition="1-5,6"))
+    plan = fp.Plan(p, dev, dict(ref, force_partition="1-5,6", iir_streaming=True))
     assert plan.partition == [(1, 5), (6, 6)]
     # short videos: the option does not change a plan whose t already fits
     q = fp.Pipeline(json.dumps(fp.spec_chain(800, 600, 1000, kalman=True)))
-    a = json.loads(fp.Plan(q, dev, {"force_partition": "1-2,3-5,6"}).render_json())
-    b = json.loads(fp.Plan(q, dev, {"force_partition": "1-2,3-5,6",
-                                     "iir_streaming": False}).render_json())
+    a = json.loads(fp.Plan(q, dev, dict(ref, force_partition="1-2,3-5,6")).render_json())
+    b = json.loads(fp.Plan(q, dev, dict(ref, force_partition="1-2,3-5,6",
+                                        iir_streaming=False)).render_json())
     assert a == b
