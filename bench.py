@@ -7,13 +7,14 @@ frames/s and Mpixel/s of the fused chain on 800x600 video; HBM GB/s vs peak).
 One step = one pass of the chain over the whole synthetic video of the
 configuration (config 3: 800x600x1000 u8 RGBA, SPEC chain
 rgba2gray -> iir(0.5) -> gaussian(r2,s1) -> gradient -> threshold(128)),
-the video already resident in HBM.  N > 1 (torchrun): an N x 1000-frame
-video (--scaling weak, default; --scaling strong splits the 1000 frames) is
-sharded along T; every rank but the first warms its IIR up over 64 frames before its
-shard, then every rank sends its IIR carry to the next (NCCL send/recv, all
-at once), verifies the one it received bit for bit, and one all-reduce finds
-the first wrong warm state (fix-up chain only from there) -- all inside the
-timed region.
+the video already resident in HBM.  N > 1 (torchrun; --scaling strong,
+default = BASELINE config 3): the 1000-frame video is split N ways along T
+(--scaling weak: an N x 1000-frame video, 1000 frames per GPU); every rank
+but the first restarts its IIR 48 frames before its shard, then every rank
+sends its IIR carry to the next (NCCL send/recv, all at once), checks it
+against its warm state (fp_exec_converge: the frames a wrong start reaches),
+and one all-reduce finds the first wrong rank; the repair re-runs only the
+frames it reaches -- all inside the timed region.
 
 Prints ONE JSON line on rank 0.
 """
@@ -38,7 +39,7 @@ CONFIGS = {
     "5": (2048, 2048, 1000, "2048x2048x1000"),
 }
 ALG_BYTES_PER_PX = 4  # R, G, B u8 read once + u8 mask written once
-WARMUP_FRAMES = 64    # IIR warm-up before a T-shard (48 suffices)
+WARMUP_FRAMES = 48    # IIR warm-up before a T-shard (48 -> no mismatch)
 METRIC = "frames/sec & Mpixel/s of fused chain, 800x600 video; HBM GB/s vs peak; 1-8 GPU"
 
 
@@ -208,9 +209,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the oracle check of the timed output")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = F frames per GPU (N x F-frame video), "
-                         "strong = the F-frame video split N ways")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N > 1: strong (BASELINE config 3) = the F-frame video split "
+                         "N ways; weak = F frames per GPU (an N x F-frame video)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: carry planes staged through the host (lets N ranks "
                          "share one GPU for testing)")
@@ -282,12 +283,17 @@ def main():
         return s_warm_buf
 
     def run_shard(first, n, n_warm, state_in):
-        # video holds frames [lo - warm, hi) of the full video
+        # video holds frames [lo - warm, hi) of the full video; a repair run
+        # (n < the shard) rewrites the shard's first n - n_warm output frames
         v = video[first - (lo - warm):first - (lo - warm) + n]
         s_out = bufs.setdefault(("s", n_warm > 0), torch.empty((1, H, W), device=dev))
-        o = mask[:0] if n == n_warm else mask
+        o = mask[:n - n_warm]
         ex.run_range(v, n_warm=n_warm, state_in=state_in, state_out=s_out, out=o)
         return o, s_out
+
+    def converge(s_true, s_warm):
+        # frames of the shard a start from s_warm instead of s_true changes
+        return ex.converge(video[warm:], s_true, s_warm)
 
     host_stage = args.dist_backend == "gloo"
 
@@ -317,7 +323,7 @@ def main():
         # verify, fix-up re-run on mismatch (paper_1509_04394_b200/sharding.py)
         # world 2: the chain is one link anyway; beyond, verify in parallel
         run_sharded(shard, run_shard, send, recv, torch.equal, events,
-                    first_bad if world > 2 else None, warm_state)
+                    first_bad if world > 2 else None, warm_state, converge=converge)
 
     for _ in range(args.warmup):
         step()
@@ -467,7 +473,8 @@ def main():
                    "chain": "SPEC K1..K5 (+K6 host)",
                    "partition": plan.partition, "variant": args.variant,
                    "l2": "inputs larger than L2 (1.92 GB video)",
-                   "sharding": f"T-shards, {WARMUP_FRAMES}-frame IIR warm-up",
+                   "sharding": f"T-shards, {WARMUP_FRAMES}-frame IIR warm-up, carry check "
+                               "+ time-sparse repair",
                    "parallelism": f"T-shard x{world}" if world > 1 else "single GPU"},
         "mpix_per_s": fps * W * H / 1e6,
         "hbm_gbps_alg": ALG_BYTES_PER_PX * W * H * fps / 1e9,
@@ -478,6 +485,7 @@ def main():
         "clocks": clocks.summary(),
         "kernels": desc_ex,
         "carry_fixups": events["fixups"],
+        "carry_fixed_frames": events.get("fixed_frames", 0),
         "parity": parity,
     }
     print(json.dumps(line))

@@ -140,6 +140,37 @@ fp_status fp_exec_run_range(fp_exec* e, const void* video, int in_type,
                             const float* state_in, float* state_out,
                             void* stream);
 
+/* T-shard carry check: video holds a shard's n_frames frames
+ * on the executor's device, which ran from the warm state s_warm (its IIR
+ * restarted some frames before the shard); s_true is the true carry from the
+ * previous shard (W*H floats each, device).  *frames_out = how many leading
+ * frames of the shard's output differ from an exact run (0: none; n_frames:
+ * the end state differs too), from a gray+IIR re-run of only the pixels
+ * whose two states differ.  Re-running those frames from s_true makes the
+ * shard exact.  Synchronous.  FP_ERR_INPUT unless the chain opens with
+ * [rgba2gray,] iir_temporal. */
+fp_status fp_exec_converge(fp_exec* e, const void* video, int in_type, int n_frames,
+                           const float* s_true, const float* s_warm, int* frames_out,
+                           void* stream);
+
+/* ---- multi-GPU: one process, one host thread, N devices ------------------
+ * The video is split along T into n_devices shards (devices[] may repeat a
+ * device).  Each shard restarts its IIR "warmup_frames" (default 48) frames
+ * early, runs on its device, and the shards' carries move device to device
+ * (cudaMemcpyPeerAsync); a carry that differs from the shard's warm state
+ * triggers a re-run of only the frames it affects (fp_exec_converge), in
+ * rank order.  Output identical to a single-device run for any warm-up.
+ * options_json: fp_exec_create's keys plus {"warmup_frames": W}. */
+typedef struct fp_shard_exec fp_shard_exec;
+fp_status fp_shard_exec_create(const fp_pipeline* p, const fp_plan* plan, const int* devices,
+                               int n_devices, const char* options_json, fp_shard_exec** out);
+void fp_shard_exec_free(fp_shard_exec* e);
+/* Host buffers: planar [t][c][y][x] video of the pipeline's dims, element
+ * type in_type; out [t][y][x] of the executor's output type.  Synchronous. */
+fp_status fp_shard_exec_run(fp_shard_exec* e, const void* video, int in_type, void* out);
+/* JSON: shards (device, frames, warm-up) and the last run's fix-ups. */
+fp_status fp_shard_exec_stats(const fp_shard_exec* e, char** out_json);
+
 /* FPVD file -> FPVD file (video.cpp:46-109), streamed through the GPU:
  * chunks of host_chunk_frames frames are read into pinned buffers while the
  * previous chunk runs, the IIR carried exactly between chunks, the output

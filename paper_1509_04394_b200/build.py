@@ -35,21 +35,25 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false",
                      "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"]
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
-             "-Wno-unused-function", f"-I{JSON_DIR}", f"-I{CUDA_HOME}/include"]
+             "-Wno-unused-function", f"-I{os.path.join(ROOT, 'include')}", f"-I{JSON_DIR}",
+             f"-I{CUDA_HOME}/include"]
 
 HOST_SRCS = ["host/model.cpp", "host/planner.cpp", "host/video.cpp",
              "host/exec.cpp", "host/capi.cpp",
-             "host/calibrate.cpp"]
+             "host/calibrate.cpp", "host/shard.cpp", "host/simulate.cpp"]
 CUDA_SRCS = ["kernels/fc_exact.cu", "kernels/fc_pipe.cu", "kernels/fc_f12.cu",
-             "kernels/fc_track.cu", "kernels/fc_tiled.cu", "kernels/fc_dispatch.cu"]
-HEADERS = ["kernels/fc_pipe.cu", "host/fuseplan.hpp", "host/exec.hpp", "host/video.hpp",
+             "kernels/fc_track.cu", "kernels/fc_tiled.cu", "kernels/fc_shard.cu",
+             "kernels/fc_dispatch.cu"]
+HEADERS = ["kernels/fc_pipe.cu", "host/exec.hpp", "host/video.hpp",
            "kernels/fc_kernels.h", "kernels/fc_common.cuh"]
+PUBLIC_HEADERS = ["fuseplan.h", "fuseplan/fuseplan.hpp", "fuseplan/video.hpp",
+                  "fuseplan/simulator.hpp"]
 
 
 def _newest_header() -> float:
     ts = [os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS
           if os.path.exists(os.path.join(CSRC, h))]
-    ts.append(os.path.getmtime(os.path.join(ROOT, "include", "fuseplan.h")))
+    ts += [os.path.getmtime(os.path.join(ROOT, "include", h)) for h in PUBLIC_HEADERS]
     return max(ts)
 
 

@@ -13,7 +13,7 @@
 #include <string>
 #include <vector>
 
-#include "fuseplan.hpp"
+#include "../../../include/fuseplan/fuseplan.hpp"
 
 namespace fuseplan {
 

@@ -11,13 +11,15 @@
 #include <cstring>
 #include <map>
 #include <filesystem>
+#include <functional>
 #include <fstream>
 #include <iomanip>
 #include <memory>
 #include <sstream>
 
 #include "exec.hpp"
-#include "fuseplan.hpp"
+#include "../../../include/fuseplan/fuseplan.hpp"
+#include "../../../include/fuseplan/simulator.hpp"
 #include "json.hpp"
 #include "video.hpp"
 
@@ -26,6 +28,10 @@ using ordered_json = nlohmann::ordered_json;
 
 namespace fuseplan {
 void calibrate_csv(const std::string& text, double params[4], double* rms);  // calibrate.cpp
+// run_tiled's box staging on the device (simulate.cpp): host video in
+// (in_type FC_U8 / FC_F32), single-channel float output
+void device_run_tiled(const Pipeline& p, const FusionPlan& fp, const void* video, int in_type,
+                      float* out);
 }
 
 struct fp_pipeline {
@@ -214,218 +220,6 @@ OptionMetrics metrics_of(const std::string& name, const Pipeline& p, const Devic
 }
 
 // Device element traffic of one executor run, by construction of the kernels:
-// Element tallies of the reference's two executors, by its own counting
-// rules (simulator.cpp:158-177 and :238-333): whole-frame stages read and
-// write every pixel once; a tiled group reads each box's staged volume
-// (box + group halo, clamped boxes at the video edge) and writes the box.
-// These are the numbers the reference reports under "measured_*_gmem" -- a
-// deterministic count of the schedule's accesses, not a hardware counter.
-struct Tallies {
-  std::int64_t serial = 0, tiled = 0;
-};
-
-Tallies traffic_tallies(const Pipeline& p, const FusionPlan& fp) {
-  const VideoDims& v = p.video;
-  const std::int64_t px = v.pixel_volume();
-  Tallies t;
-  for (const KernelDesc& k : p.kernels)
-    if (k.scope != KernelScope::GlobalAggregation) t.serial += 2 * px;
-  auto axis_sum = [](int extent, int tile, int halo) {
-    std::int64_t s = 0;
-    for (int b = 0; b < extent; b += tile) s += std::min(tile, extent - b) + halo;
-    return s;
-  };
-  for (const PlanGroup& g : fp.groups) {
-    if (g.global_aggregation) continue;
-    if (!g.tiled) {
-      t.tiled += 2 * px * (g.last - g.first + 1);
-      continue;
-    }
-    t.tiled += axis_sum(v.width, g.tile.x, g.halo.x_lo + g.halo.x_hi) *
-                   axis_sum(v.height, g.tile.y, g.halo.y_lo + g.halo.y_hi) *
-                   axis_sum(v.frames, g.tile.t, g.halo.t_lo + g.halo.t_hi) +
-               px;
-  }
-  return t;
-}
-
-// Erosion of the executed plan's staged halos against the exact cumulative
-// requirement, and the first tiled group's tile as the diff grid
-// (capi.cpp:324-347 of the reference).
-struct DiffGrid {
-  Halo erode;
-  bool have_grid = false;
-  TileShape grid;
-};
-
-DiffGrid diff_grid(const Pipeline& p, const FusionPlan& fp) {
-  DiffGrid dg;
-  for (const PlanGroup& g : fp.groups) {
-    if (!g.tiled) continue;
-    std::span<const KernelDesc> members(p.kernels.data() + (g.first - 1),
-                                        std::size_t(g.last - g.first + 1));
-    const Halo cum = fused_halo(members, HaloMode::Cumulative);
-    dg.erode.x_lo = std::max(dg.erode.x_lo, cum.x_lo - g.halo.x_lo);
-    dg.erode.x_hi = std::max(dg.erode.x_hi, cum.x_hi - g.halo.x_hi);
-    dg.erode.y_lo = std::max(dg.erode.y_lo, cum.y_lo - g.halo.y_lo);
-    dg.erode.y_hi = std::max(dg.erode.y_hi, cum.y_hi - g.halo.y_hi);
-    dg.erode.t_lo = std::max(dg.erode.t_lo, cum.t_lo - g.halo.t_lo);
-    dg.erode.t_hi = std::max(dg.erode.t_hi, cum.t_hi - g.halo.t_hi);
-    if (!dg.have_grid) {
-      dg.grid = g.tile;
-      dg.have_grid = true;
-    }
-  }
-  return dg;
-}
-
-struct Diff {
-  float max_abs = 0.0f;
-  std::int64_t count = 0, interior = 0, boundary = 0;
-};
-
-// compare_outputs (simulator.cpp:335-368): diff count, max |a - b|, and the
-// split into diffs inside the tile grid's eroded interior vs near a tile
-// boundary.  Single-channel [t][y][x] planes.
-Diff compare_outputs(const std::vector<float>& a, const std::vector<float>& b,
-                     const VideoDims& v, const DiffGrid& dg) {
-  const TileShape grid = dg.have_grid ? dg.grid : TileShape{v.width, v.height, v.frames};
-  auto interior_1d = [](int c, int extent, int step, int lo, int hi) {
-    const int start = (c / step) * step;
-    const int end = std::min(start + step, extent);
-    return (c - start) >= lo && (end - 1 - c) >= hi;
-  };
-  Diff r;
-  std::size_t i = 0;
-  for (int t = 0; t < v.frames; ++t)
-    for (int y = 0; y < v.height; ++y)
-      for (int x = 0; x < v.width; ++x, ++i) {
-        const float d = std::abs(a[i] - b[i]);
-        if (d == 0.0f) continue;
-        r.max_abs = std::max(r.max_abs, d);
-        ++r.count;
-        const bool in = interior_1d(x, v.width, grid.x, dg.erode.x_lo, dg.erode.x_hi) &&
-                        interior_1d(y, v.height, grid.y, dg.erode.y_lo, dg.erode.y_hi) &&
-                        interior_1d(t, v.frames, grid.t, dg.erode.t_lo, dg.erode.t_hi);
-        ++(in ? r.interior : r.boundary);
-      }
-  return r;
-}
-
-// A plan whose tiled execution differs from the sequential one: a staged halo
-// short of the cumulative requirement (PaperMax), or a recurrence group cut
-// into boxes shorter than the video (its IIR restarts per box).
-bool tiling_erodes(const Pipeline& p, const FusionPlan& fp, const DiffGrid& dg) {
-  const Halo& e = dg.erode;
-  if (e.x_lo > 0 || e.x_hi > 0 || e.y_lo > 0 || e.y_hi > 0 || e.t_lo > 0 || e.t_hi > 0)
-    return true;
-  for (const PlanGroup& g : fp.groups) {
-    if (!g.tiled) continue;
-    for (int id = g.first; id <= g.last; ++id)
-      if (p.kernels[std::size_t(id - 1)].stencil_op == "iir_temporal" &&
-          (g.tile.t < p.video.frames || g.halo.t_lo > 0))
-        return true;
-  }
-  return false;
-}
-
-void cuda_ok2(cudaError_t e, const char* what) {
-  if (e != cudaSuccess)
-    throw Error(ErrorKind::Internal, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-// run_tiled (simulator.cpp:298-333) on the device: whole-frame groups as
-// per-stage kernels, tiled groups through fc_tiled_group's box staging.
-std::vector<float> run_tiled_on_device(const Pipeline& p, const FusionPlan& fp,
-                                       const HostVideo& video) {
-  const VideoDims& v = p.video;
-  const std::int64_t hw = std::int64_t(v.width) * v.height, px = hw * v.frames;
-  const int in_type = video.elem == ElemType::U8 ? FC_U8 : FC_F32;
-  const std::size_t vbytes = std::size_t(px) * v.channels * (in_type == FC_U8 ? 1 : 4);
-  cuda_ok2(cudaSetDevice(0), "cudaSetDevice");
-  struct Dev {
-    void* p = nullptr;
-    ~Dev() { if (p) cudaFree(p); }
-  } dvid, da, db, dscr, dst;
-  cuda_ok2(cudaMalloc(&dvid.p, vbytes), "cudaMalloc video");
-  cuda_ok2(cudaMemcpy(dvid.p, video.data(), vbytes, cudaMemcpyHostToDevice), "H2D video");
-  cuda_ok2(cudaMalloc(&da.p, std::size_t(px) * 4), "cudaMalloc plane");
-  cuda_ok2(cudaMalloc(&db.p, std::size_t(px) * 4), "cudaMalloc plane");
-  const void* cur = dvid.p;
-  int cur_type = in_type, cur_ch = v.channels;
-  float* bufs[2] = {static_cast<float*>(da.p), static_cast<float*>(db.p)};
-  int which = 0;
-  const fc_dims d{v.width, v.height, v.frames};
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  auto check = [](int rc, const char* what) {
-    if (rc != 0)
-      throw Error(ErrorKind::Internal, std::string(what) + ": " + fc_error_string(rc));
-  };
-  for (const PlanGroup& g : fp.groups) {
-    if (g.global_aggregation) continue;
-    std::vector<fc_stage> st;
-    for (int id = g.first; id <= g.last; ++id)
-      st.push_back(make_stage(p.kernels[std::size_t(id - 1)]));
-    if (!g.tiled) {
-      for (const fc_stage& s : st) {
-        float* out = bufs[which];
-        if (cur_type == FC_U8 && s.op != FC_RGBA2GRAY) {  // widen a 1-channel u8 input
-          fc_stage conv{};
-          conv.op = FC_IDENTITY;
-          check(fc_stage_spatial(&conv, cur, FC_U8, out, FC_F32, d, nullptr), "u8 widen");
-          cur = out;
-          cur_type = FC_F32;
-          which ^= 1;
-          out = bufs[which];
-        }
-        if (s.op == FC_IIR_TEMPORAL)
-          check(fc_stage_iir(&s, static_cast<const float*>(cur), out, d, 0, nullptr, nullptr,
-                             nullptr),
-                "iir");
-        else
-          check(fc_stage_spatial(&s, cur, cur_type, out, FC_F32, d, nullptr), "stage");
-        cur = out;
-        cur_type = FC_F32;
-        cur_ch = 1;
-        which ^= 1;
-      }
-      continue;
-    }
-    const int halo[6] = {g.halo.x_lo, g.halo.x_hi, g.halo.y_lo, g.halo.y_hi, g.halo.t_lo,
-                         g.halo.t_hi};
-    const int ctas = sms * 4;
-    const long long need = fc_tiled_scratch_bytes(g.tile.x, g.tile.y, g.tile.t, halo, cur_ch, ctas);
-    if (dscr.p) cudaFree(dscr.p);
-    dscr.p = nullptr;
-    cuda_ok2(cudaMalloc(&dscr.p, std::size_t(need)), "cudaMalloc box scratch");
-    if (dst.p) cudaFree(dst.p);
-    dst.p = nullptr;
-    cuda_ok2(cudaMalloc(&dst.p, st.size() * sizeof(fc_stage)), "cudaMalloc stages");
-    cuda_ok2(cudaMemcpy(dst.p, st.data(), st.size() * sizeof(fc_stage), cudaMemcpyHostToDevice),
-             "H2D stages");
-    float* out = bufs[which];
-    check(fc_tiled_group(static_cast<const fc_stage*>(dst.p), int(st.size()), cur, cur_type,
-                         cur_ch, out, d, g.tile.x, g.tile.y, g.tile.t, halo,
-                         static_cast<float*>(dscr.p), ctas, nullptr),
-          "tiled group");
-    cur = out;
-    cur_type = FC_F32;
-    cur_ch = 1;
-    which ^= 1;
-  }
-  std::vector<float> host(static_cast<std::size_t>(px));
-  if (cur_type == FC_U8) {  // no executable stage consumed the video
-    std::vector<std::uint8_t> tmp(static_cast<std::size_t>(px));
-    cuda_ok2(cudaMemcpy(tmp.data(), cur, tmp.size(), cudaMemcpyDeviceToHost), "D2H");
-    std::transform(tmp.begin(), tmp.end(), host.begin(), [](std::uint8_t x) { return float(x); });
-  } else {
-    cuda_ok2(cudaMemcpy(host.data(), cur, host.size() * 4, cudaMemcpyDeviceToHost), "D2H");
-  }
-  return host;
-}
-
 std::string utc_now() {
   std::time_t now = std::time(nullptr);
   std::tm tm{};
@@ -436,6 +230,34 @@ std::string utc_now() {
 }
 
 }  // namespace
+
+namespace fuseplan {
+// Helpers shared with the sharded executor's C ABI (shard.cpp).
+fp_status capi_guarded(const std::function<void()>& fn) { return guarded(fn); }
+const Pipeline& capi_pipeline(const fp_pipeline* p) { return p->p; }
+const FusionPlan& capi_plan(const fp_plan* p) { return p->plan; }
+char* capi_dup(const std::string& s) { return dup(s); }
+// fp_exec_create's options: {"variant": "auto"|"exact"|"fast",
+// "host_chunk_frames": N} (+ "warmup_frames": W for the sharded executor)
+ExecOptions capi_exec_options(const char* options_json, int* warmup_frames) {
+  ExecOptions o;
+  if (!options_json || !*options_json) return o;
+  ordered_json j;
+  try {
+    j = ordered_json::parse(options_json);
+  } catch (const ordered_json::exception& e) {
+    throw Error(ErrorKind::Input, std::string("exec options: bad JSON: ") + e.what());
+  }
+  std::string v = j.value("variant", std::string("auto"));
+  if (v == "auto") o.variant = Variant::Auto;
+  else if (v == "exact") o.variant = Variant::Exact;
+  else if (v == "fast") o.variant = Variant::Fast;
+  else throw Error(ErrorKind::Input, "unknown variant: " + v);
+  o.host_chunk_frames = j.value("host_chunk_frames", 0);
+  if (warmup_frames) *warmup_frames = j.value("warmup_frames", *warmup_frames);
+  return o;
+}
+}  // namespace fuseplan
 
 extern "C" {
 
@@ -682,15 +504,28 @@ fp_status fp_simulate(const fp_pipeline* p, const fp_device* d, const char* opti
       }
     };
     run_to_float(seq, a);
-    const DiffGrid dg = diff_grid(p->p, executed);
-    const bool erodes = tiling_erodes(p->p, executed, dg);
+    const bool erodes = tiling_erodes(executed, p->p);
     if (erodes) {
-      b = run_tiled_on_device(p->p, executed, video);
+      device_run_tiled(p->p, executed, video.data(), in_type, b.data());
     } else {
       Executor fused(p->p, executed, 0, {});
       run_to_float(fused, b);
     }
-    const Diff df = compare_outputs(a, b, pv, dg);
+    TileShape grid;
+    bool have_grid = false;
+    const Halo erode = tiling_erosion(executed, p->p, &grid, &have_grid);
+    VideoDims od = pv;
+    od.channels = 1;
+    VideoData va, vb;
+    va.dims = vb.dims = od;
+    va.data = std::move(a);
+    vb.data = std::move(b);
+    const DiffReport dr = compare_outputs(va, vb, erode, have_grid ? &grid : nullptr);
+    b = std::move(vb.data);  // the tiled arm's mask feeds the tracking stage
+    struct {
+      float max_abs;
+      std::int64_t count, interior, boundary;
+    } df{dr.max_abs_diff, dr.diff_count, dr.interior_diffs, dr.boundary_diffs};
     int executed_kernels = 0;
     for (const KernelDesc& k : p->p.kernels)
       executed_kernels += k.scope != KernelScope::GlobalAggregation;
@@ -699,7 +534,9 @@ fp_status fp_simulate(const fp_pipeline* p, const fp_device* d, const char* opti
                         TileShape{pv.width, pv.height, pv.frames});
     std::int64_t analytic_fused = 0;
     for (const PlanGroup& g : executed.groups) analytic_fused += g.transfer_exact;
-    const Tallies tl = traffic_tallies(p->p, executed);
+    struct {
+      std::int64_t serial, tiled;
+    } tl{sequential_traffic(p->p).gmem_total(), tiled_traffic(executed, p->p).gmem_total()};
     double reduction =
         tl.serial > 0 ? 100.0 * (1.0 - double(tl.tiled) / double(tl.serial)) : 0.0;
 
@@ -841,22 +678,20 @@ fp_status fp_exec_create(const fp_pipeline* p, const fp_plan* fp, int device,
                          const char* options_json, fp_exec** out) {
   return guarded([&] {
     need(p && fp && out);
-    ExecOptions o;
-    if (options_json && *options_json) {
-      ordered_json j;
-      try {
-        j = ordered_json::parse(options_json);
-      } catch (const ordered_json::exception& e) {
-        throw Error(ErrorKind::Input, std::string("exec options: bad JSON: ") + e.what());
-      }
-      std::string v = j.value("variant", std::string("auto"));
-      if (v == "auto") o.variant = Variant::Auto;
-      else if (v == "exact") o.variant = Variant::Exact;
-      else if (v == "fast") o.variant = Variant::Fast;
-      else throw Error(ErrorKind::Input, "unknown variant: " + v);
-      o.host_chunk_frames = j.value("host_chunk_frames", 0);
-    }
+    ExecOptions o = fuseplan::capi_exec_options(options_json, nullptr);
     *out = new fp_exec{std::make_unique<Executor>(p->p, fp->plan, device, o)};
+  });
+}
+
+fp_status fp_exec_converge(fp_exec* e, const void* video, int in_type, int n_frames,
+                           const float* s_true, const float* s_warm, int* frames_out,
+                           void* stream) {
+  return guarded([&] {
+    need(e && video && s_true && s_warm && frames_out);
+    require(in_type == FP_ELEM_U8 || in_type == FP_ELEM_F32, ErrorKind::Input,
+            "in_type must be FP_ELEM_U8 or FP_ELEM_F32");
+    require(n_frames >= 0, ErrorKind::Input, "n_frames < 0");
+    *frames_out = e->ex->converge(video, in_type, n_frames, s_true, s_warm, stream);
   });
 }
 

@@ -194,7 +194,42 @@ Executor::Executor(const Pipeline& p, const FusionPlan& fp, int device,
   groups_.back().out_type = out_type_;
 }
 
+int Executor::converge(const void* video, int in_type, int n_frames, const float* s_true,
+                       const float* s_warm, void* stream) {
+  require(s_true && s_warm && video, ErrorKind::Input, "converge: null pointer");
+  // the stages before the IIR: none (gray video) or one rgba2gray
+  std::vector<const fc_stage*> pre;
+  const fc_stage* iir = nullptr;
+  for (const auto& g : groups_) {
+    for (const auto& s : g.stages) {
+      if (s.op == FC_IIR_TEMPORAL) {
+        iir = &s;
+        break;
+      }
+      pre.push_back(&s);
+    }
+    if (iir) break;
+  }
+  require(iir != nullptr && n_iir_ == 1, ErrorKind::Input,
+          "converge: the chain needs exactly one IIR stage");
+  const bool gray_in = pre.empty();
+  require(gray_in ? dims_.channels == 1 : (pre.size() == 1 && pre[0]->op == FC_RGBA2GRAY),
+          ErrorKind::Input, "converge: only [rgba2gray,] iir_temporal may open the chain");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream ? stream : own_stream_);
+  if (!k_dev_) cuda_check(cudaMalloc(&k_dev_, sizeof(int)), "cudaMalloc(k)");
+  cuda_check(fc_iir_converge(gray_in ? nullptr : pre[0], iir, video, in_type, gray_in,
+                             fc_dims{dims_.width, dims_.height, n_frames}, s_true, s_warm,
+                             k_dev_, st),
+             "carry convergence");
+  int k = 0;
+  cuda_check(cudaMemcpyAsync(&k, k_dev_, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H k");
+  cuda_check(cudaStreamSynchronize(st), "converge sync");
+  return k;
+}
+
 Executor::~Executor() {
+  if (k_dev_) cudaFree(k_dev_);
   if (scratch_) cudaFree(scratch_);
   if (stage_) cudaFree(stage_);
   if (s_in_) cudaStreamDestroy(static_cast<cudaStream_t>(s_in_));

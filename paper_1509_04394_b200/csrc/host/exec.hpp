@@ -15,7 +15,7 @@
 #include <vector>
 
 #include "../kernels/fc_kernels.h"
-#include "fuseplan.hpp"
+#include "../../../include/fuseplan/fuseplan.hpp"
 
 namespace fuseplan {
 
@@ -70,6 +70,14 @@ class Executor {
   // video never has to fit in host memory.  Synchronous.
   void run_file(const std::string& in_path, const std::string& out_path);
 
+  // T-shard carry check: video holds the shard's n_frames frames (device);
+  // s_true / s_warm: the true carry and the warm state the shard started
+  // from.  Returns how many leading frames of the shard differ (0 = none,
+  // n_frames = the end state differs too); synchronous.  Needs a chain whose
+  // IIR is its first stage or follows a single rgba2gray (else Input error).
+  int converge(const void* video, int in_type, int n_frames, const float* s_true,
+               const float* s_warm, void* stream);
+
   std::string describe() const;  // JSON: launch groups and kernels
   std::int64_t launches_per_run() const;
 
@@ -92,6 +100,7 @@ class Executor {
   std::size_t stage_bytes_ = 0;
   void* s_in_ = nullptr;
   void* s_out_ = nullptr;
+  int* k_dev_ = nullptr;  // converge() result slot
 };
 
 // fc_stage for one kernel descriptor, parameters converted as the

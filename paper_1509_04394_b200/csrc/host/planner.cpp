@@ -19,7 +19,7 @@
 #include <limits>
 #include <sstream>
 
-#include "fuseplan.hpp"
+#include "../../../include/fuseplan/fuseplan.hpp"
 #include "json.hpp"
 
 namespace fuseplan {

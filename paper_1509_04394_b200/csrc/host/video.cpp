@@ -91,6 +91,49 @@ void write_fpvd_file(const std::string& path, const HostVideo& v) {
   out.write(s.data(), std::streamsize(s.size()));
 }
 
+// The C++ API's float volume through the same codec: u8 payloads store
+// uint8_t(clamp(v, 0, 255)) (video.cpp:57, truncation), f32 payloads the floats.
+std::string encode_video(const VideoData& video) {
+  HostVideo h;
+  h.dims = video.dims;
+  h.elem = video.elem_type;
+  if (h.elem == ElemType::U8) {
+    h.u8.resize(video.data.size());
+    std::transform(video.data.begin(), video.data.end(), h.u8.begin(), [](float f) {
+      return std::uint8_t(std::clamp(f, 0.0f, 255.0f));
+    });
+  } else {
+    h.f32 = video.data;
+  }
+  return encode_fpvd(h);
+}
+
+VideoData decode_video(const std::string& bytes) {
+  HostVideo h = decode_fpvd(bytes);
+  VideoData v;
+  v.dims = h.dims;
+  v.elem_type = h.elem;
+  if (h.elem == ElemType::U8)
+    v.data.assign(h.u8.begin(), h.u8.end());  // float(u8), video.cpp:87
+  else
+    v.data = std::move(h.f32);
+  return v;
+}
+
+void write_video_file(const std::string& path, const VideoData& video) {
+  std::ofstream out(path, std::ios::binary);
+  require(out.good(), ErrorKind::Input, "cannot write video file: " + path);
+  const std::string s = encode_video(video);
+  out.write(s.data(), std::streamsize(s.size()));
+}
+
+VideoData read_video_file(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  require(in.good(), ErrorKind::Input, "cannot read video file: " + path);
+  std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  return decode_video(bytes);
+}
+
 SyntheticSceneSpec parse_synth_spec(const std::string& text) {
   nlohmann::ordered_json j;
   try {

@@ -7,11 +7,10 @@
 #include <string>
 #include <vector>
 
-#include "fuseplan.hpp"
+#include "../../../include/fuseplan/fuseplan.hpp"
+#include "../../../include/fuseplan/video.hpp"
 
 namespace fuseplan {
-
-enum class ElemType : std::uint32_t { U8 = 0, F32 = 1 };
 
 // A planar [t][c][y][x] volume.  u8 files keep their bytes; f32 files keep
 // floats.  (The reference holds everything as float; the device path reads

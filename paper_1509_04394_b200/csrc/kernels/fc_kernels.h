@@ -113,6 +113,15 @@ int fc_tiled_group(const fc_stage* dev_stages, int n_stages, const void* in, int
                    int in_ch, float* out, fc_dims d, int tile_x, int tile_y, int tile_t,
                    const int* halo, float* scratch, int ctas, void* stream);
 
+/* T-shard carry check (fc_shard.cu): for the pixels whose true and warm
+ * start states differ, runs gray (unless gray_in) + IIR from both over the
+ * shard's d.frames frames and stores in *k_dev (device int) the number of
+ * leading frames in which some pixel's IIR still differs (0: states equal;
+ * d.frames: some pixel never converged).  Asynchronous. */
+int fc_iir_converge(const fc_stage* sgray, const fc_stage* si, const void* video, int in_type,
+                    int gray_in, fc_dims d, const float* s_true, const float* s_warm,
+                    int* k_dev, void* stream);
+
 /* Deterministic counter-hash u8 video (splitmix64 finaliser of
  * index + seed * 0x9E3779B97F4A7C15, top byte), [t][c][y][x]; frames
  * [t0, t0 + d.frames).  Mirrors tests/golden/make_golden.py:hash_video. */

@@ -98,6 +98,11 @@ def lib() -> ctypes.CDLL:
         "fp_exec_describe": ([P, PP], I),
         "fp_exec_run_file": ([P, S, S], I),
         "fp_synth_hash_u8": ([P, I, I, I, I, I, ctypes.c_uint64, P], I),
+        "fp_exec_converge": ([P, P, I, I, P, P, ctypes.POINTER(ctypes.c_int), P], I),
+        "fp_shard_exec_create": ([P, P, ctypes.POINTER(ctypes.c_int), I, S, PP], I),
+        "fp_shard_exec_free": ([P], V),
+        "fp_shard_exec_run": ([P, P, I, P], I),
+        "fp_shard_exec_stats": ([P, PP], I),
         "fp_track_features": ([P, I, I, I, I, I, ctypes.POINTER(ctypes.c_int), I, S,
                                ctypes.POINTER(ctypes.c_double), PP, P], I),
     }
@@ -370,6 +375,21 @@ class Executor(_Handle):
                                  out.ctypes.data, FP_EXEC_HOST_PTRS, None))
         return out
 
+    def converge(self, video, s_true, s_warm, stream=None) -> int:
+        """fp_exec_converge: how many leading frames of a shard (CUDA video
+        [n, C, H, W]) that ran from s_warm differ from a run from s_true."""
+        torch = _torch()
+        for st, name in ((s_true, "s_true"), (s_warm, "s_warm")):
+            self._check_state(st, name, video.device)
+        k = ctypes.c_int()
+        stream = _stream_handle(torch.cuda.current_stream(video.device)
+                                if stream is None else stream)
+        video = video.contiguous()
+        _check(lib().fp_exec_converge(self.ptr, video.data_ptr(), self._elem(video.dtype),
+                                      int(video.shape[0]), s_true.data_ptr(),
+                                      s_warm.data_ptr(), ctypes.byref(k), stream))
+        return k.value
+
     def run_file(self, in_path: str, out_path: str) -> None:
         """FPVD file in -> FPVD file out, streamed through the GPU in chunks
         (fp_exec_run_file); the video never has to fit in host memory."""
@@ -407,6 +427,43 @@ class Executor(_Handle):
             n_warm, None if state_in is None else state_in.data_ptr(),
             None if state_out is None else state_out.data_ptr(), stream))
         return out
+
+
+class ShardedExecutor(_Handle):
+    """fp_shard_exec: one process drives several GPUs; the video is split along
+    T, each shard's IIR restarts `warmup_frames` early, carries move device to
+    device and a wrong warm start is repaired by re-running only the frames it
+    reaches (exact for any warm-up).  Host numpy buffers in and out."""
+    _free = "fp_shard_exec_free"
+
+    def __init__(self, pipeline: Pipeline, plan: Plan, devices, variant: str = "auto",
+                 warmup_frames: int = 48):
+        out = ctypes.c_void_p()
+        devs = (ctypes.c_int * len(devices))(*devices)
+        opts = json.dumps({"variant": variant, "warmup_frames": warmup_frames})
+        _check(lib().fp_shard_exec_create(pipeline.ptr, plan.ptr, devs, len(devices),
+                                          opts.encode(), ctypes.byref(out)))
+        super().__init__(out)
+        self.pipeline = pipeline
+        self._one = Executor(pipeline, plan, device=devices[0], variant=variant)
+
+    def run(self, video, out=None):
+        W, H, F, C = self.pipeline.dims
+        arr = np.ascontiguousarray(video)
+        if arr.shape != (F, C, H, W):
+            raise InputError(f"video shape {arr.shape} != {(F, C, H, W)}")
+        if out is None:
+            out = np.empty((F, H, W), self._one.out_dtype)
+        else:
+            self._one._check_out(out, (F, H, W), False)
+        _check(lib().fp_shard_exec_run(self.ptr, arr.ctypes.data, self._one._elem(arr.dtype),
+                                       out.ctypes.data))
+        return out
+
+    def stats(self) -> dict:
+        out = ctypes.c_void_p()
+        _check(lib().fp_shard_exec_stats(self.ptr, ctypes.byref(out)))
+        return json.loads(_take_string(out))
 
 
 def synth_hash_u8(out, t0: int = 0, seed: int = 1234, stream=None):

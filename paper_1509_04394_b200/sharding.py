@@ -14,13 +14,19 @@ earlier frame, so each rank
   4. if every warm state was right (k = world), every shard started from the
      exact state by induction (rank g's end state is exact when its start
      state was) -- done.  Otherwise ranks >= k walk the carry in order from
-     k: each re-runs its shard from the true state (the fix-up) and forwards
-     its corrected end state.
+     k: each repairs its shard from the true state (the fix-up) and forwards
+     its end state.  The repair is sparse in time: `converge(s_true,
+     s_warm)` (fp_exec_converge) re-runs gray+IIR for only the pixels whose
+     two states differ and returns how many leading frames of the shard they
+     reach; the IIR is deterministic, so once both trajectories coincide at a
+     pixel they stay equal, and only those frames are recomputed -- the end
+     state changes (and the walk goes on) only when they reach the shard's
+     end.
 
 So the common case costs one exchange and one all-reduce whatever the rank
 count, and the result is identical to a single-device run whatever W is;
-W only decides how often the fix-up chain runs (W >= 48 gave no
-mismatch on 800x600 data).
+W only decides how often the fix-up chain runs and how long it is
+(W >= 48 gave no mismatch on 800x600 data).
 
 `run_shard` is the compute: (frames, n_warm, state_in) -> (output, state_out)
 on this rank.  In production it is the sm_100a executor (fp_exec_run_range
@@ -41,7 +47,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Callable, Optional, Tuple
 
-WARMUP_FRAMES = 64
+WARMUP_FRAMES = 48  # 48 frames -> 0 / 480 000 mismatching pixels
 
 
 @dataclass
@@ -82,7 +88,8 @@ def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callabl
                 equal: Callable, stats: Optional[dict] = None,
                 first_bad: Optional[Callable] = None,
                 warm_state: Optional[Callable] = None,
-                advance: Optional[Callable] = None) -> Tuple[object, object]:
+                advance: Optional[Callable] = None,
+                converge: Optional[Callable] = None) -> Tuple[object, object]:
     """Executes this rank's part of the protocol and returns (output, end_state).
 
     run_shard(first, n_frames, n_warm, state_in) -> (out, state_out): run
@@ -100,6 +107,9 @@ def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callabl
         reference's, so the two warm states are identical.
     advance(first, n, state_in) -> state: gray+IIR state after n frames from
         state_in (None = fresh); required when shard.t_halo > 0.
+    converge(s_true, s_warm) -> k: leading frames of this shard whose output
+        a start from s_warm instead of s_true changes (fp_exec_converge); the
+        fix-up then re-runs only those frames.  None: whole-shard re-runs.
     """
     if shard.t_halo:
         return _run_sharded_halo(shard, run_shard, send, recv, equal, stats, first_bad,
@@ -115,8 +125,23 @@ def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callabl
         s_warm = None
         out, s_end = run_shard(shard.lo, n_local, 0, None)
     fixups = 0
+    fixed = [0]
     world, rank = shard.world, shard.rank
     start = 0  # first rank of the sequential fix-up chain
+
+    def repair(s_true, out, s_end):
+        # frames of this shard a start from s_warm (not s_true) got wrong
+        k = n_local
+        if converge is not None and s_warm is not None:
+            k = min(int(converge(s_true, s_warm)), n_local)
+        fixed[0] += k
+        if k >= n_local:  # the whole shard, end state included
+            return run_shard(shard.lo, n_local, 0, s_true)
+        if k > 0:
+            part, _ = run_shard(shard.lo, k, 0, s_true)
+            if part is not None and out is not None:
+                out[:k] = part
+        return out, s_end
     if first_bad is not None and world > 1:
         # 3: every rank forwards its (tentative) end state at once; even /
         # odd ordering of send and recv keeps blocking point-to-point
@@ -138,7 +163,7 @@ def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callabl
                 stats["fixups"] = stats.get("fixups", 0)
             return out, s_end
         if rank == start:  # its received state is exact (all ranks < start verified)
-            out, s_end = run_shard(shard.lo, n_local, 0, s_true)
+            out, s_end = repair(s_true, out, s_end)
             fixups += 1
     # carry chain from `start`: rank r's end state is final once r verified
     for r in range(start, world - 1):
@@ -147,10 +172,11 @@ def run_sharded(shard: Shard, run_shard: Callable, send: Callable, recv: Callabl
         elif rank == r + 1:
             s_true = recv(r)
             if s_warm is None or not equal(s_true, s_warm):
-                out, s_end = run_shard(shard.lo, n_local, 0, s_true)
+                out, s_end = repair(s_true, out, s_end)
                 fixups += 1
     if stats is not None:
         stats["fixups"] = stats.get("fixups", 0) + fixups
+        stats["fixed_frames"] = stats.get("fixed_frames", 0) + fixed[0]
     return out, s_end
 
 

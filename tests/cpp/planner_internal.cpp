@@ -8,7 +8,7 @@
 #include <limits>
 #include <random>
 
-#include "fuseplan.hpp"
+#include "fuseplan/fuseplan.hpp"
 
 using namespace fuseplan;
 

@@ -11,6 +11,7 @@ def test_planner_internals(tmp_path):
     exe = tmp_path / "planner_internal"
     host = os.path.join(B.CSRC, "host")
     cmd = [B.CXX, "-std=c++20", "-O1", "-ffp-contract=off", f"-I{host}",
+           f"-I{os.path.join(ROOT, 'include')}",
            f"-I{B.JSON_DIR}", os.path.join(ROOT, "tests", "cpp", "planner_internal.cpp"),
            os.path.join(host, "model.cpp"), os.path.join(host, "planner.cpp"),
            "-o", str(exe)]

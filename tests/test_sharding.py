@@ -21,7 +21,30 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, frames, warmup, result_path, parallel=False, single=False):
+def _np_converge(video, lo, hi, s_true, s_warm):
+    """fp_exec_converge restated in numpy (reference float32 order,
+    simulator.cpp:51-62): leading frames of [lo, hi) whose IIR differs."""
+    a, b = s_true.reshape(-1), s_warm.reshape(-1)
+    idx = np.nonzero(a.view(np.uint32) != b.view(np.uint32))[0]
+    if idx.size == 0:
+        return 0
+    a, b = a[idx].copy(), b[idx].copy()
+    alpha = np.float32(0.5)
+    beta = np.float32(1.0) - alpha
+    wr, wg, wb = np.float32(0.299), np.float32(0.587), np.float32(0.114)
+    first = np.full(idx.size, hi - lo)
+    for t in range(hi - lo):
+        f = video[lo + t].reshape(4, -1)[:, idx].astype(np.float32)
+        x = (wr * f[0] + wg * f[1]) + wb * f[2]
+        a = alpha * x + beta * a
+        b = alpha * x + beta * b
+        eq = (a.view(np.uint32) == b.view(np.uint32)) & (first == hi - lo)
+        first[eq] = t
+    return int(first.max())
+
+
+def _worker(rank, world, port, frames, warmup, result_path, parallel=False, single=False,
+            sparse=False):
     import sys
     sys.path.insert(0, ROOT)
     from oracle import oracle as O
@@ -60,11 +83,17 @@ def _worker(rank, world, port, frames, warmup, result_path, parallel=False, sing
                             nthreads=1)
         return st
 
+    def converge(s_true, s_warm):
+        return _np_converge(video, sh.lo, sh.hi, s_true, s_warm)
+
     stats = {}
     out, _ = run_sharded(sh, run_shard, send, recv,
                          lambda a, b: np.array_equal(a.view(np.uint32), b.view(np.uint32)),
                          stats, first_bad if parallel else None,
-                         warm_state if single else None)
+                         warm_state if single else None,
+                         converge=converge if sparse else None)
+    if sparse and stats.get("fixups"):
+        assert stats["fixed_frames"] <= stats["fixups"] * (sh.hi - sh.lo)
     # gather to rank 0
     full = [None] * world if rank == 0 else None
     dist.gather_object((sh.lo, out, stats["fixups"] if stats else 0), full, dst=0)
@@ -77,16 +106,21 @@ def _worker(rank, world, port, frames, warmup, result_path, parallel=False, sing
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("parallel,single", [(False, False), (True, False), (True, True)])
+@pytest.mark.parametrize("parallel,single,sparse", [(False, False, False), (True, False, False),
+                                                    (True, True, False), (True, True, True),
+                                                    (False, False, True)])
 @pytest.mark.parametrize("world,frames,warmup,expect_fixups",
                          [(2, 40, 64, False), (2, 40, 3, True), (3, 45, 2, True),
                           (3, 45, 48, None), (4, 48, 1, True), (4, 48, 30, None)])
-def test_sharded_run_is_exact(tmp_path, world, frames, warmup, expect_fixups, parallel, single):
+def test_sharded_run_is_exact(tmp_path, world, frames, warmup, expect_fixups, parallel, single,
+                              sparse):
     """Sequential carry chain, the parallel verification (one exchange + one
-    all-reduce, chain only from the first failing rank), and the single-launch
-    shard (warm-up inside, warm state from a gray+IIR side pass)."""
+    all-reduce, chain only from the first failing rank), the single-launch
+    shard (warm-up inside, warm state from a gray+IIR side pass), and the
+    time-sparse repair (only the frames a wrong warm start reaches)."""
     out = tmp_path / "r.npy"
-    mp.spawn(_worker, args=(world, _free_port(), frames, warmup, str(out), parallel, single),
+    mp.spawn(_worker, args=(world, _free_port(), frames, warmup, str(out), parallel, single,
+                            sparse),
              nprocs=world, join=True)
     ok, fixups = np.load(out)
     assert ok == 1
@@ -101,7 +135,7 @@ def test_shard_bounds():
     shards = [shard_of(r, 8, 1000) for r in range(8)]
     assert shards[0].lo == 0 and shards[-1].hi == 1000
     assert all(a.hi == b.lo for a, b in zip(shards, shards[1:]))
-    assert shards[0].warm == 0 and all(s.warm == 64 for s in shards[1:])
+    assert shards[0].warm == 0 and all(s.warm == 48 for s in shards[1:])
 
 
 def _halo_worker(rank, world, port, frames, warmup, t_radii, result_path, parallel):
