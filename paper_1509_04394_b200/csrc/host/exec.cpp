@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <memory>
 #include <cmath>
@@ -229,6 +230,7 @@ int Executor::converge(const void* video, int in_type, int n_frames, const float
 }
 
 Executor::~Executor() {
+  if (pitched_) cudaFree(pitched_);
   if (k_dev_) cudaFree(k_dev_);
   if (scratch_) cudaFree(scratch_);
   if (stage_) cudaFree(stage_);
@@ -257,6 +259,7 @@ std::string Executor::describe() const {
   ss << "{\"device\": " << device_ << ", \"variant\": " << int(opt_.variant)
      << ", \"output\": \"" << (out_type_ == FC_U8 ? "u8" : "f32")
      << "\", \"launches_per_run\": " << launches_per_run()
+     << ", \"last_chain_kernel\": \"" << last_chain_ << "\""
      << ", \"exact_rechecks_total\": " << fc_last_recheck_count() << ", \"groups\": [";
   for (std::size_t i = 0; i < groups_.size(); ++i) {
     const auto& g = groups_[i];
@@ -346,12 +349,49 @@ void Executor::run_device(const void* video, int in_type, void* out, int n_frame
         const fc_stage* s = g.stages.data();
         const fc_stage* sgray = gray_in ? nullptr : s;
         const fc_stage* rest = gray_in ? s : s + 1;
-        cuda_check(fc_fused_chain(sgray, &rest[0], &rest[1], &rest[2], &rest[3], cur,
-                                  cur_type, gray_in, dst, dst_type, d, warm,
-                                  state_ptr(state_in),
-                                  const_cast<float*>(state_ptr(state_out)),
-                                  int(opt_.variant), st),
+        // the frame pipeline's TMA map needs a 16-byte row pitch and base:
+        // other widths / bases get planes 0-2 copied into a pitched buffer
+        // (one 3-D copy) instead of dropping to the FP64 kernel
+        const void* pitched = nullptr;
+        int vpitch = 0;
+        void* pitched_out = nullptr;
+        const int P = (dims_.width + 15) / 16 * 16;
+        const bool misaligned = (reinterpret_cast<std::uintptr_t>(cur) & 15) != 0;
+        const bool out_misaligned =
+            dims_.width % 4 != 0 || (reinterpret_cast<std::uintptr_t>(dst) & 3) != 0;
+        if (opt_.variant != Variant::Exact && cur_type == FC_U8 && !gray_in &&
+            dims_.channels == 4 && (dims_.width % 16 != 0 || misaligned || out_misaligned) &&
+            fc_chain_pipe_applies(sgray, &rest[0], &rest[1], &rest[3], cur_type, gray_in,
+                                  dst_type, d, P)) {
+          const std::size_t vbytes = std::size_t(frames) * 4 * dims_.height * P;
+          const std::size_t obytes =
+              out_misaligned ? std::size_t(frames - warm) * dims_.height * P : 0;
+          const std::size_t need = vbytes + obytes;
+          if (need > pitched_bytes_) {
+            if (pitched_) cuda_check(cudaFree(pitched_), "cudaFree");
+            pitched_ = nullptr;
+            cuda_check(cudaMalloc(&pitched_, need), "cudaMalloc(pitched video)");
+            pitched_bytes_ = need;
+          }
+          if (out_misaligned) pitched_out = static_cast<char*>(pitched_) + vbytes;
+          cudaMemcpy3DParms cp = {};
+          cp.srcPtr = make_cudaPitchedPtr(const_cast<void*>(cur), dims_.width, dims_.width,
+                                          4 * dims_.height);
+          cp.dstPtr = make_cudaPitchedPtr(pitched_, P, dims_.width, 4 * dims_.height);
+          cp.extent = make_cudaExtent(dims_.width, 3 * dims_.height, frames);
+          cp.kind = cudaMemcpyDeviceToDevice;
+          cuda_check(cudaMemcpy3DAsync(&cp, st), "pitched copy");
+          pitched = pitched_;
+          vpitch = P;
+        }
+        cuda_check(fc_fused_chain_pitched(sgray, &rest[0], &rest[1], &rest[2], &rest[3], cur,
+                                          pitched, vpitch, pitched_out, P, cur_type, gray_in,
+                                          dst, dst_type, d, warm, state_ptr(state_in),
+                                          const_cast<float*>(state_ptr(state_out)),
+                                          int(opt_.variant), st),
                    "F12345 launch");
+        last_chain_ = fc_last_chain_kernel();
+        if (pitched) last_chain_ += " on a pitched copy";
         frames -= warm;
         warm = 0;
         ++iir_idx;

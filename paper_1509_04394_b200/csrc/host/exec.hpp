@@ -101,6 +101,11 @@ class Executor {
   void* s_in_ = nullptr;
   void* s_out_ = nullptr;
   int* k_dev_ = nullptr;  // converge() result slot
+  // pitched copy of planes 0-2 for the frame pipeline when the width is not a
+  // multiple of 16 or the video base is not 16-byte aligned (TMA strides)
+  void* pitched_ = nullptr;
+  std::size_t pitched_bytes_ = 0;
+  std::string last_chain_ = "none";
 };
 
 // fc_stage for one kernel descriptor, parameters converted as the

@@ -242,8 +242,8 @@ double kparam(const KernelDesc& k, const char* key, double dflt) {
 
 // The launch group the executor (exec.cpp) builds for this interval, and for
 // the fused classes whether the certified FP32 kernel applies (fc_common.cuh
-// fast_params / stencil_params: alpha 0.5, gaussian r = 2, a {0, 255} byte
-// mask, th > 0, width a multiple of 16).
+// fast_params / stencil_params: IIR alpha in [0, 1], gaussian r = 2, a
+// {0, 255} byte mask, th > 0).
 std::string streaming_class_of(std::span<const KernelDesc> ks, int first_id,
                                const VideoDims& video) {
   std::vector<std::string> ops;
@@ -258,10 +258,12 @@ std::string streaming_class_of(std::span<const KernelDesc> ks, int first_id,
       ops == V{"rgba2gray", "iir_temporal", "gaussian", "gradient", "threshold"}) {
     const int r = int(kparam(ks[2], "radius", 2));
     if (r >= 1 && r <= 3)
-      return float(kparam(ks[1], "alpha", 0.5)) == 0.5f && certified_tail(ks[2], ks[4]) &&
-                     video.width % 16 == 0
-                 ? "chain"
-                 : "chain_exact";
+    {
+      // the frame pipeline takes any alpha in [0, 1] and any width (a pitched
+      // copy of the video when the width is not a multiple of 16)
+      const float a = float(kparam(ks[1], "alpha", 0.5));
+      return a >= 0.0f && a <= 1.0f && certified_tail(ks[2], ks[4]) ? "chain" : "chain_exact";
+    }
   }
   if (reads_video && ops == V{"rgba2gray", "iir_temporal"}) return "gray_iir";
   if (ops == V{"gaussian", "gradient", "threshold"})

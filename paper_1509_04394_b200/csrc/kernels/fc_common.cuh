@@ -124,7 +124,9 @@ __device__ __forceinline__ uint32_t pack_white(float a, float b, float c, float 
 
 // Parameters of the certified FP32 path, shared by both fast kernels.
 struct FastParams {
-  float wr, wg, wb, wrm, wgm, wbm;  // gray weights x 0.5 (alpha folded), -w*2^23
+  float wr, wg, wb, wrm, wgm, wbm;  // gray weights (x 0.5 when alpha = 0.5), -w*2^23
+  float ia, ib;                     // IIR alpha and float(1 - alpha) (general alpha)
+  int alpha_half;                   // alpha == 0.5: folded into the weights, one FMA
   float h0, h1, h2;                 // separable fast taps: |d|=2, |d|=1, centre
   float taps[25];                   // reference taps for the exact recheck
   float mstar, band, th_val;
@@ -233,18 +235,29 @@ inline bool stencil_params(const fc_stage* sg, const fc_stage* sthr, int out_typ
   return true;
 }
 
+// pitch: bytes between the video's rows (>= width; the TMA map needs it and
+// the base address 16-byte aligned).
 inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
                         const fc_stage* sthr, const void* video, int in_type, int gray_in,
-                        int out_type, fc_dims d, FastParams* p) {
+                        int out_type, fc_dims d, int pitch, FastParams* p) {
   if (in_type != FC_U8 || out_type != FC_U8 || gray_in || sgray == nullptr) return false;
-  if (si->alpha != 0.5f) return false;
-  if (d.width % 16 != 0 || d.height < 1) return false;
+  // any alpha in [0, 1] keeps the IIR a convex combination (the value bound
+  // the certification needs); 0.5 takes the folded one-FMA update
+  if (!(si->alpha >= 0.0f && si->alpha <= 1.0f)) return false;
+  if (sgray->wr < 0.0f || sgray->wg < 0.0f || sgray->wb < 0.0f) return false;
+  // width % 4: every stencil lane owns 4 whole columns (its mask store, the
+  // edge replication of the IIR cells and the Sobel x clamp assume it)
+  if (pitch < d.width || pitch % 16 != 0 || d.width % 4 != 0 || d.height < 1) return false;
   if (reinterpret_cast<uintptr_t>(video) % 16 != 0) return false;
   std::memset(p, 0, sizeof *p);
+  p->alpha_half = si->alpha == 0.5f;
+  p->ia = si->alpha;
+  p->ib = 1.0f - si->alpha;  // host float arithmetic == the reference's
   // alpha = 0.5 folded into the gray weights (exact power-of-two scale)
-  p->wr = sgray->wr * 0.5f;
-  p->wg = sgray->wg * 0.5f;
-  p->wb = sgray->wb * 0.5f;
+  const float fold = p->alpha_half ? 0.5f : 1.0f;
+  p->wr = sgray->wr * fold;
+  p->wg = sgray->wg * fold;
+  p->wb = sgray->wb * fold;
   p->wrm = -p->wr * 8388608.0f;
   p->wgm = -p->wg * 8388608.0f;
   p->wbm = -p->wb * 8388608.0f;
@@ -282,13 +295,15 @@ inline bool plane_tensor_map(CUtensorMap* map, const void* planes, fc_dims d, in
          CUDA_SUCCESS;
 }
 
-// 3-D map over the planar video [4T][H][W] u8 with a box of (bw, rows, 3):
-// one copy brings the R, G, B planes of a haloed window of one frame.
-inline bool rgb_tensor_map(CUtensorMap* map, const void* video, fc_dims d, int bw, int rows) {
+// 3-D map over the planar video [4T][H][pitch] u8 (width W used) with a box
+// of (bw, rows, 3): one copy brings the R, G, B planes of a haloed window of
+// one frame.
+inline bool rgb_tensor_map(CUtensorMap* map, const void* video, fc_dims d, int bw, int rows,
+                           int pitch) {
   auto enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[3] = {cuuint64_t(d.width), cuuint64_t(d.height), cuuint64_t(4) * d.frames};
-  cuuint64_t strides[2] = {cuuint64_t(d.width), cuuint64_t(d.width) * d.height};
+  cuuint64_t strides[2] = {cuuint64_t(pitch), cuuint64_t(pitch) * d.height};
   cuuint32_t box[3] = {cuuint32_t(bw), cuuint32_t(rows), 3};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(video), dims, strides,

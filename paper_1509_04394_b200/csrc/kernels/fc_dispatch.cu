@@ -16,7 +16,11 @@
       float *state_out, void *stream
 
 extern "C" int fc_chain_exact(FC_CHAIN_ARGS);  // fc_exact.cu: FP64 everywhere
-extern "C" int fc_chain_pipe(FC_CHAIN_ARGS);   // fc_pipe.cu: certified, headline
+extern "C" int fc_chain_pipe(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                             const fc_stage* sthr, const void* video, int in_type, int gray_in,
+                             void* out, int out_type, fc_dims d, int n_warm,
+                             const float* state_in, float* state_out, int pitch, int opitch,
+                             void* stream);  // fc_pipe.cu: certified, headline
 extern "C" int fc_f345_pipe(const fc_stage* sg, const fc_stage* sthr, const float* in,
                             void* out, int out_type, fc_dims d, double in_max, void* stream);
 extern "C" long long fc_pipe_recheck_count(void);
@@ -54,23 +58,59 @@ extern "C" void fc_set_knobs(const fc_knobs* k) {
 
 extern "C" const fc_knobs* fc_get_knobs(void) { return &g_knobs; }
 
+namespace {
+thread_local const char* g_last_chain = "none";
+}
+
 // variant: 0 auto (certified frame pipeline when covered, else exact),
 //          1 exact, 2 fast (certified frame pipeline or -1: fail loudly).
+// video_pitch: row pitch of a pitched copy of the video for the frame
+// pipeline (0: the video itself, pitch = width); `video` is always the
+// contiguous video (the exact kernel's input).
+extern "C" int fc_fused_chain_pitched(const fc_stage* sgray, const fc_stage* si,
+                                      const fc_stage* sg, const fc_stage* sgrad,
+                                      const fc_stage* sthr, const void* video,
+                                      const void* pitched, int video_pitch, void* pitched_out,
+                                      int out_pitch, int in_type, int gray_in, void* out,
+                                      int out_type, fc_dims d, int n_warm,
+                                      const float* state_in, float* state_out, int variant,
+                                      void* stream) {
+  (void)sgrad;
+  if (variant == 2 || variant == 0) {
+    const int rc = fc_chain_pipe(sgray, si, sg, sthr, pitched ? pitched : video, in_type, gray_in,
+                                 pitched_out ? pitched_out : out, out_type, d, n_warm, state_in,
+                                 state_out, pitched ? video_pitch : 0,
+                                 pitched_out ? out_pitch : 0, stream);
+    if (rc == 0 && pitched_out)  // the mask rows back to their contiguous layout
+      return int(cudaMemcpy2DAsync(out, size_t(d.width), pitched_out, size_t(out_pitch),
+                                   size_t(d.width), size_t(d.height) * (d.frames - n_warm),
+                                   cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+    if (rc != -1) g_last_chain = "certified FP32 frame pipeline (fc_pipe.cu)";
+    if (rc != -1 || variant == 2) return rc;  // -1: parameters not covered
+  }
+  g_last_chain = "exact FP64 tiles (fc_exact.cu k_chain_exact)";
+  return fc_chain_exact(sgray, si, sg, sthr, video, in_type, gray_in, out,
+                        out_type, d, n_warm, state_in, state_out, stream);
+}
+
 extern "C" int fc_fused_chain(const fc_stage* sgray, const fc_stage* si,
                               const fc_stage* sg, const fc_stage* sgrad,
                               const fc_stage* sthr, const void* video,
                               int in_type, int gray_in, void* out, int out_type,
                               fc_dims d, int n_warm, const float* state_in,
                               float* state_out, int variant, void* stream) {
-  (void)sgrad;
-  if (variant == 2 || variant == 0) {
-    const int rc = fc_chain_pipe(sgray, si, sg, sthr, video, in_type, gray_in, out, out_type,
-                                 d, n_warm, state_in, state_out, stream);
-    if (rc != -1 || variant == 2) return rc;  // -1: parameters not covered
-  }
-  return fc_chain_exact(sgray, si, sg, sthr, video, in_type, gray_in, out,
-                        out_type, d, n_warm, state_in, state_out, stream);
+  return fc_fused_chain_pitched(sgray, si, sg, sgrad, sthr, video, nullptr, 0, nullptr, 0,
+                                in_type, gray_in, out, out_type, d, n_warm, state_in, state_out,
+                                variant, stream);
 }
+
+extern "C" const char* fc_last_chain_kernel(void) { return g_last_chain; }
+
+// Would the certified frame pipeline take this chain with a video of row
+// pitch `pitch` (values only: the pointer alignment is the caller's)?
+extern "C" int fc_chain_pipe_applies(const fc_stage* sgray, const fc_stage* si,
+                                     const fc_stage* sg, const fc_stage* sthr, int in_type,
+                                     int gray_in, int out_type, fc_dims d, int pitch);
 
 extern "C" long long fc_last_recheck_count(void) { return fc_pipe_recheck_count(); }
 

@@ -101,6 +101,25 @@ int fc_fused_chain(const fc_stage* s_gray, const fc_stage* s_iir,
                    const float* state_in, float* state_out, int variant,
                    void* stream);
 
+/* F12345 with optional pitched buffers for the certified frame pipeline (its
+ * TMA map needs a 16-byte row pitch and base; its mask stores 4-byte aligned
+ * rows): `pitched` holds planes 0-2 of every frame at [t][4][H][video_pitch]
+ * (NULL: use `video`); `pitched_out` (NULL: write `out`) receives the mask at
+ * row pitch out_pitch and is copied into `out` afterwards.  `video` / `out`
+ * are the contiguous arrays (the FP64 kernel's). */
+int fc_fused_chain_pitched(const fc_stage* s_gray, const fc_stage* s_iir,
+                           const fc_stage* s_gauss, const fc_stage* s_grad,
+                           const fc_stage* s_thr, const void* video, const void* pitched,
+                           int video_pitch, void* pitched_out, int out_pitch, int in_type,
+                           int gray_in, void* out, int out_type, fc_dims d, int n_warm,
+                           const float* state_in, float* state_out, int variant, void* stream);
+/* Would the certified frame pipeline take this chain with row pitch `pitch`? */
+int fc_chain_pipe_applies(const fc_stage* s_gray, const fc_stage* s_iir,
+                          const fc_stage* s_gauss, const fc_stage* s_thr, int in_type,
+                          int gray_in, int out_type, fc_dims d, int pitch);
+/* The kernel the last fc_fused_chain* call on this thread ran. */
+const char* fc_last_chain_kernel(void);
+
 /* run_tiled's box staging (simulator.cpp:229-333) for one tiled plan group,
  * for fp_simulate's tiled arm when a plan's halo erodes (fc_tiled.cu): one
  * CTA per output box (boxes looped over `ctas` CTAs); dev_stages: the

@@ -134,6 +134,7 @@ struct Args {
   int* seg_k;  // main segmented launch: reset to n_segs by CTA 0 (read by verify / fix-up)
   long long* dbg;  // optional per-CTA timing (FUSEPLAN_PIPE_PROFILE), 8 slots per CTA
   int skip;        // timing experiments only (FUSEPLAN_PIPE_SKIP): 1 IIR math, 2 stencil math
+  int opitch;      // output row pitch in bytes (>= W, a multiple of 4)
   int dbg_x, dbg_y, dbg_t;  // diagnostics (FUSEPLAN_PIPE_DEBUG_PX=x,y,t): dump the
   float* dbg_px;            // recheck's 7x7 IIR neighbourhood + decision
   FastParams p;
@@ -275,7 +276,7 @@ __device__ __forceinline__ float2 shfl_down2(float2 v) {
 
 // ------------------------------------------------------------------ IIR warps
 
-template <int OH, bool BX, bool BY>
+template <int OH, bool BX, bool BY, bool HALF>
 __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw, int lane,
                                          int bx, int by, int xoff, const CUtensorMap* tmap,
                                          int tx0) {
@@ -288,6 +289,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
   const uint32_t k4b = a.p.k4b;
   const float wr = a.p.wr, wg = a.p.wg, wb = a.p.wb;
   const float wrm = a.p.wrm, wgm = a.p.wgm, wbm = a.p.wbm;
+  const float ia = a.p.ia, ib = a.p.ib;
 
   int rowx[NR], rowy[NR];  // RGB slot byte offsets of the two window rows
 #pragma unroll
@@ -398,8 +400,16 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
         __fadd2_rn(wprod(f2(FP_MG(wx[0], J), FP_MG(wy[0], J)), wr, wrm),                    \
                    wprod(f2(FP_MG(wx[1], J), FP_MG(wy[1], J)), wg, wgm)),                   \
         wprod(f2(FP_MG(wx[2], J), FP_MG(wy[2], J)), wb, wbm));                              \
-    /* g = 0.5 gray exactly; IIR y = fl(0.5 x + fl(0.5 y)) == FMA(0.5, y, g) */            \
-    v[r][J] = FIRST ? __fadd2_rn(g, g) : __ffma2_rn(splat(0.5f), v[r][J], g);               \
+    /* HALF: g = 0.5 gray exactly; IIR y = fl(0.5 x + fl(0.5 y)) == FMA(0.5, y, g); */     \
+    /* else g = gray and y = fl(fl(a x) + fl(b y)) (simulator.cpp:57-62) in scalar */      \
+    /* ops: ptxas contracts mul.rn.f32x2 followed by add.rn.f32x2 into FFMA2 despite */       \
+    /* the .rn (measured), which would drop a rounding; scalar .rn ops are kept */            \
+    if (HALF)                                                                               \
+      v[r][J] = FIRST ? __fadd2_rn(g, g) : __ffma2_rn(splat(0.5f), v[r][J], g);             \
+    else                                                                                    \
+      v[r][J] = FIRST ? g                                                                   \
+                      : f2(__fadd_rn(__fmul_rn(ia, g.x), __fmul_rn(ib, v[r][J].x)),         \
+                           __fadd_rn(__fmul_rn(ia, g.y), __fmul_rn(ib, v[r][J].y)));        \
   }
         FP_CELL(0) FP_CELL(1) FP_CELL(2) FP_CELL(3)
 #undef FP_CELL
@@ -614,9 +624,10 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
       wait_phase(bar_iir_full(a, slot), par);
     }
     const unsigned base = smem0 + a.off_iir + slot * a.iir_stride;
-    unsigned char* o = a.out + (long long)(rg.out0 + u) * hw;
-    unsigned char* ox = o + (long long)(by + 3) * W + xl;  // pair-row 3, top half
-    unsigned char* oy = ox + (long long)OH * W;              // bottom half
+    const int OW = a.opitch;  // output rows: opitch bytes apart, frames opitch * H
+    unsigned char* o = a.out + (long long)(rg.out0 + u) * OW * H;
+    unsigned char* ox = o + (long long)(by + 3) * OW + xl;  // pair-row 3, top half
+    unsigned char* oy = ox + (long long)OH * OW;              // bottom half
     int nq = 0;                                              // queued records
     float amin = __int_as_float(0x7f800000);                 // running min |nd|
 
@@ -702,8 +713,8 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
           st_pred_u32(ox, pack_neg(dm[0].x, dm[1].x, dm[2].x, dm[3].x), okx);
           st_pred_u32(oy, pack_neg(dm[0].y, dm[1].y, dm[2].y, dm[3].y), oky);
         }
-        ox += W;  // running row pointers
-        oy += W;
+        ox += OW;  // running row pointers
+        oy += OW;
         // running min of |nd| over the lane's output values (branch-free;
         // checked once per 6-step body; values of rows below the video only
         // cause a harmless extra recheck)
@@ -776,7 +787,7 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
             const int y = by + q + half * OH;
             if (y >= H) continue;
             for (int j = 0; j < LC; ++j)
-              o[(long long)y * W + xl + j] =
+              o[(long long)y * OW + xl + j] =
                   exact_white<OH>(a, sb, taps, bx, by, xl + j, y, half) ? 0xFF : 0x00;
           }
       if (lane == 0) atomicAdd(&g_rechecks, (unsigned long long)(30 * LC * 2 * OH));
@@ -798,7 +809,7 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
         const int y = by + q0 + st + half * OH;
         if (y >= H) continue;
         const bool wv = exact_white<OH>(a, sb, taps, bx, by, x, y, half);
-        o[(long long)y * W + x] = wv ? 0xFF : 0x00;
+        o[(long long)y * OW + x] = wv ? 0xFF : 0x00;
         ++cnt;
         if (a.dbg_px && x == a.dbg_x && y == a.dbg_y && u == a.dbg_t) {
           for (int dy = -3; dy <= 3; ++dy)
@@ -842,7 +853,7 @@ __device__ __forceinline__ long long interior_flag(const Args& a, int bx, int by
 
 // SRC_F32 = false: the SPEC chain from the u8 RGBA video (F12345);
 // SRC_F32 = true:  gaussian + gradient + threshold from f32 planes (F345).
-template <int OH, bool SRC_F32>
+template <int OH, bool SRC_F32, bool HALF>
 __global__ void __launch_bounds__(NTHR, 1)
     k_chain_pipe(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
   constexpr int R = 2 * OH + 6;
@@ -929,13 +940,13 @@ __global__ void __launch_bounds__(NTHR, 1)
   } else if (warp < NS + NIE && !SRC_F32) {
     const int iw = warp - NS, xoff = bx - tx0;
     if (interior_iir)
-      iir_role<OH, false, false>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
+      iir_role<OH, false, false, HALF>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
     else if (FP_SPECIALISE && in_x)
-      iir_role<OH, false, true>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
+      iir_role<OH, false, true, HALF>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
     else if (FP_SPECIALISE && in_y)
-      iir_role<OH, true, false>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
+      iir_role<OH, true, false, HALF>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
     else
-      iir_role<OH, true, true>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
+      iir_role<OH, true, true, HALF>(a, fp_rg, iw, lane, bx, by, xoff, &tmap, tx0);
   } else if (lane == 0) {
     // producer: frame t -> RGB slot t % NSF once the IIR warps released it
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
@@ -992,11 +1003,13 @@ using KernelFn = void (*)(CUtensorMap, Args);
 
 #define FP_OH_LIST(X) X(3) X(4) X(5) X(8) X(10) X(12) X(15)
 
-KernelFn kernel_for(int oh, bool src_f32) {
+// src_f32: F345 (no IIR role; HALF irrelevant, one instantiation)
+KernelFn kernel_for(int oh, bool src_f32, bool half = true) {
   switch (oh) {
-#define FP_CASE(N) \
-  case N:          \
-    return src_f32 ? k_chain_pipe<N, true> : k_chain_pipe<N, false>;
+#define FP_CASE(N)                                                          \
+  case N:                                                                   \
+    return src_f32 ? k_chain_pipe<N, true, true>                            \
+                   : (half ? k_chain_pipe<N, false, true> : k_chain_pipe<N, false, false>);
     FP_OH_LIST(FP_CASE)
 #undef FP_CASE
   }
@@ -1039,6 +1052,9 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, bool src_f32, int f
     KernelFn fn = kernel_for(oh, src_f32);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
+    if (e == cudaSuccess && !src_f32)  // the general-alpha IIR variant of the same window
+      e = cudaFuncSetAttribute(kernel_for(oh, false, false),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 0;
     if (e == cudaSuccess)
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHR, smem);
@@ -1111,7 +1127,8 @@ SegScratch& seg_scratch(int dev, cudaStream_t st) {
 
 // Shared launcher of both modes (src_f32: F345 from f32 planes).
 int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, fc_dims d,
-                int n_warm, const float* state_in, float* state_out, void* stream) {
+                int n_warm, const float* state_in, float* state_out, void* stream,
+                int pitch = 0, int opitch = 0) {
   if (d.frames == 0) return 0;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1143,6 +1160,7 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
   std::memset(&a, 0, sizeof a);
   layout(cache.oh, src_f32, &a);
   a.out = static_cast<uint8_t*>(out);
+  a.opitch = opitch ? opitch : d.width;
   a.W = d.width;
   a.H = d.height;
   a.n_frames = d.frames;
@@ -1190,7 +1208,7 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
   }
   CUtensorMap map;
   if (src_f32 ? !plane_tensor_map(&map, in, d, 128, 2 * cache.oh + 6)
-              : !rgb_tensor_map(&map, in, d, BWB, 2 * cache.oh + 6))
+              : !rgb_tensor_map(&map, in, d, BWB, 2 * cache.oh + 6, pitch ? pitch : d.width))
     return -1;
   const int grid = cache.strips * cache.bands * cache.n_segs;
   const bool profile = kn.profile != 0;
@@ -1198,7 +1216,8 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
     cudaMalloc(&a.dbg, sizeof(long long) * 8 * grid);
     cudaMemsetAsync(a.dbg, 0, sizeof(long long) * 8 * grid, st);
   }
-  kernel_for(cache.oh, src_f32)<<<grid, NTHR, cache.smem, st>>>(map, a);
+  const bool half = src_f32 || fp.alpha_half;
+  kernel_for(cache.oh, src_f32, half)<<<grid, NTHR, cache.smem, st>>>(map, a);
   int rc = int(cudaGetLastError());
   if (rc == 0 && verify) {
     // verify the segment seams, then (device-side decision) re-run every
@@ -1208,7 +1227,8 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
     Args f = a;
     f.fix_k = a.seg_k;
     f.seg_k = nullptr;
-    kernel_for(cache.oh, src_f32)<<<cache.strips * cache.bands, NTHR, cache.smem, st>>>(map, f);
+    kernel_for(cache.oh, src_f32, half)<<<cache.strips * cache.bands, NTHR, cache.smem, st>>>(
+        map, f);
     rc = int(cudaGetLastError());
   }
   if (profile && a.dbg) {  // per-CTA span and per-role wait shares
@@ -1270,13 +1290,33 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
 
 using namespace FP_NAMESPACE;
 
+// pitch: the video's row pitch in bytes (0 = width); the planes stay
+// [t][4][H][pitch].  -1: the chain or the layout is outside the certified path.
+// opitch: the mask's row pitch in bytes (0 = width): the stencil warps store
+// 4 mask bytes at a time, so rows must start 4-byte aligned.
 extern "C" int FP_ENTRY(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
                         const fc_stage* sthr, const void* video, int in_type, int gray_in,
                         void* out, int out_type, fc_dims d, int n_warm,
-                        const float* state_in, float* state_out, void* stream) {
+                        const float* state_in, float* state_out, int pitch, int opitch,
+                        void* stream) {
   FastParams fp;
-  if (!fast_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d, &fp)) return -1;
-  return launch_pipe(false, fp, video, out, d, n_warm, state_in, state_out, stream);
+  if (pitch == 0) pitch = d.width;
+  if (opitch == 0) opitch = d.width;
+  if (opitch < d.width || opitch % 4 != 0 || reinterpret_cast<uintptr_t>(out) % 4 != 0)
+    return -1;
+  if (!fast_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d, pitch, &fp))
+    return -1;
+  return launch_pipe(false, fp, video, out, d, n_warm, state_in, state_out, stream, pitch,
+                     opitch);
+}
+
+extern "C" int fc_chain_pipe_applies(const fc_stage* sgray, const fc_stage* si,
+                                     const fc_stage* sg, const fc_stage* sthr, int in_type,
+                                     int gray_in, int out_type, fc_dims d, int pitch) {
+  FastParams fp;
+  alignas(16) static const unsigned char probe[16] = {};
+  return fast_params(sgray, si, sg, sthr, probe, in_type, gray_in, out_type, d, pitch, &fp) &&
+         2 * 3 <= d.height;
 }
 
 // F345 (gaussian r=2 + Sobel + threshold) on f32 planes whose values lie in

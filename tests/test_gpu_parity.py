@@ -478,3 +478,44 @@ def test_simulate_matches_reference_run_tiled(fp, cuda, oracle, tmp_path, case):
     assert sim["outputs_identical"] == (want_count == 0)
     assert sim["measured_tiled_gmem"] == int(traffic[0] + traffic[1])
     assert sim["measured_serial_gmem"] == 2 * W * H * F * 5
+
+
+@pytest.mark.parametrize("alpha", [0.3, 0.0, 1.0, 0.75])
+def test_certified_pipeline_any_alpha(fp, cuda, oracle, alpha):
+    """The frame pipeline takes any IIR alpha in [0, 1] (the reference's
+    fl(fl(a x) + fl((1 - a) y)) update in the IIR warps), not only the folded
+    alpha = 0.5 form: bit-exact, no drop to the FP64 kernel."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    W, H, F = 256, 96, 30
+    pipe = spec_chain(W, H, F, alpha=alpha, th=30.0)
+    v = hash_video_u8(F, 4, H, W, 17)
+    want = oracle.orc_chain(pipe, v)
+    out, ex = run(fp, pipe, v, {"force_partition": "1-5"}, variant="fast", torch_dev=cuda)
+    np.testing.assert_array_equal(out, want)
+    assert "certified" in ex.describe()["last_chain_kernel"]
+
+
+@pytest.mark.parametrize("shape,offset", [((204, 97, 12), 0), ((252, 64, 9), 0),
+                                          ((256, 64, 9), 1), ((100, 40, 20), 3)])
+def test_certified_pipeline_any_width_and_base(fp, cuda, oracle, shape, offset):
+    """Widths that are not a multiple of 16 and video bases that are not
+    16-byte aligned (a view at a byte offset) run the frame pipeline on a
+    pitched copy of the R, G, B planes instead of the FP64 kernel."""
+    import torch
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    W, H, F = shape
+    pipe = spec_chain(W, H, F, th=30.0)
+    v = hash_video_u8(F, 4, H, W, 23)
+    want = oracle.orc_chain(pipe, v)
+    big = torch.empty(v.size + offset, dtype=torch.uint8, device=cuda)
+    dv = big[offset:].view(F, 4, H, W)
+    dv.copy_(torch.from_numpy(v))
+    p = fp.Pipeline(json.dumps(pipe))
+    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": "1-5"}),
+                     variant="fast")
+    out = ex.run(dv)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy().astype(np.float32), want)
+    kern = ex.describe()["last_chain_kernel"]
+    assert "certified" in kern
+    assert ("pitched" in kern) == (W % 16 != 0 or offset != 0)
