@@ -441,6 +441,7 @@ def main():
     if rank == 0 and not args.no_parity:
         parity = check_parity(pipe_spec, video, mask, warm)
 
+    desc_ex = ex.describe()  # after the runs: names the kernel that actually ran
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

@@ -19,7 +19,13 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libfuseplan_b200.so")
+# A/B tuning builds: FUSEPLAN_NVCC_EXTRA="-DFP_NF=5 -DFP_NI=6" and
+# FUSEPLAN_BUILD_TAG=nf5 build _build_nf5/ + libfuseplan_b200_nf5.so, loaded
+# with FUSEPLAN_LIB=<path> (never the shipped library)
+_TAG = os.environ.get("FUSEPLAN_BUILD_TAG", "")
+if _TAG:
+    OBJ = os.path.join(PKG, "_build_" + _TAG)
+LIB = os.path.join(PKG, "libfuseplan_b200" + ("_" + _TAG if _TAG else "") + ".so")
 
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
@@ -33,7 +39,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # No fast-math and no implicit contraction: the exact kernels spell out every
 # rounding with intrinsics; -fmad=false guards any plain float expression.
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false",
-                     "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"]
+                     "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"] + \
+    os.environ.get("FUSEPLAN_NVCC_EXTRA", "").split()
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
              "-Wno-unused-function", f"-I{os.path.join(ROOT, 'include')}", f"-I{JSON_DIR}",
              f"-I{CUDA_HOME}/include"]

@@ -642,13 +642,15 @@ int fc_stage_spatial(const fc_stage* s, const void* in, int in_type, void* out,
   long long hw = (long long)d.width * d.height, n = hw * d.frames;
   if (n == 0) return 0;
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  // 2-D stencil grid: 64 x 16 tiles, frames looped inside (z <= 65535)
+  // 2-D stencil grid: 64 x 16 tiles, frames looped inside (z <= 65535) about
+  // 8 frames per CTA: many short CTAs keep the hardware scheduler's dynamic
+  // balance (a grid sized to one resident wave ran 16 % slower: SMs got 6 or
+  // 7 CTAs of 500 frames each), and the frame loop keeps the per-CTA setup
+  // amortised.
   const int gx = (d.width + GX - 1) / GX, gy = (d.height + GY - 1) / GY;
-  const long long per_frame = (long long)gx * gy;
-  const int gz = int(std::max(1LL, std::min<long long>(
-                     d.frames, std::min<long long>(65535, (148LL * 16 + per_frame - 1) /
-                                                               per_frame))));
-  const dim3 tiles(gx, gy, gz);
+  auto frame_groups = [&](const void*, size_t) {
+    return int(std::max(1, std::min(65535, (d.frames + 7) / 8)));
+  };
   switch (s->op) {
     case FC_RGBA2GRAY:
       if (out_type != FC_F32) return -1;
@@ -669,21 +671,24 @@ int fc_stage_spatial(const fc_stage* s, const void* in, int in_type, void* out,
       GaussW w;
       const int K = 2 * s->g_radius + 1;
       for (int i = 0; i < K * K; ++i) w.w[i] = double(s->g_w[i]);
+#define FC_GK(R)                                                                       \
+  k_gaussian_x4<R><<<dim3(gx, gy, frame_groups((const void*)k_gaussian_x4<R>, 0)), 256, 0, \
+                     st>>>(f, o, w, d.width, d.height, d.frames)
       switch (s->g_radius) {
-        case 0: k_gaussian_x4<0><<<tiles, 256, 0, st>>>(f, o, w, d.width, d.height, d.frames); break;
-        case 1: k_gaussian_x4<1><<<tiles, 256, 0, st>>>(f, o, w, d.width, d.height, d.frames); break;
-        case 2: k_gaussian_x4<2><<<tiles, 256, 0, st>>>(f, o, w, d.width, d.height, d.frames); break;
-        case 3: k_gaussian_x4<3><<<tiles, 256, 0, st>>>(f, o, w, d.width, d.height, d.frames); break;
-        case 4: k_gaussian_x4<4><<<tiles, 256, 0, st>>>(f, o, w, d.width, d.height, d.frames); break;
+        case 0: FC_GK(0); break;
+        case 1: FC_GK(1); break;
+        case 2: FC_GK(2); break;
+        case 3: FC_GK(3); break;
+        case 4: FC_GK(4); break;
         default: return -1;
       }
+#undef FC_GK
       return status();
     }
     case FC_GRADIENT:
       if (in_type != FC_F32 || out_type != FC_F32) return -1;
-      k_gradient_x4<<<tiles, 256, 0, st>>>(static_cast<const float*>(in),
-                                           static_cast<float*>(out), d.width, d.height,
-                                           d.frames);
+      k_gradient_x4<<<dim3(gx, gy, frame_groups((const void*)k_gradient_x4, 0)), 256, 0, st>>>(
+          static_cast<const float*>(in), static_cast<float*>(out), d.width, d.height, d.frames);
       return status();
     case FC_THRESHOLD:
     case FC_IDENTITY:

@@ -50,18 +50,31 @@
 
 // Warp-role counts (compile-time; a tuning build may predefine them together
 // with FP_NAMESPACE / FP_ENTRY to compile a second layout alongside).
-#ifndef FP_NF
-// the shipped layout: one stencil warp per frame (4-column lanes, 168
+// The shipped layout: one stencil warp per frame (4-column lanes, 168
 // registers), 6 frames in flight, 5 IIR warps + the producer warp (12 warps),
 // 3 TMA slots, 8 IIR slots (measured 940 k vs 904 k frames/s for two 2-column
-// warps per frame, 5 frames, 16 warps at 128 registers)
+// warps per frame, 5 frames, 16 warps at 128 registers).  Each count can be
+// overridden with -D for A/B builds (build.py FUSEPLAN_NVCC_EXTRA).
+#ifndef FP_LC
 #define FP_LC 4
+#endif
+#ifndef FP_NF
 #define FP_NF 6
+#endif
+#ifndef FP_NI
 #define FP_NI 5
+#endif
+#ifndef FP_KSLACK
 #define FP_KSLACK 2
+#endif
+#ifndef FP_NSF
 #define FP_NSF 3
+#endif
+#ifndef FP_SPECIALISE
 #define FP_SPECIALISE 0  // one code path: 978 k vs 950 k (per-CTA variants slow
                          // the SMs around them -- instruction caches)
+#endif
+#ifndef FP_NAMESPACE
 #define FP_NAMESPACE fcpipe
 #define FP_ENTRY fc_chain_pipe
 #define FP_F345_ENTRY fc_f345_pipe
@@ -73,19 +86,9 @@
 #ifndef FP_WAIT_SLEEP
 #define FP_WAIT_SLEEP 0  // > 0: poll with plain try_wait + __nanosleep(ns) back-off
 #endif
-#ifndef FP_NSF
-#define FP_NSF 4  // RGB (TMA) frame slots
-#endif
-#ifndef FP_SPECIALISE
-#define FP_SPECIALISE 2  // 1: interior / border variants of every role per CTA;
-                         // 0: the general (border) variant everywhere; 2: IIR /
-                         // plane roles specialised, one stencil path (measured:
-                         // 2 > 0 by 0.6 % > 1 by 1.5 % -- the stencil code must
-                         // stay single to keep the instruction caches warm)
-#endif
-#ifndef FP_LC
-#define FP_LC 2
-#endif
+// FP_SPECIALISE 1: interior / border variants of every role per CTA; 0: the
+// general (border) variant everywhere; 2: IIR / plane roles specialised, one
+// stencil path (measured: 0 is fastest in the 12-warp layout).
 #ifndef FP_IIR_TMA
 #define FP_IIR_TMA 1  // all-fused mode: the TMA producer warp is also an IIR warp
 #endif
@@ -1023,7 +1026,8 @@ struct PipePlan {
   size_t smem = 0;
 };
 
-constexpr int SEG_WARM = 64;  // IIR warm-up of a time segment (48 suffices)
+constexpr int SEG_WARM = 48;  // IIR warm-up of a time segment (48 -> no mismatch;
+                              // the seam check + fix-up keep any length exact)
 
 // Every CTA marches its frames; an SM's time is ~ (CTAs it runs) x (pair-rows
 // of a window) x (frames of a CTA, warm-up frames at ~0.4 of a full frame).

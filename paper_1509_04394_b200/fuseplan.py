@@ -24,7 +24,7 @@ from typing import Optional, Union
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libfuseplan_b200.so")
+LIB_PATH = os.environ.get("FUSEPLAN_LIB") or os.path.join(PKG, "libfuseplan_b200.so")
 DATA_DIR = os.path.join(PKG, "data")
 
 FP_OK, FP_ERR_INFEASIBLE, FP_ERR_INPUT, FP_ERR_INTERNAL = 0, 1, 2, 3
