@@ -48,7 +48,7 @@ CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
 HOST_SRCS = ["host/model.cpp", "host/planner.cpp", "host/video.cpp",
              "host/exec.cpp", "host/capi.cpp",
              "host/calibrate.cpp", "host/shard.cpp", "host/simulate.cpp"]
-CUDA_SRCS = ["kernels/fc_exact.cu", "kernels/fc_pipe.cu", "kernels/fc_f12.cu",
+CUDA_SRCS = ["kernels/fc_exact.cu", "kernels/fc_pipe.cu", "kernels/fc_pipe2.cu", "kernels/fc_f12.cu",
              "kernels/fc_track.cu", "kernels/fc_tiled.cu", "kernels/fc_shard.cu",
              "kernels/fc_dispatch.cu"]
 HEADERS = ["kernels/fc_pipe.cu", "host/exec.hpp", "host/video.hpp",

@@ -21,6 +21,12 @@ extern "C" int fc_chain_pipe(const fc_stage* sgray, const fc_stage* si, const fc
                              void* out, int out_type, fc_dims d, int n_warm,
                              const float* state_in, float* state_out, int pitch, int opitch,
                              void* stream);  // fc_pipe.cu: certified, headline
+extern "C" int fc_chain_pipe2(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                              const fc_stage* sthr, const void* video, int in_type, int gray_in,
+                              void* out, int out_type, fc_dims d, int n_warm,
+                              const float* state_in, float* state_out, int pitch, int opitch,
+                              void* stream);  // fc_pipe2.cu: certified, frame pairs
+extern "C" long long fc_pipe2_recheck_count(void);
 extern "C" int fc_f345_pipe(const fc_stage* sg, const fc_stage* sthr, const float* in,
                             void* out, int out_type, fc_dims d, double in_max, void* stream);
 extern "C" long long fc_pipe_recheck_count(void);
@@ -47,6 +53,7 @@ extern "C" void fc_knobs_from_env(fc_knobs* k) {
     k->dbg_px_on = std::sscanf(e, "%d,%d,%d", &k->dbg_px[0], &k->dbg_px[1], &k->dbg_px[2]) == 3;
   k->f12_stream = std::getenv("FUSEPLAN_F12_STREAM") != nullptr;
   k->f12_legacy = std::getenv("FUSEPLAN_F12_LEGACY") != nullptr;
+  k->pipe_impl = env_int("FUSEPLAN_PIPE_IMPL");
 }
 
 extern "C" void fc_set_knobs(const fc_knobs* k) {
@@ -77,15 +84,19 @@ extern "C" int fc_fused_chain_pitched(const fc_stage* sgray, const fc_stage* si,
                                       void* stream) {
   (void)sgrad;
   if (variant == 2 || variant == 0) {
-    const int rc = fc_chain_pipe(sgray, si, sg, sthr, pitched ? pitched : video, in_type, gray_in,
-                                 pitched_out ? pitched_out : out, out_type, d, n_warm, state_in,
-                                 state_out, pitched ? video_pitch : 0,
-                                 pitched_out ? out_pitch : 0, stream);
+    // frame-pair pipeline (fc_pipe2.cu) unless the row-pair one is forced
+    const bool pair = fc_get_knobs()->pipe_impl != 1;
+    const auto fn = pair ? fc_chain_pipe2 : fc_chain_pipe;
+    const int rc = fn(sgray, si, sg, sthr, pitched ? pitched : video, in_type, gray_in,
+                      pitched_out ? pitched_out : out, out_type, d, n_warm, state_in, state_out,
+                      pitched ? video_pitch : 0, pitched_out ? out_pitch : 0, stream);
     if (rc == 0 && pitched_out)  // the mask rows back to their contiguous layout
       return int(cudaMemcpy2DAsync(out, size_t(d.width), pitched_out, size_t(out_pitch),
                                    size_t(d.width), size_t(d.height) * (d.frames - n_warm),
                                    cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
-    if (rc != -1) g_last_chain = "certified FP32 frame pipeline (fc_pipe.cu)";
+    if (rc != -1)
+      g_last_chain = pair ? "certified FP32 frame-pair pipeline (fc_pipe2.cu)"
+                          : "certified FP32 row-pair pipeline (fc_pipe.cu)";
     if (rc != -1 || variant == 2) return rc;  // -1: parameters not covered
   }
   g_last_chain = "exact FP64 tiles (fc_exact.cu k_chain_exact)";
@@ -112,7 +123,9 @@ extern "C" int fc_chain_pipe_applies(const fc_stage* sgray, const fc_stage* si,
                                      const fc_stage* sg, const fc_stage* sthr, int in_type,
                                      int gray_in, int out_type, fc_dims d, int pitch);
 
-extern "C" long long fc_last_recheck_count(void) { return fc_pipe_recheck_count(); }
+extern "C" long long fc_last_recheck_count(void) {
+  return fc_pipe_recheck_count() + fc_pipe2_recheck_count();
+}
 
 extern "C" int fc_fused_gauss_grad_thr_v(const fc_stage* sg, const fc_stage* sgrad,
                                          const fc_stage* sthr, const float* in, void* out,

@@ -362,10 +362,14 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
   const int f0 = rg.f0;
   auto issue = [&](int tp) {
     wait_phase(bar_rgb_empty(a, pslot), ppar ^ 1u);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bar_rgb_full(a, pslot), a.rgb_bytes);
-    tma_load_3d(fp_smem + pslot * a.rgb_stride, tmap, bar_rgb_full(a, pslot), tx0, by,
-                4 * (f0 + tp));
+    if (a.skip & 4) {  // timing experiment: no RGB transfer (stale slot contents)
+      mbar_arrive(bar_rgb_full(a, pslot));
+    } else {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar_rgb_full(a, pslot), a.rgb_bytes);
+      tma_load_3d(fp_smem + pslot * a.rgb_stride, tmap, bar_rgb_full(a, pslot), tx0, by,
+                  4 * (f0 + tp));
+    }
     if (++pslot == NSF) {
       pslot = 0;
       ppar ^= 1u;

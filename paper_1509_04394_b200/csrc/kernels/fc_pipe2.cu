@@ -1,0 +1,946 @@
+// F12345 certified fast path, FRAME-PAIR PIPELINE (the headline kernel).
+//
+// Arithmetic contract: exact S1+S2 (gray products fl(w c) from one FMA on a
+// byte->float magic number, the IIR update in the reference's roundings),
+// certified packed-FP32 S3-S5 (centre-normalised separable gaussian, Sobel,
+// m compared with M* inside a rigorous error band, fccommon::certify_band_scaled)
+// and an exact FP64 recheck (simulator.cpp:63-89 order) of every value inside
+// the band.  The mask is bit-identical to run_sequential's
+// (/root/reference/proj/src/simulator.cpp:158-177).
+//
+// Work decomposition (B200: the FP32 pipe, not HBM, bounds this chain; see
+// DESIGN.md section 4).  A CTA owns a window of 128 columns x R = OUT + 6
+// rows (outputs: the central 120 columns x OUT rows) and marches all frames.
+// Every stencil value is a float2 pairing two consecutive FRAMES (t, t+1) of
+// the same pixel, so each window row is computed exactly once per frame (the
+// row-pair layout of fc_pipe.cu paired rows p and p + OH and recomputed the 6
+// rows both halves share).  Warp roles, one CTA per SM:
+//
+//   stencil warps 0..3  one per SM sub-partition; warp w takes frame pairs
+//                       w, w + 4, ... from the IIR ring and marches the
+//                       window's rows: horizontal 5-tap pass, vertical 5-tap
+//                       pass and Sobel in registers (skewed software
+//                       pipeline), certified threshold, mask words straight
+//                       to HBM (frame t and t+1), exact rechecks after the
+//                       march from the pair's exact IIR planes in the slot;
+//   IIR warps 4..11     each lane owns 4 columns of fixed window rows and
+//                       keeps their exact IIR state in registers for the
+//                       whole video; per frame: gray (packed over column
+//                       pairs) + IIR update (scalar, so the two frames of a
+//                       pixel land in one register pair), one STS.128 per 2
+//                       columns x 2 frames into the pair slot; lane 0 of the
+//                       last IIR warp also issues the R, G, B TMA copies
+//                       (NSF - 1 frames ahead; alpha never leaves HBM).
+//
+// Pair slot layout (1 KB per window row): 64 16-byte chunks, chunk k holds
+// columns 2k and 2k+1 as {IIR_t, IIR_t+1} each; even chunks at 0..31, odd
+// chunks rotated by 4 at 32..63 (conflict-light STS.128 / LDS.128).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "fc_common.cuh"
+
+namespace fcpipe2 {
+
+using namespace fccommon;
+
+constexpr int LC = 4;       // columns per stencil lane
+constexpr int NS = 4;       // stencil warps (one per SM sub-partition)
+constexpr int NI = 8;       // IIR warps (two per SM sub-partition)
+constexpr int NWARP = NS + NI;
+constexpr int NTHR = NWARP * 32;
+constexpr int K2 = NS + 1;  // pair slots: one per stencil warp + one being written
+constexpr int NSF = 3;      // TMA RGB frame slots
+constexpr int SW = 120;     // output columns per strip (window 128 = SW + 8)
+constexpr int BWB = 144;    // TMA box row bytes: 128 + worst-case 16-B alignment slack
+constexpr int PROW = 1024;  // bytes per window row of a pair slot
+constexpr int QC = 64;      // recheck queue records per stencil warp
+constexpr int BODY = 6;     // steps per rolled body of the stencil march
+
+struct Args {
+  uint8_t* out;
+  int W, H, n_frames, n_warm;
+  int strips;
+  unsigned rgb_bytes, rgb_stride;  // TMA bytes per frame, RGB slot pitch
+  unsigned off_iir, iir_stride;    // pair ring base, pair slot pitch
+  unsigned off_bar, off_taps, off_queue;
+  const float* state_in;
+  float* state_out;
+  // time segments (see fc_pipe.cu Args): CTA b works on window b % n_windows
+  // and output frames [s L, (s+1) L) of segment s = b / n_windows
+  int n_windows, n_segs, seg_len, seg_warm;
+  float* seg_end;
+  float* seg_warm_out;
+  int* fix_k;
+  int* seg_k;
+  int skip;    // timing experiments only (FUSEPLAN_PIPE_SKIP): 1 IIR math, 2 stencil math, 4 no TMA
+  int opitch;  // output row pitch in bytes (>= W, a multiple of 4)
+  FastParams p;
+};
+
+struct Range {
+  int f0;       // first input frame (video index)
+  int n;        // frames processed
+  int n_warm;   // leading warm-up frames (IIR state only)
+  int out0;     // first output frame index (relative to `out`)
+  const float* st_in;
+  float* st_out;
+  float* st_warm;
+};
+
+__shared__ Range fp2_rg;
+__device__ unsigned long long g_rechecks2;
+extern __shared__ __align__(128) unsigned char fp2_smem[];
+
+// mbarrier layout: rgb_full[NSF], rgb_empty[NSF], iir_full[K2], iir_empty[K2]
+__device__ __forceinline__ uint64_t* bar_at(const Args& a, int i) {
+  return reinterpret_cast<uint64_t*>(fp2_smem + a.off_bar) + i;
+}
+__device__ __forceinline__ uint64_t* bar_rgb_full(const Args& a, int i) { return bar_at(a, i); }
+__device__ __forceinline__ uint64_t* bar_rgb_empty(const Args& a, int i) {
+  return bar_at(a, NSF + i);
+}
+__device__ __forceinline__ uint64_t* bar_iir_full(const Args& a, int i) {
+  return bar_at(a, 2 * NSF + i);
+}
+__device__ __forceinline__ uint64_t* bar_iir_empty(const Args& a, int i) {
+  return bar_at(a, 2 * NSF + K2 + i);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_lane0(uint64_t* bar, int lane) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.eq.u32 q, %1, 0;\n@q mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::
+          "r"(smem_u32(bar)),
+      "r"(unsigned(lane))
+      : "memory");
+}
+__device__ __forceinline__ void wait_phase(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(1000000u)
+      : "memory");
+}
+
+__device__ __forceinline__ void sts_pred_u32(uint32_t* p, uint32_t v, bool on) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.shared.b32 [%0], %1;\n}\n" ::"r"(
+          smem_u32(p)),
+      "r"(v), "r"(unsigned(on))
+      : "memory");
+}
+__device__ __forceinline__ void st_pred_u32(void* p, uint32_t v, bool on) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.global.b32 [%0], %1;\n}\n" ::"l"(p),
+      "r"(v), "r"(unsigned(on))
+      : "memory");
+}
+
+// byte offset of chunk k (columns 2k, 2k+1) inside a slot row
+__device__ __forceinline__ unsigned chunk_off(int k) {
+  return unsigned((k & 1) ? 32 + (((k >> 1) + 4) & 31) : (k >> 1)) << 4;
+}
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128f(unsigned addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+// Centre-normalised 5-tap pass (centre tap 1): 4 packed ops
+__device__ __forceinline__ float2 tap4n(float2 a, float2 b, float2 c, float2 d, float2 e,
+                                        float g0, float g1) {
+  return __ffma2_rn(splat(g1), __fadd2_rn(b, d), __ffma2_rn(splat(g0), __fadd2_rn(a, e), c));
+}
+
+__device__ __forceinline__ float2 shfl_up2(float2 v) {
+  return make_float2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ float2 shfl_down2(float2 v) {
+  return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1),
+                     __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+
+// |a|, |b| folded into a running minimum: one FMNMX3
+__device__ __forceinline__ float min3abs(float m, float a, float b) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(m), "f"(fabsf(a)), "f"(fabsf(b)));
+  return r;
+}
+
+// ------------------------------------------------------------------ IIR warps
+
+template <int OUT, bool HALF>
+__device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw, int lane,
+                                         int bx, int by, int xoff, const CUtensorMap* tmap,
+                                         int tx0) {
+  constexpr int R = OUT + 6;
+  constexpr int NR = (R + NI - 1) / NI;  // rows of this warp: p = iw + NI r
+  const int W = a.W, H = a.H, n = rg.n, n_warm = rg.n_warm;
+  const int n_out = n - n_warm;
+  const int cplane = R * BWB;
+  const int xl = bx + 4 * lane;
+  const uint32_t k4b = a.p.k4b;
+  const float wr = a.p.wr, wg = a.p.wg, wb = a.p.wb;
+  const float wrm = a.p.wrm, wgm = a.p.wgm, wbm = a.p.wbm;
+  const float ia = a.p.ia, ib = a.p.ib;
+
+  int rowo[NR];  // RGB slot byte offset of row p (clamped to the video)
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int p = min(iw + NI * r, R - 1);
+    rowo[r] = (clampi(by + p, 0, H - 1) - by) * BWB;
+  }
+  int coloff = xoff + 4 * lane;
+  // magic-float PRMT selectors: byte j of the word, or (lanes left / right
+  // of the video) the edge byte in every cell
+  uint32_t msel[4] = {0x7440u, 0x7441u, 0x7442u, 0x7443u};
+  if (xl < 0 || xl > W - 1) {
+    const int edge = xl < 0 ? 0 : W - 1;
+    coloff = (edge & ~3) - bx + xoff;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) msel[j] = 0x7440u + unsigned(edge & 3);
+  }
+  const unsigned so0 = chunk_off(2 * lane), so1 = chunk_off(2 * lane + 1);
+
+  float y[NR][4];  // exact IIR state of the lane's cells
+  const bool fresh = rg.st_in == nullptr;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int p = iw + NI * r;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (fresh || p >= R)
+        y[r][j] = 0.0f;
+      else
+        y[r][j] = rg.st_in[(long long)clampi(by + p, 0, H - 1) * W + clampi(xl + j, 0, W - 1)];
+    }
+  }
+  // the lane's output cells (window rows 3 .. OUT + 2) -> a state plane
+  auto write_state = [&](float* dst) {
+    if (!dst || lane < 1 || lane > 30 || xl >= W) return;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int p = iw + NI * r;
+      if (p < 3 || p > OUT + 2 || by + p >= H) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[(long long)(by + p) * W + xl + j] = y[r][j];
+    }
+  };
+
+  const unsigned smem0 = smem_u32(fp2_smem);
+  int rslot = 0, islot = 0;
+  unsigned rpar = 0, ipar = 0;
+  // lane 0 of the last IIR warp keeps NSF - 1 frames of RGB in flight; the
+  // slot of frame t + NSF - 1 is that of frame t - 1, released by every IIR
+  // warp (this one included) before this warp starts frame t
+  const bool prod = iw == NI - 1 && lane == 0;
+  int pslot = 0;
+  unsigned ppar = 0;
+  const int f0 = rg.f0;
+  auto issue = [&](int tp) {
+    wait_phase(bar_rgb_empty(a, pslot), ppar ^ 1u);
+    if (a.skip & 4) {
+      mbar_arrive(bar_rgb_full(a, pslot));
+    } else {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar_rgb_full(a, pslot), a.rgb_bytes);
+      tma_load_3d(fp2_smem + pslot * a.rgb_stride, tmap, bar_rgb_full(a, pslot), tx0, by,
+                  4 * (f0 + tp));
+    }
+    if (++pslot == NSF) {
+      pslot = 0;
+      ppar ^= 1u;
+    }
+  };
+  if (prod) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+    for (int tp = 0; tp < NSF - 1 && tp < n; ++tp) issue(tp);
+  }
+
+  // gray of frame t for every cell: g[r][h] = {gray(col 2h), gray(col 2h+1)}
+  // (x 0.5 when HALF: alpha folded into the weights)
+  auto gray = [&](int t, float2 (&g)[NR][2]) {
+    if (prod && t + NSF - 1 < n) issue(t + NSF - 1);
+    wait_phase(bar_rgb_full(a, rslot), rpar);
+    const unsigned char* f = fp2_smem + rslot * a.rgb_stride;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      if (iw + NI * r >= R) continue;
+      uint32_t w[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        w[c] = *reinterpret_cast<const uint32_t*>(f + c * cplane + rowo[r] + coloff);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float2 pr = wprod(f2(magic_rs(w[0], k4b, msel[2 * h]),
+                                   magic_rs(w[0], k4b, msel[2 * h + 1])), wr, wrm);
+        const float2 pg = wprod(f2(magic_rs(w[1], k4b, msel[2 * h]),
+                                   magic_rs(w[1], k4b, msel[2 * h + 1])), wg, wgm);
+        const float2 pb = wprod(f2(magic_rs(w[2], k4b, msel[2 * h]),
+                                   magic_rs(w[2], k4b, msel[2 * h + 1])), wb, wbm);
+        g[r][h] = __fadd2_rn(__fadd2_rn(pr, pg), pb);  // (wr r + wg g) + wb b
+      }
+    }
+    __syncwarp();  // the warp's RGB reads are done (values in registers)
+    mbar_arrive_lane0(bar_rgb_empty(a, rslot), lane);
+    if (++rslot == NSF) {
+      rslot = 0;
+      rpar ^= 1u;
+    }
+  };
+  // IIR update of cell (r, j) with its gray value gj (simulator.cpp:57-62):
+  // HALF: fl(0.5 x + fl(0.5 y)) == FMA(0.5, y, 0.5 x) (x = gray > 0 dwarfs
+  // any rounding of 0.5 y; x = 0 gives fl(0.5 y) either way); otherwise
+  // fl(fl(a x) + fl(b y)) in scalar .rn ops.  First frame: y = gray.
+  auto upd = [&](float yo, float gj, bool first) -> float {
+    if (HALF) return first ? __fadd_rn(gj, gj) : __fmaf_rn(0.5f, yo, gj);
+    return first ? gj : __fadd_rn(__fmul_rn(ia, gj), __fmul_rn(ib, yo));
+  };
+  auto step_frame = [&](int t, float (&yn)[NR][4], const float (&yo)[NR][4]) {
+    float2 g[NR][2];
+    gray(t, g);
+    const bool first = fresh && t == 0;
+    if (a.skip & 1) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) yn[r][j] = yo[r][j];
+      return;
+    }
+    if (first) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        yn[r][0] = upd(yo[r][0], g[r][0].x, true);
+        yn[r][1] = upd(yo[r][1], g[r][0].y, true);
+        yn[r][2] = upd(yo[r][2], g[r][1].x, true);
+        yn[r][3] = upd(yo[r][3], g[r][1].y, true);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        yn[r][0] = upd(yo[r][0], g[r][0].x, false);
+        yn[r][1] = upd(yo[r][1], g[r][0].y, false);
+        yn[r][2] = upd(yo[r][2], g[r][1].x, false);
+        yn[r][3] = upd(yo[r][3], g[r][1].y, false);
+      }
+    }
+  };
+
+  // warm-up frames: state only
+  for (int t = 0; t < n_warm; ++t) {
+    float yn[NR][4];
+    step_frame(t, yn, y);
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) y[r][j] = yn[r][j];
+    if (t == n_warm - 1) write_state(rg.st_warm);
+  }
+  // output frames in pairs (A = t, B = t + 1; an odd tail stores {A, A})
+  for (int k = 0; k < n_out; k += 2) {
+    const int t = n_warm + k;
+    float ya[NR][4];
+    step_frame(t, ya, y);
+    if (k + 1 < n_out) {
+      step_frame(t + 1, y, ya);
+    } else {
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) y[r][j] = ya[r][j];
+    }
+    wait_phase(bar_iir_empty(a, islot), ipar ^ 1u);
+    const unsigned base = smem0 + a.off_iir + islot * a.iir_stride;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int p = iw + NI * r;
+      if (p >= R) continue;
+      sts128f(base + p * PROW + so0, ya[r][0], y[r][0], ya[r][1], y[r][1]);
+      sts128f(base + p * PROW + so1, ya[r][2], y[r][2], ya[r][3], y[r][3]);
+    }
+    __syncwarp();  // the warp's stores precede the release arrive
+    mbar_arrive_lane0(bar_iir_full(a, islot), lane);
+    if (++islot == K2) {
+      islot = 0;
+      ipar ^= 1u;
+    }
+  }
+  write_state(rg.st_out);
+}
+
+// ------------------------------------------------------------------ stencil warps
+
+// Exact IIR value of window cell (row rho, col c) of frame `comp` of the pair
+__device__ __forceinline__ float iir_at(const unsigned char* base, int rho, int c, int comp) {
+  return *reinterpret_cast<const float*>(base + rho * PROW + chunk_off(c >> 1) + (c & 1) * 8 +
+                                         comp * 4);
+}
+
+// Exact reference threshold decision at video (x, y), frame `comp` of the
+// pair: FP64 gaussian in dy/dx order at the 3x3 clamped centres, Sobel in
+// the reference's float order, IEEE sqrt (simulator.cpp:63-89).
+__device__ __noinline__ bool exact_white(const Args& a, const unsigned char* base,
+                                         const double* taps, int bx, int by, int x, int y,
+                                         int comp) {
+  float g[3][3];
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < 3; ++i) {
+      const int cx = clampi(x + i - 1, 0, a.W - 1), cy = clampi(y + j - 1, 0, a.H - 1);
+      double acc = 0.0;
+      for (int dy = -2; dy <= 2; ++dy) {
+        const int ry = clampi(cy + dy, 0, a.H - 1) - by;
+        for (int dx = -2; dx <= 2; ++dx) {
+          const int rx = clampi(cx + dx, 0, a.W - 1) - bx;
+          acc = __fma_rn(taps[(dy + 2) * 5 + dx + 2], double(iir_at(base, ry, rx, comp)), acc);
+        }
+      }
+      g[j][i] = __double2float_rn(acc);
+    }
+  auto s = [&](int dx, int dy) { return g[dy + 1][dx + 1]; };
+  const float gx =
+      __fsub_rn(__fadd_rn(__fadd_rn(s(1, -1), __fmul_rn(2.0f, s(1, 0))), s(1, 1)),
+                __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(-1, 0))), s(-1, 1)));
+  const float gy =
+      __fsub_rn(__fadd_rn(__fadd_rn(s(-1, 1), __fmul_rn(2.0f, s(0, 1))), s(1, 1)),
+                __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(0, -1))), s(1, -1)));
+  return __fsqrt_rn(__fadd_rn(__fmul_rn(gx, gx), __fmul_rn(gy, gy))) >= a.p.th_val;
+}
+
+template <int N>
+using ic = std::integral_constant<int, N>;
+
+// Stencil warp sw: frame pairs sw, sw + NS, ... of the pair ring.  Lane L
+// owns window columns 4L .. 4L+3 (outputs: lanes 1..30).  The march over the
+// window rows p = 0 .. R + 1 is a loop of 6-step bodies (ring indices are
+// compile-time constants):
+//   step p: H row p (4 x 16-byte loads: chunks 2L-1 .. 2L+2);
+//           G row p - 3 (from H rows p-5 .. p-1); Sobel + threshold at row p - 5.
+// Uncertain values are queued in shared memory (record: first row, lane,
+// rows) and recomputed exactly after the march.
+template <int OUT>
+__device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int sw, int lane,
+                                             int bx, int by) {
+  constexpr int NP = OUT + 6;
+  const int W = a.W, H = a.H;
+  const int n_out = rg.n - rg.n_warm;
+  const int n_pairs = (n_out + 1) / 2;
+  const float mlo = a.p.mlo_n, band = a.p.band_n;  // scaled domain (normalised taps)
+  const float g0 = a.p.g0, g1 = a.p.g1;
+  const double* taps = reinterpret_cast<const double*>(fp2_smem + a.off_taps);
+  uint32_t* queue = reinterpret_cast<uint32_t*>(fp2_smem + a.off_queue) + sw * QC;
+  const int k = 2 * lane;       // the lane's first chunk
+  const int xl = bx + 2 * k;    // video column of the lane's first cell
+  const bool outl = lane >= 1 && lane <= 30 && xl < W;
+  const bool xlo = xl == 0, xhi = xl + LC - 1 == W - 1;  // Sobel x clamps (video edges)
+  unsigned cch[LC / 2 + 2];
+#pragma unroll
+  for (int i = 0; i < LC / 2 + 2; ++i) cch[i] = chunk_off((k - 1 + i + 64) & 63);
+  const unsigned smem0 = smem_u32(fp2_smem);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int OW = a.opitch;
+  const long long fstride = (long long)OW * H;
+
+  int slot = sw % K2;
+  unsigned par = (sw / K2) & 1u;
+  for (int u = sw; u < n_pairs; u += NS) {
+    wait_phase(bar_iir_full(a, slot), par);
+    const unsigned base = smem0 + a.off_iir + slot * a.iir_stride;
+    const bool has_b = 2 * u + 1 < n_out;
+    unsigned char* o = a.out + (long long)(rg.out0 + 2 * u) * fstride;
+    unsigned char* ox = o + (long long)(by + 3) * OW + xl;  // frame A, window row 3
+    const bool oka = outl, okb = outl && has_b;
+    int nq = 0;
+    float amin = __int_as_float(0x7f800000);
+
+    float2 hr[6][LC];  // H row r at ring index r % 6 ({frame A, frame B})
+    float2 gr[6][LC];  // G row r at ring index r % 6
+
+    auto step = [&](auto pm_t, auto h_t, auto v_t, auto s_t, auto yb_t, int p) {
+      constexpr int PM = decltype(pm_t)::value;  // p % 6
+      constexpr bool DO_H = decltype(h_t)::value, DO_V = decltype(v_t)::value;
+      constexpr bool DO_S = decltype(s_t)::value;
+      constexpr int YB = decltype(yb_t)::value;
+      if constexpr (DO_H) {
+        const unsigned rb = base + p * PROW;
+        float2 v[LC + 4];  // columns c-2 .. c+LC+1
+#pragma unroll
+        for (int i = 0; i < LC / 2 + 2; ++i) {
+          const float4 q4 = lds128(rb + cch[i]);
+          v[2 * i] = lo2(q4);
+          v[2 * i + 1] = hi2(q4);
+        }
+#pragma unroll
+        for (int j = 0; j < LC; ++j)
+          hr[PM][j] = tap4n(v[j], v[j + 1], v[j + 2], v[j + 3], v[j + 4], g0, g1);
+      }
+      if constexpr (DO_V) {
+#pragma unroll
+        for (int j = 0; j < LC; ++j)
+          gr[(PM + 3) % 6][j] = tap4n(hr[(PM + 1) % 6][j], hr[(PM + 2) % 6][j],
+                                      hr[(PM + 3) % 6][j], hr[(PM + 4) % 6][j],
+                                      hr[(PM + 5) % 6][j], g0, g1);
+      }
+      if constexpr (DO_S) {
+        constexpr int QM = (PM + 1) % 6;  // q % 6
+        const int yq = by + p - 5;        // video row of the Sobel centre
+        float2 s2[LC], d2[LC];
+#pragma unroll
+        for (int j = 0; j < LC; ++j) {
+          float2 gm = gr[(QM + 5) % 6][j], gc = gr[QM][j], gp = gr[(QM + 1) % 6][j];
+          if (YB == 1 && yq == 0) gm = gc;      // top video row (band 0, first Sobel step)
+          if (YB == 2 && yq == H - 1) gp = gc;  // bottom video row (last band, last step)
+          s2[j] = __fadd2_rn(__ffma2_rn(splat(2.0f), gc, gm), gp);
+          d2[j] = __ffma2_rn(splat(-1.0f), gm, gp);
+        }
+        float2 sl = shfl_up2(s2[LC - 1]), dl = shfl_up2(d2[LC - 1]);
+        float2 sr = shfl_down2(s2[0]), dr = shfl_down2(d2[0]);
+        if (xlo) sl = s2[0], dl = d2[0];
+        if (xhi) sr = s2[LC - 1], dr = d2[LC - 1];
+        float2 S[LC + 2], D[LC + 2];
+        S[0] = sl, D[0] = dl, S[LC + 1] = sr, D[LC + 1] = dr;
+#pragma unroll
+        for (int j = 0; j < LC; ++j) S[j + 1] = s2[j], D[j + 1] = d2[j];
+        float2 dm[LC];
+#pragma unroll
+        for (int j = 0; j < LC; ++j) {
+          const float2 gx = __ffma2_rn(splat(-1.0f), S[j], S[j + 2]);
+          const float2 gy = __fadd2_rn(__ffma2_rn(splat(2.0f), D[j + 1], D[j]), D[j + 2]);
+          // nd = mlo - gy^2 - gx^2 (< 0 <=> white)
+          const float2 ngx = f2(-gx.x, -gx.y), ngy = f2(-gy.x, -gy.y);
+          dm[j] = __ffma2_rn(ngx, gx, __ffma2_rn(ngy, gy, splat(mlo)));
+        }
+        st_pred_u32(ox, pack_neg(dm[0].x, dm[1].x, dm[2].x, dm[3].x), oka);
+        st_pred_u32(ox + fstride, pack_neg(dm[0].y, dm[1].y, dm[2].y, dm[3].y), okb);
+        ox += OW;
+#pragma unroll
+        for (int j = 0; j < LC; ++j) amin = min3abs(amin, dm[j].x, dm[j].y);
+      }
+    };
+    auto flush = [&](int q0, int nstep) {
+      const bool amb = outl && amin <= band;
+      const unsigned ballot = __ballot_sync(0xffffffffu, amb);
+      if (ballot) {
+        const int i = nq + __popc(ballot & lt_mask);
+        sts_pred_u32(queue + min(i, QC - 1),
+                     (unsigned(q0) << 16) | (lane << 8) | unsigned(nstep), amb && i < QC);
+        nq += __popc(ballot);
+        amin = __int_as_float(0x7f800000);
+      }
+    };
+
+    const auto F = std::false_type{};
+    const auto T = std::true_type{};
+    if (!(a.skip & 2)) {
+      const auto Y0 = ic<0>{};
+      step(ic<0>{}, T, F, F, Y0, 0);
+      step(ic<1>{}, T, F, F, Y0, 1);
+      step(ic<2>{}, T, F, F, Y0, 2);
+      step(ic<3>{}, T, F, F, Y0, 3);
+      step(ic<4>{}, T, F, F, Y0, 4);
+      step(ic<5>{}, T, T, F, Y0, 5);
+      step(ic<0>{}, T, T, F, Y0, 6);
+      step(ic<1>{}, T, T, F, Y0, 7);
+      step(ic<2>{}, T, T, T, ic<1>{}, 8);  // Sobel row 3: the video's top row in band 0
+      flush(3, 1);
+#pragma unroll 1
+      for (int p = 9; p + 6 <= NP; p += 6) {
+        step(ic<3>{}, T, T, T, Y0, p);
+        step(ic<4>{}, T, T, T, Y0, p + 1);
+        step(ic<5>{}, T, T, T, Y0, p + 2);
+        step(ic<0>{}, T, T, T, Y0, p + 3);
+        step(ic<1>{}, T, T, T, Y0, p + 4);
+        step(ic<2>{}, T, T, T, Y0, p + 5);
+        flush(p - 5, BODY);
+      }
+      constexpr int PT = 9 + 6 * ((NP - 9) / 6);
+      if constexpr (NP - PT >= 1) step(ic<3>{}, T, T, T, Y0, PT);
+      if constexpr (NP - PT >= 2) step(ic<4>{}, T, T, T, Y0, PT + 1);
+      if constexpr (NP - PT >= 3) step(ic<5>{}, T, T, T, Y0, PT + 2);
+      if constexpr (NP - PT >= 4) step(ic<0>{}, T, T, T, Y0, PT + 3);
+      if constexpr (NP - PT >= 5) step(ic<1>{}, T, T, T, Y0, PT + 4);
+      if constexpr (NP - PT >= 1) flush(PT - 5, NP - PT);
+      step(ic<NP % 6>{}, F, T, T, Y0, NP);
+      step(ic<(NP + 1) % 6>{}, F, F, T, ic<2>{}, NP + 1);  // bottom row of the last band
+      flush(NP - 5, 2);
+
+      // ---- exact recheck of the queued uncertain values (rare)
+      if (nq > QC) {
+        // queue overflow (adversarial input): the exact decision for every
+        // output pixel of this warp's pair
+        __syncwarp();
+        const unsigned char* sb = fp2_smem + (base - smem0);
+        if (outl)
+          for (int q = 3; q <= OUT + 2; ++q)
+            for (int c = 0; c < (has_b ? 2 : 1); ++c) {
+              const int yy = by + q;
+              if (yy >= H) continue;
+              for (int j = 0; j < LC; ++j)
+                o[c * fstride + (long long)yy * OW + xl + j] =
+                    exact_white(a, sb, taps, bx, by, xl + j, yy, c) ? 0xFF : 0x00;
+            }
+        if (lane == 0) atomicAdd(&g_rechecks2, (unsigned long long)(30 * LC * 2 * OUT));
+        __syncwarp();
+      } else if (nq) {
+        __syncwarp();
+        const unsigned char* sb = fp2_smem + (base - smem0);
+        unsigned cnt = 0;
+        constexpr int PER = 2 * LC * BODY;  // values per record: rows x 2 frames x LC cols
+        const int items = nq * PER;
+        for (int it = lane; it < items; it += 32) {
+          const uint32_t rec = queue[it / PER];
+          const int e = it % PER, st = e / (2 * LC), c = (e / LC) & 1, j = e % LC;
+          const int q0 = int(rec >> 16), L = int((rec >> 8) & 31), nstep = int(rec & 0xFFu);
+          if (st >= nstep || (c == 1 && !has_b)) continue;
+          const int x = bx + 4 * L + j;
+          const int yy = by + q0 + st;
+          if (yy >= H) continue;
+          const bool wv = exact_white(a, sb, taps, bx, by, x, yy, c);
+          o[c * fstride + (long long)yy * OW + x] = wv ? 0xFF : 0x00;
+          ++cnt;
+        }
+        for (int k2 = 16; k2 > 0; k2 >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, k2);
+        if (lane == 0) atomicAdd(&g_rechecks2, (unsigned long long)cnt);
+        __syncwarp();
+      }
+    }
+    __syncwarp();  // the warp's slot reads (and rechecks) are done
+    mbar_arrive_lane0(bar_iir_empty(a, slot), lane);
+    slot += NS;
+    if (slot >= K2) {
+      slot -= K2;
+      par ^= 1u;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+
+template <int OUT, bool HALF>
+__global__ void __launch_bounds__(NTHR, 1)
+    k_chain_pair(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
+  constexpr int R = OUT + 6;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int win = blockIdx.x % a.n_windows, seg = blockIdx.x / a.n_windows;
+  const int strip = win % a.strips, band = win / a.strips;
+  Range rg{0, a.n_frames, a.n_warm, 0, a.state_in, a.state_out, nullptr};
+  {
+    const long long hwl = (long long)a.W * a.H;
+    const int n_out = a.n_frames - a.n_warm;
+    if (a.fix_k) {  // fix-up: re-run every window from the first wrong segment
+      const int k = *a.fix_k;
+      if (k >= a.n_segs) return;
+      rg.out0 = k * a.seg_len;
+      rg.f0 = rg.out0;
+      rg.n = n_out - rg.out0;
+      rg.n_warm = 0;
+      rg.st_in = a.seg_end + (long long)(k - 1) * hwl;
+    } else if (a.n_segs > 1) {
+      rg.out0 = seg * a.seg_len;
+      const int e = min(rg.out0 + a.seg_len, n_out);
+      rg.f0 = max(0, rg.out0 - a.seg_warm);
+      rg.n_warm = rg.out0 - rg.f0;
+      rg.n = e - rg.f0;
+      rg.st_in = nullptr;
+      rg.st_out = seg < a.n_segs - 1 ? (a.seg_end ? a.seg_end + (long long)seg * hwl : nullptr)
+                                     : a.state_out;
+      rg.st_warm = seg > 0 && a.seg_warm_out ? a.seg_warm_out + (long long)seg * hwl : nullptr;
+    }
+    if (rg.n <= 0) return;
+    if (a.fix_k == nullptr && a.n_segs > 1 && blockIdx.x == 0 && tid == 0 && a.seg_k)
+      *a.seg_k = a.n_segs;
+  }
+  // the last band ends exactly at row H - 1 (overlapping the band above it;
+  // both write identical values): the Sobel y clamps sit at fixed steps
+  const int bands = a.n_windows / a.strips;
+  const int x0 = strip * SW, y0 = band == bands - 1 ? max(0, a.H - OUT) : band * OUT;
+  const int bx = x0 - 4, by = y0 - 3;
+  const int tx0 = bx >= 0 ? (bx & ~15) : -((-bx + 15) & ~15);
+  double* taps = reinterpret_cast<double*>(fp2_smem + a.off_taps);
+  if (tid == 0) {
+    for (int i = 0; i < NSF; ++i) {
+      mbar_init(bar_rgb_full(a, i), 1);
+      mbar_init(bar_rgb_empty(a, i), NI);
+    }
+    for (int i = 0; i < K2; ++i) {
+      mbar_init(bar_iir_full(a, i), NI);
+      mbar_init(bar_iir_empty(a, i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < 25) taps[tid] = double(a.p.taps[tid]);
+  if (tid == 0) fp2_rg = rg;
+  __syncthreads();  // the only CTA-wide barrier: roles run decoupled from here
+  (void)R;
+  if (warp < NS)
+    stencil_role<OUT>(a, fp2_rg, warp, lane, bx, by);
+  else
+    iir_role<OUT, HALF>(a, fp2_rg, warp - NS, lane, bx, by, bx - tx0, &tmap, tx0);
+}
+
+// ------------------------------------------------------------------ host
+
+size_t layout(int out_rows, Args* a) {
+  const int R = out_rows + 6;
+  const size_t rgb = size_t(3) * R * BWB;
+  const size_t rgb_stride = (rgb + 127) / 128 * 128;
+  size_t off = NSF * rgb_stride;
+  const size_t off_iir = off;
+  const size_t iir_stride = size_t(R) * PROW;
+  off += K2 * iir_stride;
+  const size_t off_bar = off;
+  off += (2 * NSF + 2 * K2) * 8;
+  const size_t off_taps = (off + 7) / 8 * 8;
+  off = off_taps + 25 * 8;
+  const size_t off_queue = off;
+  off += size_t(NS) * QC * 4;
+  if (a) {
+    a->off_queue = unsigned(off_queue);
+    a->rgb_bytes = unsigned(rgb);
+    a->rgb_stride = unsigned(rgb_stride);
+    a->off_iir = unsigned(off_iir);
+    a->iir_stride = unsigned(iir_stride);
+    a->off_bar = unsigned(off_bar);
+    a->off_taps = unsigned(off_taps);
+  }
+  return off;
+}
+
+using KernelFn = void (*)(CUtensorMap, Args);
+
+#define FP2_OUT_LIST(X) X(6) X(10) X(14) X(18) X(22) X(26) X(29) X(30)
+
+KernelFn kernel_for(int out_rows, bool half) {
+  switch (out_rows) {
+#define FP2_CASE(N) \
+  case N:           \
+    return half ? k_chain_pair<N, true> : k_chain_pair<N, false>;
+    FP2_OUT_LIST(FP2_CASE)
+#undef FP2_CASE
+  }
+  return nullptr;
+}
+
+struct PairPlan {
+  int W = -1, H = -1, dev = -1, frames = -1, force_out = 0, force_segs = 0;
+  bool segs_ok = false;
+  int out_rows = 0, strips = 0, bands = 0, n_segs = 1, seg_len = 0;
+  size_t smem = 0;
+};
+
+constexpr int SEG_WARM = 48;  // IIR warm-up of a time segment (verified + fixed up)
+
+// An SM's time ~ (CTAs it runs) x (window rows) x (frames of a CTA, warm-up
+// frames at ~0.4 of a full frame).  Pick (OUT, segments) minimising the
+// busiest SM's load; ties go to the taller window.
+bool choose(int W, int H, int frames, bool segs_ok, int dev, int force, int force_segs,
+            PairPlan* pp) {
+  int sms = 0, optin = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int strips = (W + SW - 1) / SW;
+  double best = 1e300;
+  const int outs[] = {
+#define FP2_ITEM(N) N,
+      FP2_OUT_LIST(FP2_ITEM)
+#undef FP2_ITEM
+  };
+  const bool dbg = fc_get_knobs()->debug != 0;
+  for (int o : outs) {
+    if (force && o != force) continue;
+    const size_t smem = layout(o, nullptr);
+    if (smem > size_t(optin) || o > H) continue;  // the last band must fit the video
+    cudaError_t e = cudaSuccess;
+    for (int h = 0; h < 2 && e == cudaSuccess; ++h)
+      e = cudaFuncSetAttribute(kernel_for(o, h != 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem));
+    int per_sm = 0;
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(o, true), NTHR, smem);
+    if (dbg)
+      std::fprintf(stderr, "fc_pipe2 choose: out=%d smem=%zu optin=%d err=%s per_sm=%d\n", o,
+                   smem, optin, cudaGetErrorString(e), per_sm);
+    if (e != cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    const long long bands = (H + o - 1) / o;
+    const long long windows = strips * bands;
+    const int max_segs = segs_ok ? 16 : 1;
+    for (int segs = 1; segs <= max_segs; ++segs) {
+      if (force_segs && segs_ok && segs != force_segs) continue;
+      const long long L = (frames + segs - 1) / segs;
+      if (!force_segs && segs > 1 && L < 2 * SEG_WARM) break;
+      if (segs > 1 && L < 2) break;
+      const long long ctas = windows * segs;
+      const long long per_busiest = (ctas + sms - 1) / sms;
+      const double cta_frames = double(L) + (segs > 1 ? 0.4 * SEG_WARM : 0.0);
+      const double cost = double(per_busiest) * (o + 6) * cta_frames * (1.0 - 1e-4 * o);
+      if (cost < best) {
+        best = cost;
+        pp->out_rows = o;
+        pp->strips = strips;
+        pp->bands = int(bands);
+        pp->smem = smem;
+        pp->n_segs = segs;
+        pp->seg_len = int(L);
+      }
+    }
+  }
+  if (best >= 1e300 && force_segs)
+    return choose(W, H, frames, segs_ok, dev, force, 0, pp);
+  if (dbg && best < 1e300)
+    std::fprintf(stderr, "fc_pipe2 choose: -> out=%d segs=%d seg_len=%d\n", pp->out_rows,
+                 pp->n_segs, pp->seg_len);
+  return best < 1e300;
+}
+
+__global__ void k_verify_segments(const float* __restrict__ warm, const float* __restrict__ end,
+                                  long long hw, int n_segs, int* k) {
+  const long long total = (long long)(n_segs - 1) * hw;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = int(i / hw) + 1;
+    const long long px = i % hw;
+    if (__float_as_uint(warm[s * hw + px]) != __float_as_uint(end[(s - 1) * hw + px]))
+      atomicMin(k, s);
+  }
+}
+
+struct SegScratch {
+  float* buf = nullptr;
+  size_t cap = 0;
+  int* k = nullptr;
+};
+
+SegScratch& seg_scratch(int dev, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SegScratch> all;
+  std::lock_guard<std::mutex> lock(mu);
+  return all[{dev, st}];
+}
+
+int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_warm,
+           const float* state_in, float* state_out, void* stream, int pitch, int opitch) {
+  if (d.frames == 0) return 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static thread_local PairPlan cache;
+  const fc_knobs& kn = *fc_get_knobs();
+  const bool segs_ok = state_in == nullptr && n_warm == 0;
+  const int force_out = kn.pipe_oh, force_segs = kn.pipe_segs;
+  if (cache.W != d.width || cache.H != d.height || cache.dev != dev ||
+      cache.frames != d.frames || cache.segs_ok != segs_ok || cache.force_out != force_out ||
+      cache.force_segs != force_segs) {
+    PairPlan pp;
+    if (!choose(d.width, d.height, d.frames - n_warm, segs_ok, dev, force_out, force_segs, &pp))
+      return -1;
+    pp.force_out = force_out;
+    pp.force_segs = force_segs;
+    pp.W = d.width;
+    pp.H = d.height;
+    pp.dev = dev;
+    pp.frames = d.frames;
+    pp.segs_ok = segs_ok;
+    cache = pp;
+  }
+  Args a;
+  std::memset(&a, 0, sizeof a);
+  layout(cache.out_rows, &a);
+  a.out = static_cast<uint8_t*>(out);
+  a.opitch = opitch ? opitch : d.width;
+  a.W = d.width;
+  a.H = d.height;
+  a.n_frames = d.frames;
+  a.n_warm = n_warm;
+  a.strips = cache.strips;
+  a.n_windows = cache.strips * cache.bands;
+  a.n_segs = cache.n_segs;
+  a.seg_len = cache.seg_len;
+  a.seg_warm = kn.pipe_seg_warm > 0 ? kn.pipe_seg_warm : SEG_WARM;
+  const long long hwl = (long long)d.width * d.height;
+  const bool verify = cache.n_segs > 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (verify) {
+    SegScratch& sc = seg_scratch(dev, st);
+    const size_t need = size_t(2 * cache.n_segs) * size_t(hwl);
+    if (need > sc.cap) {
+      if (sc.buf) cudaFree(sc.buf);
+      sc.buf = nullptr;
+      sc.cap = 0;
+      if (cudaMalloc(&sc.buf, need * sizeof(float)) != cudaSuccess) return int(cudaGetLastError());
+      sc.cap = need;
+    }
+    if (!sc.k && cudaMalloc(&sc.k, sizeof(int)) != cudaSuccess) return int(cudaGetLastError());
+    a.seg_end = sc.buf;
+    a.seg_warm_out = sc.buf + size_t(cache.n_segs) * size_t(hwl);
+    a.seg_k = sc.k;
+  }
+  a.state_in = state_in;
+  a.state_out = state_out;
+  a.p = fp;
+  a.skip = kn.pipe_skip;
+  if (kn.band_scale > 0.0f) a.p.band_n *= kn.band_scale;  // tests / diagnostics only
+  CUtensorMap map;
+  if (!rgb_tensor_map(&map, in, d, BWB, cache.out_rows + 6, pitch ? pitch : d.width)) return -1;
+  const int grid = cache.strips * cache.bands * cache.n_segs;
+  KernelFn fn = kernel_for(cache.out_rows, fp.alpha_half != 0);
+  fn<<<grid, NTHR, cache.smem, st>>>(map, a);
+  int rc = int(cudaGetLastError());
+  if (rc == 0 && verify) {
+    k_verify_segments<<<296, 256, 0, st>>>(a.seg_warm_out, a.seg_end, hwl, cache.n_segs,
+                                           a.seg_k);
+    Args f = a;
+    f.fix_k = a.seg_k;
+    f.seg_k = nullptr;
+    fn<<<cache.strips * cache.bands, NTHR, cache.smem, st>>>(map, f);
+    rc = int(cudaGetLastError());
+  }
+  return rc;
+}
+
+}  // namespace fcpipe2
+
+// Same contract as fc_chain_pipe (fc_pipe.cu): -1 when the chain or the
+// layout is outside the certified path.
+extern "C" int fc_chain_pipe2(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                              const fc_stage* sthr, const void* video, int in_type, int gray_in,
+                              void* out, int out_type, fc_dims d, int n_warm,
+                              const float* state_in, float* state_out, int pitch, int opitch,
+                              void* stream) {
+  using namespace fcpipe2;
+  FastParams fp;
+  if (pitch == 0) pitch = d.width;
+  if (opitch == 0) opitch = d.width;
+  if (opitch < d.width || opitch % 4 != 0 || reinterpret_cast<uintptr_t>(out) % 4 != 0)
+    return -1;
+  if (d.height < 6) return -1;
+  if (!fast_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d, pitch, &fp))
+    return -1;
+  return launch(fp, video, out, d, n_warm, state_in, state_out, stream, pitch, opitch);
+}
+
+extern "C" long long fc_pipe2_recheck_count(void) {
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, fcpipe2::g_rechecks2, sizeof v) != cudaSuccess) return -1;
+  return (long long)v;
+}
