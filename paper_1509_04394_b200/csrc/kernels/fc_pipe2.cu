@@ -50,12 +50,17 @@ namespace fcpipe2 {
 
 using namespace fccommon;
 
-constexpr int LC = 4;       // columns per stencil lane
-constexpr int NS = 4;       // stencil warps (one per SM sub-partition)
+#ifndef FP2_LC
+#define FP2_LC 4
+#endif
+constexpr int LC = FP2_LC;  // columns per stencil lane: 4 (one warp per pair) or 2 (two)
+constexpr int WPF = 4 / LC; // stencil warps per frame pair
+constexpr int NPF = 4;      // frame pairs in flight in the stencil
+constexpr int NS = WPF * NPF;  // stencil warps
 constexpr int NI = 8;       // IIR warps (two per SM sub-partition)
 constexpr int NWARP = NS + NI;
 constexpr int NTHR = NWARP * 32;
-constexpr int K2 = NS + 1;  // pair slots: one per stencil warp + one being written
+constexpr int K2 = NPF + 1; // pair slots: one per pair in flight + one being written
 constexpr int NSF = 3;      // TMA RGB frame slots
 constexpr int SW = 120;     // output columns per strip (window 128 = SW + 8)
 constexpr int BWB = 144;    // TMA box row bytes: 128 + worst-case 16-B alignment slack
@@ -142,6 +147,18 @@ __device__ __forceinline__ void sts_pred_u32(uint32_t* p, uint32_t v, bool on) {
       "r"(v), "r"(unsigned(on))
       : "memory");
 }
+__device__ __forceinline__ void st_pred_u16(void* p, uint32_t v, bool on) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.global.b16 [%0], %1;\n}\n" ::"l"(p),
+      "h"(uint16_t(v)), "r"(unsigned(on))
+      : "memory");
+}
+// 0xFF where nd < 0 for two values -> the low 16 bits (sign-replicate PRMT)
+__device__ __forceinline__ uint32_t pack_neg2(float a, float b) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x00FB;" : "=r"(r) : "r"(__float_as_uint(a)), "r"(__float_as_uint(b)));
+  return r;
+}
 __device__ __forceinline__ void st_pred_u32(void* p, uint32_t v, bool on) {
   asm volatile(
       "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.global.b32 [%0], %1;\n}\n" ::"l"(p),
@@ -204,12 +221,6 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
   const float wrm = a.p.wrm, wgm = a.p.wgm, wbm = a.p.wbm;
   const float ia = a.p.ia, ib = a.p.ib;
 
-  int rowo[NR];  // RGB slot byte offset of row p (clamped to the video)
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const int p = min(iw + NI * r, R - 1);
-    rowo[r] = (clampi(by + p, 0, H - 1) - by) * BWB;
-  }
   int coloff = xoff + 4 * lane;
   // magic-float PRMT selectors: byte j of the word, or (lanes left / right
   // of the video) the edge byte in every cell
@@ -220,19 +231,30 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
 #pragma unroll
     for (int j = 0; j < 4; ++j) msel[j] = 0x7440u + unsigned(edge & 3);
   }
+  int rowo[NR];  // RGB slot byte offset of the lane's word in row p (clamped row)
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int p = min(iw + NI * r, R - 1);
+    rowo[r] = (clampi(by + p, 0, H - 1) - by) * BWB + coloff;
+  }
   const unsigned so0 = chunk_off(2 * lane), so1 = chunk_off(2 * lane + 1);
 
-  float y[NR][4];  // exact IIR state of the lane's cells
+  // q[r][j] = {IIR of frame A of the current pair, exact IIR state}: the state
+  // lives in .y; a pair computes .x = IIR(A) from .y, then .y = IIR(B) from .x,
+  // and stores {q(c0), q(c1)} as one 16-byte chunk (no register moves)
+  float2 q[NR][4];
   const bool fresh = rg.st_in == nullptr;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const int p = iw + NI * r;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      q[r][j].x = 0.0f;
       if (fresh || p >= R)
-        y[r][j] = 0.0f;
+        q[r][j].y = 0.0f;
       else
-        y[r][j] = rg.st_in[(long long)clampi(by + p, 0, H - 1) * W + clampi(xl + j, 0, W - 1)];
+        q[r][j].y =
+            rg.st_in[(long long)clampi(by + p, 0, H - 1) * W + clampi(xl + j, 0, W - 1)];
     }
   }
   // the lane's output cells (window rows 3 .. OUT + 2) -> a state plane
@@ -243,7 +265,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
       const int p = iw + NI * r;
       if (p < 3 || p > OUT + 2 || by + p >= H) continue;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dst[(long long)(by + p) * W + xl + j] = y[r][j];
+      for (int j = 0; j < 4; ++j) dst[(long long)(by + p) * W + xl + j] = q[r][j].y;
     }
   };
 
@@ -289,7 +311,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
       uint32_t w[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
-        w[c] = *reinterpret_cast<const uint32_t*>(f + c * cplane + rowo[r] + coloff);
+        w[c] = *reinterpret_cast<const uint32_t*>(f + c * cplane + rowo[r]);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const float2 pr = wprod(f2(magic_rs(w[0], k4b, msel[2 * h]),
@@ -308,75 +330,42 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
       rpar ^= 1u;
     }
   };
-  // IIR update of cell (r, j) with its gray value gj (simulator.cpp:57-62):
+  // IIR update y' from y and the cell's gray value x (simulator.cpp:57-62):
   // HALF: fl(0.5 x + fl(0.5 y)) == FMA(0.5, y, 0.5 x) (x = gray > 0 dwarfs
   // any rounding of 0.5 y; x = 0 gives fl(0.5 y) either way); otherwise
-  // fl(fl(a x) + fl(b y)) in scalar .rn ops.  First frame: y = gray.
+  // fl(fl(a x) + fl(b y)) in scalar .rn ops.  First frame: y' = gray.
   auto upd = [&](float yo, float gj, bool first) -> float {
     if (HALF) return first ? __fadd_rn(gj, gj) : __fmaf_rn(0.5f, yo, gj);
     return first ? gj : __fadd_rn(__fmul_rn(ia, gj), __fmul_rn(ib, yo));
   };
-  auto step_frame = [&](int t, float (&yn)[NR][4], const float (&yo)[NR][4]) {
+  // frame t into component A (.x, from the state .y) or B (.y, from .x)
+  auto frame = [&](int t, bool to_b) {
     float2 g[NR][2];
     gray(t, g);
+    if (a.skip & 1) return;
     const bool first = fresh && t == 0;
-    if (a.skip & 1) {
-#pragma unroll
-      for (int r = 0; r < NR; ++r)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) yn[r][j] = yo[r][j];
-      return;
-    }
-    if (first) {
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        yn[r][0] = upd(yo[r][0], g[r][0].x, true);
-        yn[r][1] = upd(yo[r][1], g[r][0].y, true);
-        yn[r][2] = upd(yo[r][2], g[r][1].x, true);
-        yn[r][3] = upd(yo[r][3], g[r][1].y, true);
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        yn[r][0] = upd(yo[r][0], g[r][0].x, false);
-        yn[r][1] = upd(yo[r][1], g[r][0].y, false);
-        yn[r][2] = upd(yo[r][2], g[r][1].x, false);
-        yn[r][3] = upd(yo[r][3], g[r][1].y, false);
-      }
-    }
-  };
-
-  // warm-up frames: state only
-  for (int t = 0; t < n_warm; ++t) {
-    float yn[NR][4];
-    step_frame(t, yn, y);
 #pragma unroll
     for (int r = 0; r < NR; ++r)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) y[r][j] = yn[r][j];
-    if (t == n_warm - 1) write_state(rg.st_warm);
-  }
-  // output frames in pairs (A = t, B = t + 1; an odd tail stores {A, A})
-  for (int k = 0; k < n_out; k += 2) {
-    const int t = n_warm + k;
-    float ya[NR][4];
-    step_frame(t, ya, y);
-    if (k + 1 < n_out) {
-      step_frame(t + 1, y, ya);
-    } else {
-#pragma unroll
-      for (int r = 0; r < NR; ++r)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) y[r][j] = ya[r][j];
-    }
+      for (int j = 0; j < 4; ++j) {
+        const float gj = (j & 1) ? g[r][j >> 1].y : g[r][j >> 1].x;
+        if (to_b)
+          q[r][j].y = upd(q[r][j].x, gj, false);  // B never starts a recurrence
+        else if (first)
+          q[r][j].x = upd(q[r][j].y, gj, true);
+        else
+          q[r][j].x = upd(q[r][j].y, gj, false);
+      }
+  };
+  auto store_pair = [&]() {
     wait_phase(bar_iir_empty(a, islot), ipar ^ 1u);
     const unsigned base = smem0 + a.off_iir + islot * a.iir_stride;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const int p = iw + NI * r;
       if (p >= R) continue;
-      sts128f(base + p * PROW + so0, ya[r][0], y[r][0], ya[r][1], y[r][1]);
-      sts128f(base + p * PROW + so1, ya[r][2], y[r][2], ya[r][3], y[r][3]);
+      sts128f(base + p * PROW + so0, q[r][0].x, q[r][0].y, q[r][1].x, q[r][1].y);
+      sts128f(base + p * PROW + so1, q[r][2].x, q[r][2].y, q[r][3].x, q[r][3].y);
     }
     __syncwarp();  // the warp's stores precede the release arrive
     mbar_arrive_lane0(bar_iir_full(a, islot), lane);
@@ -384,6 +373,31 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
       islot = 0;
       ipar ^= 1u;
     }
+  };
+
+  // warm-up frames: state only (A then copy to the state)
+  for (int t = 0; t < n_warm; ++t) {
+    frame(t, false);
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q[r][j].y = q[r][j].x;
+    if (t == n_warm - 1) write_state(rg.st_warm);
+  }
+  // output frames in pairs (A = t, B = t + 1)
+  int k = 0;
+  for (; k + 1 < n_out; k += 2) {
+    frame(n_warm + k, false);
+    frame(n_warm + k + 1, true);
+    store_pair();
+  }
+  if (k < n_out) {  // odd tail: {A, A}
+    frame(n_warm + k, false);
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q[r][j].y = q[r][j].x;
+    store_pair();
   }
   write_state(rg.st_out);
 }
@@ -448,7 +462,12 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
   const float g0 = a.p.g0, g1 = a.p.g1;
   const double* taps = reinterpret_cast<const double*>(fp2_smem + a.off_taps);
   uint32_t* queue = reinterpret_cast<uint32_t*>(fp2_smem + a.off_queue) + sw * QC;
-  const int k = 2 * lane;       // the lane's first chunk
+  // LC = 4: warp w alone on pair w, lane columns 4L .. 4L+3 (outputs: lanes
+  // 1..30); LC = 2: warps 2f, 2f+1 share pair f, side s owns chunks
+  // k = 1 + 30 s + L (columns 2k, 2k+1; outputs: lanes 1..30 = columns
+  // 4..63 / 64..123)
+  const int fp0 = sw / WPF, side = sw % WPF;
+  const int k = LC == 2 ? 1 + 30 * side + lane : 2 * lane;  // the lane's first chunk
   const int xl = bx + 2 * k;    // video column of the lane's first cell
   const bool outl = lane >= 1 && lane <= 30 && xl < W;
   const bool xlo = xl == 0, xhi = xl + LC - 1 == W - 1;  // Sobel x clamps (video edges)
@@ -460,9 +479,9 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
   const int OW = a.opitch;
   const long long fstride = (long long)OW * H;
 
-  int slot = sw % K2;
-  unsigned par = (sw / K2) & 1u;
-  for (int u = sw; u < n_pairs; u += NS) {
+  int slot = fp0 % K2;
+  unsigned par = (fp0 / K2) & 1u;
+  for (int u = fp0; u < n_pairs; u += NPF) {
     wait_phase(bar_iir_full(a, slot), par);
     const unsigned base = smem0 + a.off_iir + slot * a.iir_stride;
     const bool has_b = 2 * u + 1 < n_out;
@@ -529,8 +548,13 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
           const float2 ngx = f2(-gx.x, -gx.y), ngy = f2(-gy.x, -gy.y);
           dm[j] = __ffma2_rn(ngx, gx, __ffma2_rn(ngy, gy, splat(mlo)));
         }
-        st_pred_u32(ox, pack_neg(dm[0].x, dm[1].x, dm[2].x, dm[3].x), oka);
-        st_pred_u32(ox + fstride, pack_neg(dm[0].y, dm[1].y, dm[2].y, dm[3].y), okb);
+        if constexpr (LC == 4) {
+          st_pred_u32(ox, pack_neg(dm[0].x, dm[1].x, dm[2].x, dm[3].x), oka);
+          st_pred_u32(ox + fstride, pack_neg(dm[0].y, dm[1].y, dm[2].y, dm[3].y), okb);
+        } else {
+          st_pred_u16(ox, pack_neg2(dm[0].x, dm[1].x), oka);
+          st_pred_u16(ox + fstride, pack_neg2(dm[0].y, dm[1].y), okb);
+        }
         ox += OW;
 #pragma unroll
         for (int j = 0; j < LC; ++j) amin = min3abs(amin, dm[j].x, dm[j].y);
@@ -611,7 +635,7 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
           const int e = it % PER, st = e / (2 * LC), c = (e / LC) & 1, j = e % LC;
           const int q0 = int(rec >> 16), L = int((rec >> 8) & 31), nstep = int(rec & 0xFFu);
           if (st >= nstep || (c == 1 && !has_b)) continue;
-          const int x = bx + 4 * L + j;
+          const int x = bx + 2 * (LC == 2 ? 1 + 30 * side + L : 2 * L) + j;
           const int yy = by + q0 + st;
           if (yy >= H) continue;
           const bool wv = exact_white(a, sb, taps, bx, by, x, yy, c);
@@ -625,7 +649,7 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
     }
     __syncwarp();  // the warp's slot reads (and rechecks) are done
     mbar_arrive_lane0(bar_iir_empty(a, slot), lane);
-    slot += NS;
+    slot += NPF;
     if (slot >= K2) {
       slot -= K2;
       par ^= 1u;
@@ -683,7 +707,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     }
     for (int i = 0; i < K2; ++i) {
       mbar_init(bar_iir_full(a, i), NI);
-      mbar_init(bar_iir_empty(a, i), 1);
+      mbar_init(bar_iir_empty(a, i), WPF);  // the pair's stencil warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
