@@ -62,6 +62,15 @@ constexpr int NWARP = NS + NI;
 constexpr int NTHR = NWARP * 32;
 constexpr int K2 = NPF + 1; // pair slots: one per pair in flight + one being written
 constexpr int NSF = 3;      // TMA RGB frame slots
+#ifndef FP2_NAMED
+#define FP2_NAMED 1  // IIR <-> stencil hand-offs on named barriers (no polling)
+#endif
+#ifndef FP2_STENCIL_HI
+#define FP2_STENCIL_HI 1  // stencil warps at the high warp ids: scheduler priority (+3.7 %)
+#endif
+// named barriers: 1 + slot = "slot empty", 1 + K2 + slot = "slot full"; the
+// pair's stencil warp(s) and every IIR warp take part
+constexpr unsigned NB_THREADS = (NI + WPF) * 32;
 constexpr int SW = 120;     // output columns per strip (window 128 = SW + 8)
 constexpr int BWB = 144;    // TMA box row bytes: 128 + worst-case 16-B alignment slack
 constexpr int PROW = 1024;  // bytes per window row of a pair slot
@@ -118,6 +127,12 @@ __device__ __forceinline__ uint64_t* bar_iir_empty(const Args& a, int i) {
   return bar_at(a, 2 * NSF + K2 + i);
 }
 
+__device__ __forceinline__ void nb_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NB_THREADS) : "memory");
+}
+__device__ __forceinline__ void nb_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(NB_THREADS) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -357,8 +372,13 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
           q[r][j].x = upd(q[r][j].y, gj, false);
       }
   };
+  int n_stored = 0;
   auto store_pair = [&]() {
-    wait_phase(bar_iir_empty(a, islot), ipar ^ 1u);
+    if (FP2_NAMED) {
+      if (n_stored >= K2) nb_sync(1 + islot);  // the stencil released pair n_stored - K2
+    } else {
+      wait_phase(bar_iir_empty(a, islot), ipar ^ 1u);
+    }
     const unsigned base = smem0 + a.off_iir + islot * a.iir_stride;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
@@ -367,8 +387,13 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
       sts128f(base + p * PROW + so0, q[r][0].x, q[r][0].y, q[r][1].x, q[r][1].y);
       sts128f(base + p * PROW + so1, q[r][2].x, q[r][2].y, q[r][3].x, q[r][3].y);
     }
-    __syncwarp();  // the warp's stores precede the release arrive
-    mbar_arrive_lane0(bar_iir_full(a, islot), lane);
+    if (FP2_NAMED) {
+      nb_arrive(1 + K2 + islot);
+    } else {
+      __syncwarp();  // the warp's stores precede the release arrive
+      mbar_arrive_lane0(bar_iir_full(a, islot), lane);
+    }
+    ++n_stored;
     if (++islot == K2) {
       islot = 0;
       ipar ^= 1u;
@@ -482,7 +507,10 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
   int slot = fp0 % K2;
   unsigned par = (fp0 / K2) & 1u;
   for (int u = fp0; u < n_pairs; u += NPF) {
-    wait_phase(bar_iir_full(a, slot), par);
+    if (FP2_NAMED)
+      nb_sync(1 + K2 + slot);
+    else
+      wait_phase(bar_iir_full(a, slot), par);
     const unsigned base = smem0 + a.off_iir + slot * a.iir_stride;
     const bool has_b = 2 * u + 1 < n_out;
     unsigned char* o = a.out + (long long)(rg.out0 + 2 * u) * fstride;
@@ -647,8 +675,12 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
         __syncwarp();
       }
     }
-    __syncwarp();  // the warp's slot reads (and rechecks) are done
-    mbar_arrive_lane0(bar_iir_empty(a, slot), lane);
+    if (FP2_NAMED) {
+      if (u + K2 < n_pairs) nb_arrive(1 + slot);  // the IIR warps wait for it
+    } else {
+      __syncwarp();  // the warp's slot reads (and rechecks) are done
+      mbar_arrive_lane0(bar_iir_empty(a, slot), lane);
+    }
     slot += NPF;
     if (slot >= K2) {
       slot -= K2;
@@ -715,10 +747,12 @@ __global__ void __launch_bounds__(NTHR, 1)
   if (tid == 0) fp2_rg = rg;
   __syncthreads();  // the only CTA-wide barrier: roles run decoupled from here
   (void)R;
-  if (warp < NS)
-    stencil_role<OUT>(a, fp2_rg, warp, lane, bx, by);
+  const int sw = FP2_STENCIL_HI ? warp - NI : warp;  // stencil warp index (or < 0)
+  if (sw >= 0 && sw < NS)
+    stencil_role<OUT>(a, fp2_rg, sw, lane, bx, by);
   else
-    iir_role<OUT, HALF>(a, fp2_rg, warp - NS, lane, bx, by, bx - tx0, &tmap, tx0);
+    iir_role<OUT, HALF>(a, fp2_rg, FP2_STENCIL_HI ? warp : warp - NS, lane, bx, by, bx - tx0,
+                        &tmap, tx0);
 }
 
 // ------------------------------------------------------------------ host
