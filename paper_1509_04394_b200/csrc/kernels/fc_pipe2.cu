@@ -50,11 +50,16 @@ namespace fcpipe2 {
 
 using namespace fccommon;
 
-#ifndef FP2_LC
-#define FP2_LC 4
+#ifndef FP2_SPLIT
+#define FP2_SPLIT 1  // stencil warps per frame pair (2: row halves of the window + setmaxnreg;
+                     // measured 1.06-1.19 ms vs 0.80 ms: the IIR warps fall behind)
 #endif
-constexpr int LC = FP2_LC;  // columns per stencil lane: 4 (one warp per pair) or 2 (two)
-constexpr int WPF = 4 / LC; // stencil warps per frame pair
+#ifndef FP2_SREG
+#define FP2_SREG 160  // setmaxnreg (SPLIT 2): stencil / IIR warpgroup registers
+#define FP2_IREG 96
+#endif
+constexpr int LC = 4;       // columns per stencil lane
+constexpr int WPF = FP2_SPLIT;  // stencil warps per frame pair
 constexpr int NPF = 4;      // frame pairs in flight in the stencil
 constexpr int NS = WPF * NPF;  // stencil warps
 constexpr int NI = 8;       // IIR warps (two per SM sub-partition)
@@ -316,7 +321,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
 
   // gray of frame t for every cell: g[r][h] = {gray(col 2h), gray(col 2h+1)}
   // (x 0.5 when HALF: alpha folded into the weights)
-  auto gray = [&](int t, float2 (&g)[NR][2]) {
+  auto gray = [&](int t, auto&& row_fn) {
     if (prod && t + NSF - 1 < n) issue(t + NSF - 1);
     wait_phase(bar_rgb_full(a, rslot), rpar);
     const unsigned char* f = fp2_smem + rslot * a.rgb_stride;
@@ -324,6 +329,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
     for (int r = 0; r < NR; ++r) {
       if (iw + NI * r >= R) continue;
       uint32_t w[3];
+      float2 g[2];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
         w[c] = *reinterpret_cast<const uint32_t*>(f + c * cplane + rowo[r]);
@@ -335,8 +341,9 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
                                    magic_rs(w[1], k4b, msel[2 * h + 1])), wg, wgm);
         const float2 pb = wprod(f2(magic_rs(w[2], k4b, msel[2 * h]),
                                    magic_rs(w[2], k4b, msel[2 * h + 1])), wb, wbm);
-        g[r][h] = __fadd2_rn(__fadd2_rn(pr, pg), pb);  // (wr r + wg g) + wb b
+        g[h] = __fadd2_rn(__fadd2_rn(pr, pg), pb);  // (wr r + wg g) + wb b
       }
+      row_fn(r, g);  // consume the row at once (few live registers)
     }
     __syncwarp();  // the warp's RGB reads are done (values in registers)
     mbar_arrive_lane0(bar_rgb_empty(a, rslot), lane);
@@ -355,15 +362,13 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
   };
   // frame t into component A (.x, from the state .y) or B (.y, from .x)
   auto frame = [&](int t, bool to_b) {
-    float2 g[NR][2];
-    gray(t, g);
-    if (a.skip & 1) return;
     const bool first = fresh && t == 0;
-#pragma unroll
-    for (int r = 0; r < NR; ++r)
+    const bool skip = (a.skip & 1) != 0;
+    gray(t, [&](int r, const float2 (&g)[2]) {
+      if (skip) return;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float gj = (j & 1) ? g[r][j >> 1].y : g[r][j >> 1].x;
+        const float gj = (j & 1) ? g[j >> 1].y : g[j >> 1].x;
         if (to_b)
           q[r][j].y = upd(q[r][j].x, gj, false);  // B never starts a recurrence
         else if (first)
@@ -371,6 +376,7 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
         else
           q[r][j].x = upd(q[r][j].y, gj, false);
       }
+    });
   };
   int n_stored = 0;
   auto store_pair = [&]() {
@@ -478,8 +484,14 @@ using ic = std::integral_constant<int, N>;
 // rows) and recomputed exactly after the march.
 template <int OUT>
 __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int sw, int lane,
-                                             int bx, int by) {
-  constexpr int NP = OUT + 6;
+                                             int bx, int by0) {
+  // SPLIT 2: warp sw marches the top (sw < NPF) or bottom half of the
+  // window's output rows (ceil(OUT/2) each; with OUT odd the middle row is
+  // computed by both and stored twice with identical values)
+  constexpr int OT = WPF == 2 ? (OUT + 1) / 2 : OUT;  // output rows of this warp
+  constexpr int NP = OT + 6;
+  const int r0 = sw >= NPF ? OUT - OT : 0;  // first window row of this warp's march
+  const int by = by0 + r0;                  // origin of the march
   const int W = a.W, H = a.H;
   const int n_out = rg.n - rg.n_warm;
   const int n_pairs = (n_out + 1) / 2;
@@ -487,12 +499,9 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
   const float g0 = a.p.g0, g1 = a.p.g1;
   const double* taps = reinterpret_cast<const double*>(fp2_smem + a.off_taps);
   uint32_t* queue = reinterpret_cast<uint32_t*>(fp2_smem + a.off_queue) + sw * QC;
-  // LC = 4: warp w alone on pair w, lane columns 4L .. 4L+3 (outputs: lanes
-  // 1..30); LC = 2: warps 2f, 2f+1 share pair f, side s owns chunks
-  // k = 1 + 30 s + L (columns 2k, 2k+1; outputs: lanes 1..30 = columns
-  // 4..63 / 64..123)
-  const int fp0 = sw / WPF, side = sw % WPF;
-  const int k = LC == 2 ? 1 + 30 * side + lane : 2 * lane;  // the lane's first chunk
+  // lane columns 4L .. 4L+3 (outputs: lanes 1..30)
+  const int fp0 = sw % NPF;
+  const int k = 2 * lane;  // the lane's first chunk
   const int xl = bx + 2 * k;    // video column of the lane's first cell
   const bool outl = lane >= 1 && lane <= 30 && xl < W;
   const bool xlo = xl == 0, xhi = xl + LC - 1 == W - 1;  // Sobel x clamps (video edges)
@@ -511,7 +520,8 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
       nb_sync(1 + K2 + slot);
     else
       wait_phase(bar_iir_full(a, slot), par);
-    const unsigned base = smem0 + a.off_iir + slot * a.iir_stride;
+    const unsigned sbase = smem0 + a.off_iir + slot * a.iir_stride;  // slot row 0
+    const unsigned base = sbase + r0 * PROW;                         // march row 0
     const bool has_b = 2 * u + 1 < n_out;
     unsigned char* o = a.out + (long long)(rg.out0 + 2 * u) * fstride;
     unsigned char* ox = o + (long long)(by + 3) * OW + xl;  // frame A, window row 3
@@ -576,13 +586,8 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
           const float2 ngx = f2(-gx.x, -gx.y), ngy = f2(-gy.x, -gy.y);
           dm[j] = __ffma2_rn(ngx, gx, __ffma2_rn(ngy, gy, splat(mlo)));
         }
-        if constexpr (LC == 4) {
-          st_pred_u32(ox, pack_neg(dm[0].x, dm[1].x, dm[2].x, dm[3].x), oka);
-          st_pred_u32(ox + fstride, pack_neg(dm[0].y, dm[1].y, dm[2].y, dm[3].y), okb);
-        } else {
-          st_pred_u16(ox, pack_neg2(dm[0].x, dm[1].x), oka);
-          st_pred_u16(ox + fstride, pack_neg2(dm[0].y, dm[1].y), okb);
-        }
+        st_pred_u32(ox, pack_neg(dm[0].x, dm[1].x, dm[2].x, dm[3].x), oka);
+        st_pred_u32(ox + fstride, pack_neg(dm[0].y, dm[1].y, dm[2].y, dm[3].y), okb);
         ox += OW;
 #pragma unroll
         for (int j = 0; j < LC; ++j) amin = min3abs(amin, dm[j].x, dm[j].y);
@@ -640,21 +645,21 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
         // queue overflow (adversarial input): the exact decision for every
         // output pixel of this warp's pair
         __syncwarp();
-        const unsigned char* sb = fp2_smem + (base - smem0);
+        const unsigned char* sb = fp2_smem + (sbase - smem0);
         if (outl)
-          for (int q = 3; q <= OUT + 2; ++q)
+          for (int q = 3; q <= OT + 2; ++q)
             for (int c = 0; c < (has_b ? 2 : 1); ++c) {
               const int yy = by + q;
               if (yy >= H) continue;
               for (int j = 0; j < LC; ++j)
                 o[c * fstride + (long long)yy * OW + xl + j] =
-                    exact_white(a, sb, taps, bx, by, xl + j, yy, c) ? 0xFF : 0x00;
+                    exact_white(a, sb, taps, bx, by0, xl + j, yy, c) ? 0xFF : 0x00;
             }
-        if (lane == 0) atomicAdd(&g_rechecks2, (unsigned long long)(30 * LC * 2 * OUT));
+        if (lane == 0) atomicAdd(&g_rechecks2, (unsigned long long)(30 * LC * 2 * OT));
         __syncwarp();
       } else if (nq) {
         __syncwarp();
-        const unsigned char* sb = fp2_smem + (base - smem0);
+        const unsigned char* sb = fp2_smem + (sbase - smem0);
         unsigned cnt = 0;
         constexpr int PER = 2 * LC * BODY;  // values per record: rows x 2 frames x LC cols
         const int items = nq * PER;
@@ -663,10 +668,10 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
           const int e = it % PER, st = e / (2 * LC), c = (e / LC) & 1, j = e % LC;
           const int q0 = int(rec >> 16), L = int((rec >> 8) & 31), nstep = int(rec & 0xFFu);
           if (st >= nstep || (c == 1 && !has_b)) continue;
-          const int x = bx + 2 * (LC == 2 ? 1 + 30 * side + L : 2 * L) + j;
+          const int x = bx + 4 * L + j;
           const int yy = by + q0 + st;
           if (yy >= H) continue;
-          const bool wv = exact_white(a, sb, taps, bx, by, x, yy, c);
+          const bool wv = exact_white(a, sb, taps, bx, by0, x, yy, c);
           o[c * fstride + (long long)yy * OW + x] = wv ? 0xFF : 0x00;
           ++cnt;
         }
@@ -748,11 +753,14 @@ __global__ void __launch_bounds__(NTHR, 1)
   __syncthreads();  // the only CTA-wide barrier: roles run decoupled from here
   (void)R;
   const int sw = FP2_STENCIL_HI ? warp - NI : warp;  // stencil warp index (or < 0)
-  if (sw >= 0 && sw < NS)
+  if (sw >= 0 && sw < NS) {
+    if (WPF == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(FP2_SREG));
     stencil_role<OUT>(a, fp2_rg, sw, lane, bx, by);
-  else
+  } else {
+    if (WPF == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(FP2_IREG));
     iir_role<OUT, HALF>(a, fp2_rg, FP2_STENCIL_HI ? warp : warp - NS, lane, bx, by, bx - tx0,
                         &tmap, tx0);
+  }
 }
 
 // ------------------------------------------------------------------ host

@@ -12,7 +12,9 @@ for (W, H, F) in [(800, 600, 24), (192, 432, 31), (132, 40, 9)]:
 bad += run(800, 600, 20, 2, th=20.0, band=64.0)[3]
 ms = sorted(timeit(800, 600, 1000, 2) for _ in range(3))[1]
 ms2 = timeit(2048, 2048, 200, 2)
-print(f"mismatches {bad}  800x600x1000 {ms:.3f} ms {1e6/ms:.0f} fps  2048x2048x200 {ms2:.3f} ms {2e5/ms2:.0f} fps", flush=True)
+ex = run(800, 600, 64, 2, check=False)[0]
+rc = ex.describe().get("exact_rechecks_total")
+print(f"mismatches {bad}  800x600x1000 {ms:.3f} ms {1e6/ms:.0f} fps  2048x2048x200 {ms2:.3f} ms {2e5/ms2:.0f} fps  rechecks(total so far) {rc}", flush=True)
 '''
 for rnd in range(2):
     for lib in libs:
