@@ -143,6 +143,31 @@ def cpu_reference_rate(W, H, sample_frames, seed=1234):
     return sample_frames / dt, cores, kind, f"{W}x{H}x{sample_frames} u8 hash video"
 
 
+def cpu_reference_single_core(sample_frames=24):
+    """the reference's unmodified run_sequential
+    (simulator.cpp:158-177, oracle/_ref) on ONE thread at config 1's frame size
+    on the reference's own marker scene (synth.cpp:35-78 through the FPVD
+    codec), over a bounded sample of frames."""
+    from oracle import oracle as O
+    from paper_1509_04394_b200.fuseplan import spec_chain
+    if not O.ref_available():
+        return None
+    W, H = 192, 432
+    markers = [{"x": 20.0, "y": 30.0, "vx": 1.0, "vy": 0.0, "radius": 3.0, "intensity": 255.0},
+               {"x": 100.0, "y": 200.0, "vx": 0.5, "vy": 0.5, "radius": 3.0,
+                "intensity": 255.0}]
+    video = O.ref_synth_u8({"width": W, "height": H, "frames": sample_frames, "channels": 4,
+                            "noise_sigma": 8.0, "seed": 1234, "markers": markers})
+    pipe = json.dumps(spec_chain(W, H, sample_frames, kalman=True))
+    t0 = time.perf_counter()
+    O.ref_run_sequential(pipe, video)
+    dt = time.perf_counter() - t0
+    return {"value": sample_frames / dt, "unit": "frames/s", "cores": 1, "kind": "reference",
+            "mpix_per_s": sample_frames * W * H / dt / 1e6,
+            "sample": f"config 1 frame size {W}x{H}x{sample_frames}, reference marker scene "
+                      "(synth_video + FPVD u8), run_sequential on one thread"}
+
+
 def check_parity(pipe_spec, video, mask, warm, chunk=100):
     """Every frame of the timed mask against the streaming C restatement of
     run_sequential (oracle/fusechain_oracle.c, pinned to the reference build by
@@ -461,7 +486,7 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         r, cores, kind, samp = cpu_reference_rate(W, H, 12)
         cpu = {"value": r, "unit": "frames/s", "cores": cores, "kind": kind,
-               "sample": samp}
+               "sample": samp, "single_core_cfg1": cpu_reference_single_core()}
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

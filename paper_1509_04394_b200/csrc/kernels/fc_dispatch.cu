@@ -54,6 +54,7 @@ extern "C" void fc_knobs_from_env(fc_knobs* k) {
   k->f12_stream = std::getenv("FUSEPLAN_F12_STREAM") != nullptr;
   k->f12_legacy = std::getenv("FUSEPLAN_F12_LEGACY") != nullptr;
   k->pipe_impl = env_int("FUSEPLAN_PIPE_IMPL");
+  k->pipe_out = env_int("FUSEPLAN_PIPE_OUT");
 }
 
 extern "C" void fc_set_knobs(const fc_knobs* k) {

@@ -175,6 +175,7 @@ typedef struct {
   int f12_stream;     /* FUSEPLAN_F12_STREAM: force the streaming F12 kernel */
   int f12_legacy;     /* FUSEPLAN_F12_LEGACY: the per-pixel F12 kernel */
   int pipe_impl;      /* FUSEPLAN_PIPE_IMPL: 0 auto, 1 row-pair pipe, 2 frame-pair pipe */
+  int pipe_out;       /* FUSEPLAN_PIPE_OUT: force the frame-pair window's output rows */
 } fc_knobs;
 
 void fc_knobs_from_env(fc_knobs* k);

@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(NTHR, 1)
                                      : a.state_out;
       rg.st_warm = seg > 0 && a.seg_warm_out ? a.seg_warm_out + (long long)seg * hwl : nullptr;
     }
-    if (rg.n <= 0) return;
+    if (rg.n <= 0 || rg.n_warm > rg.n) return;
     if (a.fix_k == nullptr && a.n_segs > 1 && blockIdx.x == 0 && tid == 0 && a.seg_k)
       *a.seg_k = a.n_segs;  // verification result slot (reset before verify runs)
   }
@@ -1079,9 +1079,13 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, bool src_f32, int f
     for (int segs = 1; segs <= max_segs; ++segs) {
       if (force_segs && segs_ok && segs != force_segs) continue;
       const long long L = (frames + segs - 1) / segs;
+      // segments that actually hold frames (16 asked of 161 frames: L = 11,
+      // 15 segments); an empty trailing segment would march warm-up frames
+      // past the end of its range
+      const int nseg = int((frames + L - 1) / L);
       if (!force_segs && segs > 1 && !src_f32 && L < 2 * SEG_WARM) break;  // warm-up dominates
       if (segs > 1 && L < 2) break;
-      const long long ctas = windows * segs;
+      const long long ctas = windows * nseg;
       const long long per_busiest = (ctas + sms - 1) / sms;
       const double cta_frames = double(L) + (segs > 1 ? warm_cost * SEG_WARM : 0.0);
       const double cost = double(per_busiest) * (oh + 6) * cta_frames * (1.0 - 1e-4 * oh);
@@ -1091,7 +1095,7 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, bool src_f32, int f
         pp->strips = strips;
         pp->bands = int(bands);
         pp->smem = smem;
-        pp->n_segs = segs;
+        pp->n_segs = nseg;
         pp->seg_len = int(L);
       }
     }

@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(NTHR, 1)
                                      : a.state_out;
       rg.st_warm = seg > 0 && a.seg_warm_out ? a.seg_warm_out + (long long)seg * hwl : nullptr;
     }
-    if (rg.n <= 0) return;
+    if (rg.n <= 0 || rg.n_warm > rg.n) return;
     if (a.fix_k == nullptr && a.n_segs > 1 && blockIdx.x == 0 && tid == 0 && a.seg_k)
       *a.seg_k = a.n_segs;
   }
@@ -855,9 +855,13 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, int force, int forc
     for (int segs = 1; segs <= max_segs; ++segs) {
       if (force_segs && segs_ok && segs != force_segs) continue;
       const long long L = (frames + segs - 1) / segs;
+      // segments that actually hold frames (16 asked of 161 frames: L = 11,
+      // 15 segments); an empty trailing segment would march warm-up frames
+      // past the end of its range
+      const int nseg = int((frames + L - 1) / L);
       if (!force_segs && segs > 1 && L < 2 * SEG_WARM) break;
       if (segs > 1 && L < 2) break;
-      const long long ctas = windows * segs;
+      const long long ctas = windows * nseg;
       const long long per_busiest = (ctas + sms - 1) / sms;
       const double cta_frames = double(L) + (segs > 1 ? 0.4 * SEG_WARM : 0.0);
       const double cost = double(per_busiest) * (o + 6) * cta_frames * (1.0 - 1e-4 * o);
@@ -867,7 +871,7 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, int force, int forc
         pp->strips = strips;
         pp->bands = int(bands);
         pp->smem = smem;
-        pp->n_segs = segs;
+        pp->n_segs = nseg;
         pp->seg_len = int(L);
       }
     }
@@ -913,7 +917,7 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
   static thread_local PairPlan cache;
   const fc_knobs& kn = *fc_get_knobs();
   const bool segs_ok = state_in == nullptr && n_warm == 0;
-  const int force_out = kn.pipe_oh, force_segs = kn.pipe_segs;
+  const int force_out = kn.pipe_out, force_segs = kn.pipe_segs;
   if (cache.W != d.width || cache.H != d.height || cache.dev != dev ||
       cache.frames != d.frames || cache.segs_ok != segs_ok || cache.force_out != force_out ||
       cache.force_segs != force_segs) {

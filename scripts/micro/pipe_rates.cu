@@ -68,6 +68,56 @@ __device__ __forceinline__ void step(float* a, uint32_t* u, float x, float y, ui
                    : "r"(s + 16 * i));
     if (OP == 18) asm volatile("fma.rn.f32 %0, %0, %0, %1;" : "+f"(a[i]) : "f"(y));  // RRR, 2 distinct
     if (OP == 19) asm volatile("sub.f32 %0, %1, %0;" : "+f"(a[i]) : "f"(x));
+    if (OP == 20 && (i & 1) == 0)  // DFMA on a register pair
+      asm volatile(
+          "{.reg .f64 p, q;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %3};\n"
+          " fma.rn.f64 p, p, q, q;\n mov.b64 {%0, %1}, p;}"
+          : "+f"(a[i]), "+f"(a[i + 1])
+          : "f"(x), "f"(y));
+    if (OP == 21 && (i & 3) == 0) {  // 2 FFMA2 + 1 DFMA interleaved
+      asm volatile(
+          "{.reg .b64 p, q, r;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %2};\n mov.b64 r, {%3, %3};\n"
+          " fma.rn.f32x2 p, p, q, r;\n mov.b64 {%0, %1}, p;}"
+          : "+f"(a[i]), "+f"(a[i + 1])
+          : "f"(x), "f"(y));
+      asm volatile(
+          "{.reg .f64 p, q;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %3};\n"
+          " fma.rn.f64 p, p, q, q;\n mov.b64 {%0, %1}, p;}"
+          : "+f"(a[i + 2]), "+f"(a[i + 3])
+          : "f"(x), "f"(y));
+    }
+    if (OP == 22 && (i & 1) == 0)  // cvt.f64.f32
+      asm volatile("{.reg .f64 p;\n cvt.f64.f32 p, %0;\n mov.b64 {%0, %1}, p;}"
+                   : "+f"(a[i]), "+f"(a[i + 1]));
+    if (OP == 23 && (i & 1) == 0)  // cvt.rn.f32.f64
+      asm volatile("{.reg .f64 p;\n mov.b64 p, {%0, %1};\n cvt.rn.f32.f64 %0, p;}"
+                   : "+f"(a[i]), "+f"(a[i + 1]));
+    if (OP == 24)  // HFMA2 (two halves per lane)
+      asm volatile("fma.rn.f16x2 %0, %0, %1, %1;" : "+r"(u[i]) : "r"(s));
+    if (OP == 25 && (i & 1) == 0) {  // FFMA2 + FMNMX3 (alu) interleaved
+      asm volatile(
+          "{.reg .b64 p, q, r;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %2};\n mov.b64 r, {%3, %3};\n"
+          " fma.rn.f32x2 p, p, q, r;\n mov.b64 {%0, %1}, p;}"
+          : "+f"(a[i]), "+f"(a[i + 1])
+          : "f"(x), "f"(y));
+      asm volatile("min.f32 %0, %0, %1, %2;" : "+r"(u[i]) : "r"(s), "r"(u[i + 1]));
+    }
+    if (OP == 26 && (i & 1) == 0) {  // FFMA2 + LDS.64
+      asm volatile(
+          "{.reg .b64 p, q, r;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %2};\n mov.b64 r, {%3, %3};\n"
+          " fma.rn.f32x2 p, p, q, r;\n mov.b64 {%0, %1}, p;}"
+          : "+f"(a[i]), "+f"(a[i + 1])
+          : "f"(x), "f"(y));
+      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(u[i]), "=r"(u[i + 1]) : "r"(s + 8 * i));
+    }
+    if (OP == 27 && (i & 1) == 0) {  // FFMA2 + SHFL
+      asm volatile(
+          "{.reg .b64 p, q, r;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %2};\n mov.b64 r, {%3, %3};\n"
+          " fma.rn.f32x2 p, p, q, r;\n mov.b64 {%0, %1}, p;}"
+          : "+f"(a[i]), "+f"(a[i + 1])
+          : "f"(x), "f"(y));
+      asm volatile("shfl.sync.down.b32 %0, %0, 1, 31, -1;" : "+r"(u[i]));
+    }
   }
 }
 
@@ -79,7 +129,7 @@ __global__ void k(float* out, long long* cyc, int iters, float px, float py, uin
   uint32_t u[CH];
   const float x = px + threadIdx.x * 1e-9f, y = py * (1.0f + threadIdx.x * 1e-9f);
   uint32_t s = ps ^ threadIdx.x;
-  if (OP == 16 || OP == 17) s = (unsigned)__cvta_generic_to_shared(sm) + 16 * (threadIdx.x & 31) * 0;
+  if (OP == 16 || OP == 17 || OP == 26) s = (unsigned)__cvta_generic_to_shared(sm) + 16 * (threadIdx.x & 31) * 0;
   for (int i = 0; i < CH; ++i) {
     a[i] = threadIdx.x * 1e-3f + i;
     u[i] = threadIdx.x * 77 + i;
@@ -138,5 +188,13 @@ int main() {
   run<15>("FFMA RRR+imm", CH, 1, out, cyc);
   run<16>("LDS.32", CH, 1, out, cyc);
   run<17>("LDS.128", CH / 4, 4, out, cyc);
+  run<20>("DFMA", CH / 2, 1, out, cyc);
+  run<21>("2 FFMA2 + DFMA", CH / 4 * 3, 1, out, cyc);
+  run<22>("F2F.F64.F32", CH / 2, 1, out, cyc);
+  run<23>("F2F.F32.F64", CH / 2, 1, out, cyc);
+  run<24>("HFMA2", CH, 2, out, cyc);
+  run<25>("FFMA2 + FMNMX3", CH, 1, out, cyc);
+  run<26>("FFMA2 + LDS.64", CH, 1, out, cyc);
+  run<27>("FFMA2 + SHFL", CH, 1, out, cyc);
   return 0;
 }

@@ -406,12 +406,34 @@ def test_pipe_every_window_height_exact(fp, cuda, oracle, monkeypatch, oh, part,
     if 2 * oh > H:
         pytest.skip("window taller than the video")
     monkeypatch.setenv("FUSEPLAN_PIPE_OH", str(oh))
+    monkeypatch.setenv("FUSEPLAN_PIPE_IMPL", "1")  # the row-pair pipeline (fc_pipe.cu)
     monkeypatch.setenv("FUSEPLAN_PIPE_BAND_SCALE", "100")
     pipe = spec_chain(W, H, F)
     v = hash_video_u8(F, 4, H, W, 70 + oh)
     want = oracle.orc_chain(pipe, v)
     out, _ = run(fp, pipe, v, {"force_partition": part},
                  variant="fast" if part == "1-5" else "auto", torch_dev=cuda)
+    np.testing.assert_array_equal(out, want)
+
+
+@pytest.mark.parametrize("out_rows", [6, 10, 14, 18, 22, 26, 29, 30])
+@pytest.mark.parametrize("shape", [(256, 131, 7), (136, 61, 6), (64, 37, 5)])
+def test_pair_every_window_height_exact(fp, cuda, oracle, monkeypatch, out_rows, shape):
+    """The frame-pair pipeline (fc_pipe2.cu) at every window height it is built
+    for, on frame heights that are not multiples of it (the last band shifted
+    up to end at the bottom row) and odd frame counts (a {A, A} tail pair):
+    bit-exact with widened certification bands (forced rechecks)."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    W, H, F = shape
+    if out_rows > H:
+        pytest.skip("window taller than the video")
+    monkeypatch.setenv("FUSEPLAN_PIPE_OUT", str(out_rows))
+    monkeypatch.setenv("FUSEPLAN_PIPE_BAND_SCALE", "100")
+    pipe = spec_chain(W, H, F)
+    v = hash_video_u8(F, 4, H, W, 170 + out_rows)
+    want = oracle.orc_chain(pipe, v)
+    out, ex = run(fp, pipe, v, {"force_partition": "1-5"}, variant="fast", torch_dev=cuda)
+    assert "frame-pair" in ex.describe()["last_chain_kernel"]
     np.testing.assert_array_equal(out, want)
 
 
