@@ -198,6 +198,14 @@ fp_status fp_track_features(const void* mask, int elem_type, int mask_on_device,
 /* JSON: the launch groups and the kernel each runs. */
 fp_status fp_exec_describe(const fp_exec* e, char** out_json);
 
+/* Certification parameters of the all-fused SPEC chain (host only, no
+ * device): JSON {g0, g1, mlo_n, band_n, S, mstar} -- the centre-normalised
+ * separable taps, the normalised-domain threshold and certified band on
+ * nd = mlo_n - gx^2 - gy^2, the scale S and the float threshold M* on m.
+ * FP_ERR_INPUT when the chain is not the SPEC chain or its parameters are
+ * outside the certified path.  Free with fp_string_free. */
+fp_status fp_certified_params(const fp_pipeline* p, char** out_json);
+
 /* Fills a device buffer with the deterministic counter-hash u8 test video
  * (frames [t0, t0 + frames) of a W x H x C volume). */
 fp_status fp_synth_hash_u8(void* device_out, int width, int height,

@@ -743,6 +743,27 @@ fp_status fp_exec_run_file(fp_exec* e, const char* in_path, const char* out_path
   });
 }
 
+fp_status fp_certified_params(const fp_pipeline* p, char** out_json) {
+  return guarded([&] {
+    need(p && out_json);
+    const auto& ks = p->p.kernels;
+    require(ks.size() >= 5 && ks[0].stencil_op == "rgba2gray" &&
+                ks[1].stencil_op == "iir_temporal" && ks[2].stencil_op == "gaussian" &&
+                ks[3].stencil_op == "gradient" && ks[4].stencil_op == "threshold",
+            ErrorKind::Input, "certified parameters exist for the SPEC chain only");
+    fc_stage st[5];
+    for (int i = 0; i < 5; ++i) st[i] = make_stage(ks[i]);
+    double c[6];
+    require(fc_certified_params(&st[0], &st[1], &st[2], &st[4], c) == 0, ErrorKind::Input,
+            "the chain's parameters are outside the certified path");
+    std::ostringstream ss;
+    ss.precision(17);
+    ss << "{\"g0\": " << c[0] << ", \"g1\": " << c[1] << ", \"mlo_n\": " << c[2]
+       << ", \"band_n\": " << c[3] << ", \"S\": " << c[4] << ", \"mstar\": " << c[5] << "}";
+    *out_json = dup(ss.str());
+  });
+}
+
 fp_status fp_exec_describe(const fp_exec* e, char** out_json) {
   return guarded([&] {
     need(e && out_json);

@@ -260,7 +260,20 @@ std::string Executor::describe() const {
      << ", \"output\": \"" << (out_type_ == FC_U8 ? "u8" : "f32")
      << "\", \"launches_per_run\": " << launches_per_run()
      << ", \"last_chain_kernel\": \"" << last_chain_ << "\""
-     << ", \"exact_rechecks_total\": " << fc_last_recheck_count() << ", \"groups\": [";
+     << ", \"exact_rechecks_total\": " << fc_last_recheck_count();
+  // the certified band of an all-fused SPEC chain (gray + IIR + gaussian + threshold)
+  for (const auto& g : groups_) {
+    if (g.kind != LaunchGroup::Chain || g.stages.size() != 5) continue;
+    double c[6];
+    if (fc_certified_params(&g.stages[0], &g.stages[1], &g.stages[2], &g.stages[4], c) == 0) {
+      ss.precision(17);
+      ss << ", \"certified\": {\"g0\": " << c[0] << ", \"g1\": " << c[1]
+         << ", \"mlo_n\": " << c[2] << ", \"band_n\": " << c[3] << ", \"S\": " << c[4]
+         << ", \"mstar\": " << c[5] << "}";
+    }
+    break;
+  }
+  ss << ", \"groups\": [";
   for (std::size_t i = 0; i < groups_.size(); ++i) {
     const auto& g = groups_[i];
     ss << (i ? ", " : "") << "{\"first\": " << g.first << ", \"last\": " << g.last

@@ -8,6 +8,7 @@
 #include <cstring>
 
 #include "fc_kernels.h"
+#include "fc_common.cuh"
 
 #define FC_CHAIN_ARGS                                                          \
   const fc_stage *sgray, const fc_stage *si, const fc_stage *sg,               \
@@ -123,6 +124,28 @@ extern "C" const char* fc_last_chain_kernel(void) { return g_last_chain; }
 extern "C" int fc_chain_pipe_applies(const fc_stage* sgray, const fc_stage* si,
                                      const fc_stage* sg, const fc_stage* sthr, int in_type,
                                      int gray_in, int out_type, fc_dims d, int pitch);
+
+// Certification parameters of the fused chain (host only; for reports and
+// the error-bound tests): out = {g0, g1, mlo_n, band_n, S, mstar}, where g0,
+// g1 are the centre-normalised separable taps, S = 1 / h2^2 the scale of the
+// normalised domain, mlo_n ~ S^2 M* and band_n the certified band on
+// nd = mlo_n - gx^2 - gy^2 (fc_common.cuh certify_band_scaled).  Returns 0,
+// or -1 when the chain is outside the certified path.
+extern "C" int fc_certified_params(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                                   const fc_stage* sthr, double* out) {
+  fccommon::FastParams p;
+  static const unsigned char dummy[16] __attribute__((aligned(16))) = {};
+  fc_dims d{16, 8, 1};
+  if (!fccommon::fast_params(sgray, si, sg, sthr, dummy, FC_U8, 0, FC_U8, d, 16, &p)) return -1;
+  const double e2 = double(p.h2);
+  out[0] = p.g0;
+  out[1] = p.g1;
+  out[2] = p.mlo_n;
+  out[3] = p.band_n;
+  out[4] = 1.0 / (e2 * e2);
+  out[5] = p.mstar;
+  return 0;
+}
 
 extern "C" long long fc_last_recheck_count(void) {
   return fc_pipe_recheck_count() + fc_pipe2_recheck_count();

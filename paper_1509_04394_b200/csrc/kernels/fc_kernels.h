@@ -150,6 +150,10 @@ int fc_hash_video_u8(uint8_t* out, fc_dims d, int channels, int t0,
 /* Count of pixels that took the exact recheck path in the last certified
  * launch on this stream's device (diagnostic; 0 if unavailable). */
 long long fc_last_recheck_count(void);
+/* Certification parameters of the fused chain, {g0, g1, mlo_n, band_n, S,
+ * mstar} (fc_dispatch.cu); -1 when the chain is outside the certified path. */
+int fc_certified_params(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                        const fc_stage* sthr, double* out);
 
 /* K6 tracking: one CTA per marker (fc_track.cu).  rois_dev: n x (x, y, w, h)
  * int32 on the device; points_dev: n x frames x 23 doubles on the device. */

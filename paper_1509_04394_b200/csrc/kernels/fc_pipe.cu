@@ -1082,7 +1082,7 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, bool src_f32, int f
       // segments that actually hold frames (16 asked of 161 frames: L = 11,
       // 15 segments); an empty trailing segment would march warm-up frames
       // past the end of its range
-      const int nseg = int((frames + L - 1) / L);
+      const int nseg = L > 0 ? int((frames + L - 1) / L) : 1;
       if (!force_segs && segs > 1 && !src_f32 && L < 2 * SEG_WARM) break;  // warm-up dominates
       if (segs > 1 && L < 2) break;
       const long long ctas = windows * nseg;

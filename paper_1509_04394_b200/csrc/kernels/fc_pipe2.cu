@@ -30,7 +30,7 @@
 //                       pixel land in one register pair), one STS.128 per 2
 //                       columns x 2 frames into the pair slot; lane 0 of the
 //                       last IIR warp also issues the R, G, B TMA copies
-//                       (NSF - 1 frames ahead; alpha never leaves HBM).
+//                       (one frame ahead; alpha never leaves HBM).
 //
 // Pair slot layout (1 KB per window row): 64 16-byte chunks, chunk k holds
 // columns 2k and 2k+1 as {IIR_t, IIR_t+1} each; even chunks at 0..31, odd
@@ -66,10 +66,17 @@ constexpr int NI = 8;       // IIR warps (two per SM sub-partition)
 constexpr int NWARP = NS + NI;
 constexpr int NTHR = NWARP * 32;
 constexpr int K2 = NPF + 1; // pair slots: one per pair in flight + one being written
-constexpr int NSF = 3;      // TMA RGB frame slots
-#ifndef FP2_NAMED
-#define FP2_NAMED 1  // IIR <-> stencil hand-offs on named barriers (no polling)
+#ifndef FP2_MRSPLIT
+#define FP2_MRSPLIT 0  // 1: IIR row counts per warp at compile time (two code variants:
+                       // 0.86 vs 0.80 ms, the instruction cache)
 #endif
+#ifndef FP2_NSF
+#define FP2_NSF 3
+#endif
+// TMA RGB frame slots (3: a ring, two frames of prefetch; 2: output frame A
+// of a pair in slot 0, B in slot 1 -- compile-time LDS offsets but one frame
+// of prefetch: 0.88 vs 0.80 ms)
+constexpr int NSF = FP2_NSF;
 #ifndef FP2_STENCIL_HI
 #define FP2_STENCIL_HI 1  // stencil warps at the high warp ids: scheduler priority (+3.7 %)
 #endif
@@ -98,7 +105,8 @@ struct Args {
   float* seg_warm_out;
   int* fix_k;
   int* seg_k;
-  int skip;    // timing experiments only (FUSEPLAN_PIPE_SKIP): 1 IIR math, 2 stencil math, 4 no TMA
+  int skip;    // timing experiments only (FUSEPLAN_PIPE_SKIP): 1 IIR math, 2 stencil math,
+               // 4 no TMA, 8 no gray (IIR warps only hand off slots)
   int opitch;  // output row pitch in bytes (>= W, a multiple of 4)
   FastParams p;
 };
@@ -117,19 +125,10 @@ __shared__ Range fp2_rg;
 __device__ unsigned long long g_rechecks2;
 extern __shared__ __align__(128) unsigned char fp2_smem[];
 
-// mbarrier layout: rgb_full[NSF], rgb_empty[NSF], iir_full[K2], iir_empty[K2]
-__device__ __forceinline__ uint64_t* bar_at(const Args& a, int i) {
+// mbarriers: rgb_full[NSF] (TMA completion); every other hand-off is a
+// named barrier
+__device__ __forceinline__ uint64_t* bar_rgb_full(const Args& a, int i) {
   return reinterpret_cast<uint64_t*>(fp2_smem + a.off_bar) + i;
-}
-__device__ __forceinline__ uint64_t* bar_rgb_full(const Args& a, int i) { return bar_at(a, i); }
-__device__ __forceinline__ uint64_t* bar_rgb_empty(const Args& a, int i) {
-  return bar_at(a, NSF + i);
-}
-__device__ __forceinline__ uint64_t* bar_iir_full(const Args& a, int i) {
-  return bar_at(a, 2 * NSF + i);
-}
-__device__ __forceinline__ uint64_t* bar_iir_empty(const Args& a, int i) {
-  return bar_at(a, 2 * NSF + K2 + i);
 }
 
 __device__ __forceinline__ void nb_sync(int id) {
@@ -137,6 +136,12 @@ __device__ __forceinline__ void nb_sync(int id) {
 }
 __device__ __forceinline__ void nb_arrive(int id) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(NB_THREADS) : "memory");
+}
+__device__ __forceinline__ void nb_sync_n(int id, unsigned n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nb_arrive_n(int id, unsigned n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -226,12 +231,25 @@ __device__ __forceinline__ float min3abs(float m, float a, float b) {
 
 // ------------------------------------------------------------------ IIR warps
 
-template <int OUT, bool HALF>
-__device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw, int lane,
+template <int N>
+using ic = std::integral_constant<int, N>;
+
+// RGB slot pitch for a window of R rows (R, G, B planes of BWB-byte rows)
+__host__ __device__ constexpr unsigned rgb_stride_of(int R) { return (unsigned(3 * R * BWB) + 127u) / 128u * 128u; }
+
+// RGB slot release on named barriers (IDs after the pair-slot ones): every
+// IIR warp but the producer's arrives after reading a frame, the producer
+// warp syncs before it issues the TMA copy into that slot
+constexpr int NB_RGB = 1 + 2 * K2;
+constexpr unsigned NB_RGB_THREADS = NI * 32;
+static_assert(NB_RGB + NSF <= 16, "named barrier ids");
+
+// MR: rows of this warp, p = iw + NI r for r < MR (all inside the window)
+template <int OUT, bool HALF, int MR>
+__device__ __forceinline__ void iir_rows(const Args& a, const Range& rg, int iw, int lane,
                                          int bx, int by, int xoff, const CUtensorMap* tmap,
                                          int tx0) {
   constexpr int R = OUT + 6;
-  constexpr int NR = (R + NI - 1) / NI;  // rows of this warp: p = iw + NI r
   const int W = a.W, H = a.H, n = rg.n, n_warm = rg.n_warm;
   const int n_out = n - n_warm;
   const int cplane = R * BWB;
@@ -251,88 +269,109 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
 #pragma unroll
     for (int j = 0; j < 4; ++j) msel[j] = 0x7440u + unsigned(edge & 3);
   }
-  int rowo[NR];  // RGB slot byte offset of the lane's word in row p (clamped row)
+  // rows past the window (FP2_MRSPLIT 0: every warp runs the longest row count)
+  auto row_ok = [&](int r) { return FP2_MRSPLIT || r < MR - 1 || iw + NI * r < R; };
+  int rowo[MR];  // RGB slot byte offset of the lane's word in row p (clamped row)
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const int p = min(iw + NI * r, R - 1);
-    rowo[r] = (clampi(by + p, 0, H - 1) - by) * BWB + coloff;
+  for (int r = 0; r < MR; ++r) {
+    const int p = iw + NI * r;
+    rowo[r] = (clampi(min(by + p, by + R - 1), 0, H - 1) - by) * BWB + coloff;
   }
   const unsigned so0 = chunk_off(2 * lane), so1 = chunk_off(2 * lane + 1);
 
   // q[r][j] = {IIR of frame A of the current pair, exact IIR state}: the state
   // lives in .y; a pair computes .x = IIR(A) from .y, then .y = IIR(B) from .x,
   // and stores {q(c0), q(c1)} as one 16-byte chunk (no register moves)
-  float2 q[NR][4];
+  float2 q[MR][4];
   const bool fresh = rg.st_in == nullptr;
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
+  for (int r = 0; r < MR; ++r) {
     const int p = iw + NI * r;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       q[r][j].x = 0.0f;
-      if (fresh || p >= R)
-        q[r][j].y = 0.0f;
-      else
-        q[r][j].y =
-            rg.st_in[(long long)clampi(by + p, 0, H - 1) * W + clampi(xl + j, 0, W - 1)];
+      q[r][j].y = fresh ? 0.0f
+                        : rg.st_in[(long long)clampi(by + p, 0, H - 1) * W +
+                                   clampi(xl + j, 0, W - 1)];
     }
   }
   // the lane's output cells (window rows 3 .. OUT + 2) -> a state plane
   auto write_state = [&](float* dst) {
     if (!dst || lane < 1 || lane > 30 || xl >= W) return;
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
+    for (int r = 0; r < MR; ++r) {
       const int p = iw + NI * r;
       if (p < 3 || p > OUT + 2 || by + p >= H) continue;
 #pragma unroll
       for (int j = 0; j < 4; ++j) dst[(long long)(by + p) * W + xl + j] = q[r][j].y;
     }
   };
+  auto to_state = [&]() {  // frame A becomes the state (warm-up, odd tail)
+#pragma unroll
+    for (int r = 0; r < MR; ++r)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q[r][j].y = q[r][j].x;
+  };
 
   const unsigned smem0 = smem_u32(fp2_smem);
-  int rslot = 0, islot = 0;
-  unsigned rpar = 0, ipar = 0;
-  // lane 0 of the last IIR warp keeps NSF - 1 frames of RGB in flight; the
-  // slot of frame t + NSF - 1 is that of frame t - 1, released by every IIR
-  // warp (this one included) before this warp starts frame t
-  const bool prod = iw == NI - 1 && lane == 0;
-  int pslot = 0;
-  unsigned ppar = 0;
+  int islot = 0;
+  // RGB slot of frame t: (t - n_warm) & 1, so every output pair's A frame
+  // sits in slot 0 and its B frame in slot 1 (compile-time LDS offsets)
+  constexpr unsigned RGB_STRIDE = rgb_stride_of(R);
+  unsigned rph = 0;  // mbarrier phase bit of each RGB slot (bit s)
+  int rs = 0;        // NSF > 2: ring slot of the next frame (frame t in slot t % NSF)
+  // the last IIR warp is the producer: its lane 0 copies frame t + 1 into
+  // the slot of frame t - 1 when it starts frame t, once every IIR warp has
+  // released that slot (named barrier)
+  const bool pwarp = iw == NI - 1;
   const int f0 = rg.f0;
-  auto issue = [&](int tp) {
-    wait_phase(bar_rgb_empty(a, pslot), ppar ^ 1u);
-    if (a.skip & 4) {
-      mbar_arrive(bar_rgb_full(a, pslot));
-    } else {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(bar_rgb_full(a, pslot), a.rgb_bytes);
-      tma_load_3d(fp2_smem + pslot * a.rgb_stride, tmap, bar_rgb_full(a, pslot), tx0, by,
-                  4 * (f0 + tp));
-    }
-    if (++pslot == NSF) {
-      pslot = 0;
-      ppar ^= 1u;
+  auto issue = [&](int tp, int slot) {  // producer warp only
+    if (tp >= NSF) nb_sync_n(NB_RGB + slot, NB_RGB_THREADS);
+    if (lane == 0) {
+      if (a.skip & 4) {
+        mbar_arrive(bar_rgb_full(a, slot));
+      } else {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar_rgb_full(a, slot), a.rgb_bytes);
+        tma_load_3d(fp2_smem + slot * RGB_STRIDE, tmap, bar_rgb_full(a, slot), tx0, by,
+                    4 * (f0 + tp));
+      }
     }
   };
-  if (prod) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
-    for (int tp = 0; tp < NSF - 1 && tp < n; ++tp) issue(tp);
+  if (pwarp) {
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+    if (NSF == 2) {
+      if (n > 0) issue(0, n_warm & 1);
+    } else {
+      for (int tp = 0; tp < NSF - 1 && tp < n; ++tp) issue(tp, tp);
+    }
   }
+  const unsigned rgb0 = smem0;  // shared-space address of RGB slot 0
+  int rowa[MR];                 // + the lane's word in row p
+#pragma unroll
+  for (int r = 0; r < MR; ++r) rowa[r] = int(rgb0) + rowo[r];
 
   // gray of frame t for every cell: g[r][h] = {gray(col 2h), gray(col 2h+1)}
-  // (x 0.5 when HALF: alpha folded into the weights)
-  auto gray = [&](int t, auto&& row_fn) {
-    if (prod && t + NSF - 1 < n) issue(t + NSF - 1);
-    wait_phase(bar_rgb_full(a, rslot), rpar);
-    const unsigned char* f = fp2_smem + rslot * a.rgb_stride;
+  // (x 0.5 when HALF: alpha folded into the weights), consumed row by row.
+  // SLOT: the frame's RGB slot, 0 / 1, or -1 (warm-up frames: (t - n_warm) & 1)
+  auto gray = [&](int t, auto slot_t, auto&& row_fn) {
+    constexpr int SLOT = NSF == 2 ? decltype(slot_t)::value : -1;
+    const int slot = NSF != 2 ? rs : SLOT >= 0 ? SLOT : ((t - n_warm) & 1);
+    if (pwarp && t + NSF - 1 < n)
+      issue(t + NSF - 1, NSF == 2 ? (slot ^ 1) : (slot == 0 ? NSF - 1 : slot - 1));
+    wait_phase(bar_rgb_full(a, slot), (rph >> slot) & 1u);
+    rph ^= 1u << slot;
+    const unsigned soff = SLOT >= 0 ? unsigned(SLOT) * RGB_STRIDE : unsigned(slot) * RGB_STRIDE;
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      if (iw + NI * r >= R) continue;
+    for (int r = 0; r < MR; ++r) {
+      if (!row_ok(r) || (a.skip & 8)) continue;  // skip 8: no gray at all (timing only)
       uint32_t w[3];
       float2 g[2];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
-        w[c] = *reinterpret_cast<const uint32_t*>(f + c * cplane + rowo[r]);
+        asm volatile("ld.shared.b32 %0, [%1];"
+                     : "=r"(w[c])
+                     : "r"(unsigned(rowa[r]) + soff + unsigned(c * cplane)));
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const float2 pr = wprod(f2(magic_rs(w[0], k4b, msel[2 * h]),
@@ -345,92 +384,107 @@ __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw,
       }
       row_fn(r, g);  // consume the row at once (few live registers)
     }
-    __syncwarp();  // the warp's RGB reads are done (values in registers)
-    mbar_arrive_lane0(bar_rgb_empty(a, rslot), lane);
-    if (++rslot == NSF) {
-      rslot = 0;
-      rpar ^= 1u;
-    }
+    // the warp's RGB reads are done (values in registers): release the slot
+    // to the producer warp's copy of frame t + 2 into it
+    if (!pwarp && t + NSF < n) nb_arrive_n(NB_RGB + slot, NB_RGB_THREADS);
+    if (NSF != 2) rs = rs == NSF - 1 ? 0 : rs + 1;
   };
   // IIR update y' from y and the cell's gray value x (simulator.cpp:57-62):
   // HALF: fl(0.5 x + fl(0.5 y)) == FMA(0.5, y, 0.5 x) (x = gray > 0 dwarfs
   // any rounding of 0.5 y; x = 0 gives fl(0.5 y) either way); otherwise
   // fl(fl(a x) + fl(b y)) in scalar .rn ops.  First frame: y' = gray.
-  auto upd = [&](float yo, float gj, bool first) -> float {
-    if (HALF) return first ? __fadd_rn(gj, gj) : __fmaf_rn(0.5f, yo, gj);
-    return first ? gj : __fadd_rn(__fmul_rn(ia, gj), __fmul_rn(ib, yo));
+  auto upd = [&](float yo, float gj, auto first_t) -> float {
+    constexpr bool FIRST = decltype(first_t)::value;
+    if (HALF) return FIRST ? __fadd_rn(gj, gj) : __fmaf_rn(0.5f, yo, gj);
+    return FIRST ? gj : __fadd_rn(__fmul_rn(ia, gj), __fmul_rn(ib, yo));
   };
   // frame t into component A (.x, from the state .y) or B (.y, from .x)
-  auto frame = [&](int t, bool to_b) {
-    const bool first = fresh && t == 0;
+  auto frame = [&](int t, auto to_b_t, auto first_t, auto slot_t) {
+    constexpr bool TO_B = decltype(to_b_t)::value;
     const bool skip = (a.skip & 1) != 0;
-    gray(t, [&](int r, const float2 (&g)[2]) {
+    gray(t, slot_t, [&](int r, const float2 (&g)[2]) {
       if (skip) return;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const float gj = (j & 1) ? g[j >> 1].y : g[j >> 1].x;
-        if (to_b)
-          q[r][j].y = upd(q[r][j].x, gj, false);  // B never starts a recurrence
-        else if (first)
-          q[r][j].x = upd(q[r][j].y, gj, true);
+        if (TO_B)
+          q[r][j].y = upd(q[r][j].x, gj, first_t);  // B never starts a recurrence
         else
-          q[r][j].x = upd(q[r][j].y, gj, false);
+          q[r][j].x = upd(q[r][j].y, gj, first_t);
       }
     });
   };
   int n_stored = 0;
   auto store_pair = [&]() {
-    if (FP2_NAMED) {
-      if (n_stored >= K2) nb_sync(1 + islot);  // the stencil released pair n_stored - K2
-    } else {
-      wait_phase(bar_iir_empty(a, islot), ipar ^ 1u);
-    }
+    if (n_stored >= K2) nb_sync(1 + islot);  // the stencil released pair n_stored - K2
     const unsigned base = smem0 + a.off_iir + islot * a.iir_stride;
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
+    for (int r = 0; r < MR; ++r) {
       const int p = iw + NI * r;
-      if (p >= R) continue;
+      if (!row_ok(r)) continue;
       sts128f(base + p * PROW + so0, q[r][0].x, q[r][0].y, q[r][1].x, q[r][1].y);
       sts128f(base + p * PROW + so1, q[r][2].x, q[r][2].y, q[r][3].x, q[r][3].y);
     }
-    if (FP2_NAMED) {
-      nb_arrive(1 + K2 + islot);
-    } else {
-      __syncwarp();  // the warp's stores precede the release arrive
-      mbar_arrive_lane0(bar_iir_full(a, islot), lane);
-    }
+    nb_arrive(1 + K2 + islot);
     ++n_stored;
-    if (++islot == K2) {
-      islot = 0;
-      ipar ^= 1u;
-    }
+    if (++islot == K2) islot = 0;
   };
+  const auto A = std::false_type{};
+  const auto B = std::true_type{};
+  const auto FIRST = std::true_type{};
+  const auto NEXT = std::false_type{};
+  const auto S0 = ic<0>{};
+  const auto S1 = ic<1>{};
+  const auto SR = ic<-1>{};
 
-  // warm-up frames: state only (A then copy to the state)
-  for (int t = 0; t < n_warm; ++t) {
-    frame(t, false);
-#pragma unroll
-    for (int r = 0; r < NR; ++r)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) q[r][j].y = q[r][j].x;
-    if (t == n_warm - 1) write_state(rg.st_warm);
+  // frame 0 of a fresh run starts the recurrence (y = gray): peeled, so the
+  // loops below carry no first-frame test
+  int t = 0;
+  if (fresh && n > 0) {
+    frame(0, A, FIRST, SR);
+    to_state();
+    t = 1;
   }
-  // output frames in pairs (A = t, B = t + 1)
+  // warm-up frames: state only
+  for (; t < n_warm; ++t) {
+    frame(t, A, NEXT, SR);
+    to_state();
+  }
+  if (n_warm > 0) write_state(rg.st_warm);
+  // output frames in pairs (A = t in RGB slot 0, B = t + 1 in slot 1); an
+  // odd tail is stored {A, A}
   int k = 0;
+  if (t > n_warm) {  // the peeled frame 0 is the first pair's A
+    if (n_out > 1)
+      frame(1, B, NEXT, S1);
+    else
+      to_state();
+    store_pair();
+    k = 2;
+  }
   for (; k + 1 < n_out; k += 2) {
-    frame(n_warm + k, false);
-    frame(n_warm + k + 1, true);
+    frame(n_warm + k, A, NEXT, S0);
+    frame(n_warm + k + 1, B, NEXT, S1);
     store_pair();
   }
-  if (k < n_out) {  // odd tail: {A, A}
-    frame(n_warm + k, false);
-#pragma unroll
-    for (int r = 0; r < NR; ++r)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) q[r][j].y = q[r][j].x;
+  if (k < n_out) {
+    frame(n_warm + k, A, NEXT, S0);
+    to_state();
     store_pair();
   }
   write_state(rg.st_out);
+}
+
+template <int OUT, bool HALF>
+__device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw, int lane,
+                                         int bx, int by, int xoff, const CUtensorMap* tmap,
+                                         int tx0) {
+  constexpr int R = OUT + 6;
+  constexpr int NR = (R + NI - 1) / NI;  // rows of the first R % NI warps (all, if 0)
+  if (!FP2_MRSPLIT || R % NI == 0 || iw < R % NI)
+    iir_rows<OUT, HALF, NR>(a, rg, iw, lane, bx, by, xoff, tmap, tx0);
+  else
+    iir_rows<OUT, HALF, NR - 1>(a, rg, iw, lane, bx, by, xoff, tmap, tx0);
 }
 
 // ------------------------------------------------------------------ stencil warps
@@ -470,9 +524,6 @@ __device__ __noinline__ bool exact_white(const Args& a, const unsigned char* bas
                 __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(0, -1))), s(1, -1)));
   return __fsqrt_rn(__fadd_rn(__fmul_rn(gx, gx), __fmul_rn(gy, gy))) >= a.p.th_val;
 }
-
-template <int N>
-using ic = std::integral_constant<int, N>;
 
 // Stencil warp sw: frame pairs sw, sw + NS, ... of the pair ring.  Lane L
 // owns window columns 4L .. 4L+3 (outputs: lanes 1..30).  The march over the
@@ -514,12 +565,8 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
   const long long fstride = (long long)OW * H;
 
   int slot = fp0 % K2;
-  unsigned par = (fp0 / K2) & 1u;
   for (int u = fp0; u < n_pairs; u += NPF) {
-    if (FP2_NAMED)
-      nb_sync(1 + K2 + slot);
-    else
-      wait_phase(bar_iir_full(a, slot), par);
+    nb_sync(1 + K2 + slot);  // the IIR warps stored pair u
     const unsigned sbase = smem0 + a.off_iir + slot * a.iir_stride;  // slot row 0
     const unsigned base = sbase + r0 * PROW;                         // march row 0
     const bool has_b = 2 * u + 1 < n_out;
@@ -680,17 +727,9 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
         __syncwarp();
       }
     }
-    if (FP2_NAMED) {
-      if (u + K2 < n_pairs) nb_arrive(1 + slot);  // the IIR warps wait for it
-    } else {
-      __syncwarp();  // the warp's slot reads (and rechecks) are done
-      mbar_arrive_lane0(bar_iir_empty(a, slot), lane);
-    }
+    if (u + K2 < n_pairs) nb_arrive(1 + slot);  // the IIR warps wait for it
     slot += NPF;
-    if (slot >= K2) {
-      slot -= K2;
-      par ^= 1u;
-    }
+    if (slot >= K2) slot -= K2;
   }
 }
 
@@ -738,14 +777,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int tx0 = bx >= 0 ? (bx & ~15) : -((-bx + 15) & ~15);
   double* taps = reinterpret_cast<double*>(fp2_smem + a.off_taps);
   if (tid == 0) {
-    for (int i = 0; i < NSF; ++i) {
-      mbar_init(bar_rgb_full(a, i), 1);
-      mbar_init(bar_rgb_empty(a, i), NI);
-    }
-    for (int i = 0; i < K2; ++i) {
-      mbar_init(bar_iir_full(a, i), NI);
-      mbar_init(bar_iir_empty(a, i), WPF);  // the pair's stencil warps
-    }
+    for (int i = 0; i < NSF; ++i) mbar_init(bar_rgb_full(a, i), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < 25) taps[tid] = double(a.p.taps[tid]);
@@ -768,13 +800,13 @@ __global__ void __launch_bounds__(NTHR, 1)
 size_t layout(int out_rows, Args* a) {
   const int R = out_rows + 6;
   const size_t rgb = size_t(3) * R * BWB;
-  const size_t rgb_stride = (rgb + 127) / 128 * 128;
+  const size_t rgb_stride = rgb_stride_of(R);
   size_t off = NSF * rgb_stride;
   const size_t off_iir = off;
   const size_t iir_stride = size_t(R) * PROW;
   off += K2 * iir_stride;
   const size_t off_bar = off;
-  off += (2 * NSF + 2 * K2) * 8;
+  off += NSF * 8;
   const size_t off_taps = (off + 7) / 8 * 8;
   off = off_taps + 25 * 8;
   const size_t off_queue = off;
@@ -793,7 +825,7 @@ size_t layout(int out_rows, Args* a) {
 
 using KernelFn = void (*)(CUtensorMap, Args);
 
-#define FP2_OUT_LIST(X) X(6) X(10) X(14) X(18) X(22) X(26) X(29) X(30)
+#define FP2_OUT_LIST(X) X(6) X(10) X(14) X(18) X(22) X(26) X(29)  // 30 rows exceed 227 KB
 
 KernelFn kernel_for(int out_rows, bool half) {
   switch (out_rows) {
@@ -858,7 +890,7 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, int force, int forc
       // segments that actually hold frames (16 asked of 161 frames: L = 11,
       // 15 segments); an empty trailing segment would march warm-up frames
       // past the end of its range
-      const int nseg = int((frames + L - 1) / L);
+      const int nseg = L > 0 ? int((frames + L - 1) / L) : 1;
       if (!force_segs && segs > 1 && L < 2 * SEG_WARM) break;
       if (segs > 1 && L < 2) break;
       const long long ctas = windows * nseg;

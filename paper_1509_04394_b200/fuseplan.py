@@ -96,6 +96,7 @@ def lib() -> ctypes.CDLL:
         "fp_exec_run": ([P, P, I, P, I, P], I),
         "fp_exec_run_range": ([P, P, I, P, I, I, P, P, P], I),
         "fp_exec_describe": ([P, PP], I),
+        "fp_certified_params": ([P, PP], I),
         "fp_exec_run_file": ([P, S, S], I),
         "fp_synth_hash_u8": ([P, I, I, I, I, I, ctypes.c_uint64, P], I),
         "fp_exec_converge": ([P, P, I, I, P, P, ctypes.POINTER(ctypes.c_int), P], I),
@@ -179,6 +180,14 @@ class Pipeline(_Handle):
         _check(lib().fp_analyze_report(self.ptr, fmt.encode(), int(timestamp),
                                        ctypes.byref(out)))
         return _take_string(out)
+
+
+    def certified_params(self) -> dict:
+        """Certification parameters of the all-fused SPEC chain (host only):
+        {g0, g1, mlo_n, band_n, S, mstar} (fp_certified_params)."""
+        out = ctypes.c_void_p()
+        _check(lib().fp_certified_params(self.ptr, ctypes.byref(out)))
+        return json.loads(_take_string(out))
 
 
 class Device(_Handle):

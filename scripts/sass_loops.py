@@ -14,7 +14,7 @@ for line in blk.splitlines():
 addr = {a: i for i, (a, _) in enumerate(ins)}
 print("function", blk.split("\n")[0].strip(), "instructions", len(ins))
 for i, (a, t) in enumerate(ins):
-    m = re.search(r"BRA\S* (?:`\()?\.?L?_?x?_?(0x[0-9a-f]+)", t)
+    m = re.search(r"BRA\S*.*?(0x[0-9a-f]+)\s*$", t)
     if not m: continue
     tgt = int(m.group(1), 16)
     if tgt >= a or tgt not in addr: continue
