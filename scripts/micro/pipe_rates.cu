@@ -110,6 +110,32 @@ __device__ __forceinline__ void step(float* a, uint32_t* u, float x, float y, ui
           : "f"(x), "f"(y));
       asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(u[i]), "=r"(u[i + 1]) : "r"(s + 8 * i));
     }
+    if (OP == 28) asm volatile("cvt.rn.f32.u32 %0, %1;" : "=f"(a[i]) : "r"(u[i] ^ s));  // I2FP (+LOP)
+    if (OP == 29) {  // I2F.U8 from the low byte
+      asm volatile("{.reg .u16 h;\n cvt.u16.u32 h, %1;\n cvt.rn.f32.u8 %0, h;}" : "=f"(a[i]) : "r"(u[i]));
+      u[i] += 1;
+    }
+    if (OP == 30) asm volatile("shr.b32 %0, %0, 1;" : "+r"(u[i]));
+    if (OP == 31) asm volatile("{.reg .pred p;\n setp.ne.u32 p, %2, 0;\n selp.f32 %0, %0, %1, p;}" : "+f"(a[i]) : "f"(x), "r"(s));
+    if (OP == 32) asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(a[i]) : "f"(x), "f"(y));
+    if (OP == 33) asm volatile("mad.lo.u32 %0, %0, %1, %1;" : "+r"(u[i]) : "r"(s));
+    if (OP == 34) {  // HADD2.F32: half -> float
+      asm volatile("{.reg .f16 h;\n mov.b32 {h, _}, %1;\n cvt.f32.f16 %0, h;}" : "=f"(a[i]) : "r"(u[i]));
+      u[i] += 1;
+    }
+    if (OP == 35 && (i & 1) == 0) {  // FFMA2 + FSEL
+      asm volatile(
+          "{.reg .b64 p, q, r;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %2};\n mov.b64 r, {%3, %3};\n"
+          " fma.rn.f32x2 p, p, q, r;\n mov.b64 {%0, %1}, p;}"
+          : "+f"(a[i]), "+f"(a[i + 1])
+          : "f"(x), "f"(y));
+      asm volatile("{.reg .pred p;\n setp.ne.u32 p, %1, 0;\n selp.b32 %0, %0, %1, p;}" : "+r"(u[i]) : "r"(s));
+    }
+    if (OP == 36) asm volatile("add.u32 %0, %0, %1;\n add.u32 %0, %0, %2;" : "+r"(u[i]) : "r"(s), "r"(u[(i + 1) % CH]));  // IADD3
+    if (OP == 37) asm volatile("shf.r.wrap.b32 %0, %0, %1, 8;" : "+r"(u[i]) : "r"(s));  // funnel shift
+    if (OP == 38) {  // mixed f16 x f16 + f32 (sm_100 FFMA with f16 sources)
+      asm volatile("{.reg .f16 h;\n mov.b32 {h, _}, %1;\n fma.rn.f32.f16 %0, h, h, %0;}" : "+f"(a[i]) : "r"(s));
+    }
     if (OP == 27 && (i & 1) == 0) {  // FFMA2 + SHFL
       asm volatile(
           "{.reg .b64 p, q, r;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %2};\n mov.b64 r, {%3, %3};\n"
@@ -196,5 +222,16 @@ int main() {
   run<25>("FFMA2 + FMNMX3", CH, 1, out, cyc);
   run<26>("FFMA2 + LDS.64", CH, 1, out, cyc);
   run<27>("FFMA2 + SHFL", CH, 1, out, cyc);
+  run<28>("I2FP.F32.U32", CH, 1, out, cyc);
+  run<29>("I2F.U8", CH, 1, out, cyc);
+  run<30>("SHF.R", CH, 1, out, cyc);
+  run<31>("FSEL", CH, 1, out, cyc);
+  run<32>("FMNMX3", CH, 1, out, cyc);
+  run<33>("IMAD", CH, 1, out, cyc);
+  run<34>("HADD2.F32 (f16->f32)", CH, 1, out, cyc);
+  run<35>("FFMA2 + SEL", CH, 1, out, cyc);
+  run<36>("IADD3 (2 adds)", CH, 1, out, cyc);
+  run<37>("SHF funnel", CH, 1, out, cyc);
+  run<38>("FFMA f32.f16", CH, 1, out, cyc);
   return 0;
 }
