@@ -40,6 +40,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <type_traits>
 #include <utility>
 #include <vector>
@@ -946,25 +947,24 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
   if (d.frames == 0) return 0;
   int dev = 0;
   cudaGetDevice(&dev);
-  static thread_local PairPlan cache;
   const fc_knobs& kn = *fc_get_knobs();
   const bool segs_ok = state_in == nullptr && n_warm == 0;
   const int force_out = kn.pipe_out, force_segs = kn.pipe_segs;
-  if (cache.W != d.width || cache.H != d.height || cache.dev != dev ||
-      cache.frames != d.frames || cache.segs_ok != segs_ok || cache.force_out != force_out ||
-      cache.force_segs != force_segs) {
+  // plans per (device, shape, frames, segment eligibility, forcing knobs): a
+  // host thread driving several devices or executors does not re-plan (and
+  // re-set the kernels' shared-memory attributes) on every launch
+  using Key = std::tuple<int, int, int, int, int, bool, int, int>;
+  static thread_local std::map<Key, PairPlan> plans;
+  const Key key{dev, d.width, d.height, d.frames, n_warm, segs_ok, force_out, force_segs};
+  auto it = plans.find(key);
+  if (it == plans.end()) {
     PairPlan pp;
     if (!choose(d.width, d.height, d.frames - n_warm, segs_ok, dev, force_out, force_segs, &pp))
       return -1;
-    pp.force_out = force_out;
-    pp.force_segs = force_segs;
-    pp.W = d.width;
-    pp.H = d.height;
-    pp.dev = dev;
-    pp.frames = d.frames;
-    pp.segs_ok = segs_ok;
-    cache = pp;
+    if (plans.size() > 256) plans.clear();
+    it = plans.emplace(key, pp).first;
   }
+  const PairPlan& cache = it->second;
   Args a;
   std::memset(&a, 0, sizeof a);
   layout(cache.out_rows, &a);
