@@ -138,6 +138,14 @@ struct FastParams {
   float g0, g1, mlo_n, band_n;
 };
 
+// M* = the smallest float m with sqrtf(m) >= th (white <=> m >= M*)
+inline float threshold_mstar(float th) {
+  float m = th * th;
+  while (m > 0.0f && std::sqrt(std::nextafter(m, 0.0f)) >= th) m = std::nextafter(m, 0.0f);
+  while (std::sqrt(m) < th) m = std::nextafter(m, INFINITY);
+  return m;
+}
+
 // Certified error band on m = gx^2 + gy^2 (u = 2^-24, all stencil inputs >= 0):
 //   kappa : relative error of the FP32 separable gaussian vs the reference's
 //           FP64-accumulated, float-rounded value: <= 8.1u (two passes of at
@@ -208,12 +216,8 @@ inline bool stencil_params(const fc_stage* sg, const fc_stage* sthr, int out_typ
   if (!(dw < 1e-5)) return false;  // not separable enough to certify
   std::memcpy(p->taps, sg->g_w, sizeof p->taps);
   p->th_val = sthr->th;
-  // M* = min float m with sqrtf(m) >= th
-  float m = sthr->th * sthr->th;
-  while (m > 0.0f && std::sqrt(std::nextafter(m, 0.0f)) >= sthr->th) m = std::nextafter(m, 0.0f);
-  while (std::sqrt(m) < sthr->th) m = std::nextafter(m, INFINITY);
-  p->mstar = m;
-  p->mlo = std::nextafter(m, 0.0f);
+  p->mstar = threshold_mstar(sthr->th);
+  p->mlo = std::nextafter(p->mstar, 0.0f);
   double tap_sum = 0.0;
   for (int k = 0; k < 25; ++k) tap_sum += sg->g_w[k];
   p->band = certify_band(p->mstar, in_max * tap_sum * 1.001, dw);
@@ -235,20 +239,21 @@ inline bool stencil_params(const fc_stage* sg, const fc_stage* sthr, int out_typ
   return true;
 }
 
-// pitch: bytes between the video's rows (>= width; the TMA map needs it and
-// the base address 16-byte aligned).
-inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
-                        const fc_stage* sthr, const void* video, int in_type, int gray_in,
-                        int out_type, fc_dims d, int pitch, FastParams* p) {
-  if (in_type != FC_U8 || out_type != FC_U8 || gray_in || sgray == nullptr) return false;
+// Gray + IIR half of both frame pipelines (exact S1+S2): the u8 RGBA video's
+// layout requirements and the folded weights.  pitch: bytes between the
+// video's rows (>= width; the TMA map needs it and the base address 16-byte
+// aligned).  Returns the upper bound of the IIR values (0: not covered).
+inline double iir_params(const fc_stage* sgray, const fc_stage* si, const void* video,
+                         int in_type, int gray_in, fc_dims d, int pitch, FastParams* p) {
+  if (in_type != FC_U8 || gray_in || sgray == nullptr) return 0.0;
   // any alpha in [0, 1] keeps the IIR a convex combination (the value bound
   // the certification needs); 0.5 takes the folded one-FMA update
-  if (!(si->alpha >= 0.0f && si->alpha <= 1.0f)) return false;
-  if (sgray->wr < 0.0f || sgray->wg < 0.0f || sgray->wb < 0.0f) return false;
+  if (!(si->alpha >= 0.0f && si->alpha <= 1.0f)) return 0.0;
+  if (sgray->wr < 0.0f || sgray->wg < 0.0f || sgray->wb < 0.0f) return 0.0;
   // width % 4: every stencil lane owns 4 whole columns (its mask store, the
   // edge replication of the IIR cells and the Sobel x clamp assume it)
-  if (pitch < d.width || pitch % 16 != 0 || d.width % 4 != 0 || d.height < 1) return false;
-  if (reinterpret_cast<uintptr_t>(video) % 16 != 0) return false;
+  if (pitch < d.width || pitch % 16 != 0 || d.width % 4 != 0 || d.height < 1) return 0.0;
+  if (reinterpret_cast<uintptr_t>(video) % 16 != 0) return 0.0;
   std::memset(p, 0, sizeof *p);
   p->alpha_half = si->alpha == 0.5f;
   p->ia = si->alpha;
@@ -263,8 +268,29 @@ inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stag
   p->wbm = -p->wb * 8388608.0f;
   p->k4b = 0x4B000000u;
   // IIR values are convex combinations of gray values in [0, gray_max]
-  const double gray_max = 255.0 * (double(sgray->wr) + double(sgray->wg) + double(sgray->wb));
-  return stencil_params(sg, sthr, out_type, gray_max, p);
+  return 255.0 * (double(sgray->wr) + double(sgray->wg) + double(sgray->wb));
+}
+
+inline bool fast_params(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                        const fc_stage* sthr, const void* video, int in_type, int gray_in,
+                        int out_type, fc_dims d, int pitch, FastParams* p) {
+  const double gray_max = iir_params(sgray, si, video, in_type, gray_in, d, pitch, p);
+  return gray_max > 0.0 && stencil_params(sg, sthr, out_type, gray_max, p);
+}
+
+// The exact frame pipeline (FP64 gaussian in the reference's order, float
+// Sobel, m >= M*): any 5x5 gaussian, a {0, 255} byte mask, th > 0.
+inline bool exact_params(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg,
+                         const fc_stage* sthr, const void* video, int in_type, int gray_in,
+                         int out_type, fc_dims d, int pitch, FastParams* p) {
+  if (iir_params(sgray, si, video, in_type, gray_in, d, pitch, p) <= 0.0) return false;
+  if (out_type != FC_U8 || sg->g_radius != 2 || !(sthr->th > 0.0f)) return false;
+  if (sthr->white != 255.0f || sthr->black != 0.0f) return false;
+  std::memcpy(p->taps, sg->g_w, sizeof p->taps);
+  p->th_val = sthr->th;
+  p->mstar = threshold_mstar(sthr->th);
+  p->mlo = std::nextafter(p->mstar, 0.0f);
+  return true;
 }
 
 inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

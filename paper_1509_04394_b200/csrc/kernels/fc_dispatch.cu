@@ -28,6 +28,11 @@ extern "C" int fc_chain_pipe2(const fc_stage* sgray, const fc_stage* si, const f
                               const float* state_in, float* state_out, int pitch, int opitch,
                               void* stream);  // fc_pipe2.cu: certified, frame pairs
 extern "C" long long fc_pipe2_recheck_count(void);
+extern "C" int fc_chain_pipe2_exact(const fc_stage* sgray, const fc_stage* si,
+                                    const fc_stage* sg, const fc_stage* sthr, const void* video,
+                                    int in_type, int gray_in, void* out, int out_type, fc_dims d,
+                                    int n_warm, const float* state_in, float* state_out,
+                                    int pitch, int opitch, void* stream);  // fc_pipe2.cu: exact
 extern "C" int fc_f345_pipe(const fc_stage* sg, const fc_stage* sthr, const float* in,
                             void* out, int out_type, fc_dims d, double in_max, void* stream);
 extern "C" long long fc_pipe_recheck_count(void);
@@ -100,6 +105,23 @@ extern "C" int fc_fused_chain_pitched(const fc_stage* sgray, const fc_stage* si,
       g_last_chain = pair ? "certified FP32 frame-pair pipeline (fc_pipe2.cu)"
                           : "certified FP32 row-pair pipeline (fc_pipe.cu)";
     if (rc != -1 || variant == 2) return rc;  // -1: parameters not covered
+  }
+  // reference-exact: the frame-pair pipeline with the FP64 stencil role where
+  // it applies (u8 RGBA in, 5x5 gaussian, {0, 255} byte mask), else the FP64
+  // tile march
+  {
+    const int rc = fc_chain_pipe2_exact(sgray, si, sg, sthr, pitched ? pitched : video, in_type,
+                                        gray_in, pitched_out ? pitched_out : out, out_type, d,
+                                        n_warm, state_in, state_out, pitched ? video_pitch : 0,
+                                        pitched_out ? out_pitch : 0, stream);
+    if (rc == 0 && pitched_out)
+      return int(cudaMemcpy2DAsync(out, size_t(d.width), pitched_out, size_t(out_pitch),
+                                   size_t(d.width), size_t(d.height) * (d.frames - n_warm),
+                                   cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+    if (rc != -1) {
+      g_last_chain = "exact FP64 frame-pair pipeline (fc_pipe2.cu)";
+      return rc;
+    }
   }
   g_last_chain = "exact FP64 tiles (fc_exact.cu k_chain_exact)";
   return fc_chain_exact(sgray, si, sg, sthr, video, in_type, gray_in, out,

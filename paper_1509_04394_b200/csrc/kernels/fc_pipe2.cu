@@ -110,6 +110,7 @@ struct Args {
                // 4 no TMA, 8 no gray (IIR warps only hand off slots)
   int opitch;  // output row pitch in bytes (>= W, a multiple of 4)
   FastParams p;
+  double dtaps[25];  // the reference taps widened once (EXACT: DFMA constant operands)
 };
 
 struct Range {
@@ -734,9 +735,172 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
   }
 }
 
+// ------------------------------------------------------------------ exact stencil warps
+
+// Reference-exact stencil role (the EXACT pipeline, variant "exact"): for each
+// frame of the pair a march over the window rows computing the FP64 gaussian
+// in the reference's dy-outer / dx-inner order, rounding it to float, the
+// Sobel magnitude^2 in the reference's float order and `m >= M*` (==
+// sqrtf(m) >= th, M* the smallest such float), simulator.cpp:63-89.  No
+// certification, no rechecks: every operation is the reference's.
+//
+// Each loaded window row p (converted to double once) feeds the five gaussian
+// rows g = p - 2 .. p + 2 that read it, as their dy = p - g + 2 term: the
+// 25-term chain of G row g advances one tap row per step in the reference's
+// order, and a step carries 5 rows x 4 columns = 20 independent DFMA chains
+// (a per-row 25-deep chain would leave the FP64 pipe latency-bound).  G row
+// g completes at step g + 2; the Sobel of row q = p - 3 runs at step p.
+// Lane L owns window columns 4L .. 4L+3 (outputs: lanes 1..30).
+template <int OUT>
+__device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& rg, int sw,
+                                                   int lane, int bx, int by) {
+  constexpr int R = OUT + 6;
+  static_assert(R >= 10, "window too short for the exact march");
+  const int W = a.W, H = a.H;
+  const int n_out = rg.n - rg.n_warm;
+  const int n_pairs = (n_out + 1) / 2;
+  const float mstar = a.p.mstar;
+  const int k = 2 * lane;
+  const int xl = bx + 2 * k;
+  const bool outl = lane >= 1 && lane <= 30 && xl < W;
+  const bool xlo = xl == 0, xhi = xl + LC - 1 == W - 1;
+  unsigned cch[LC / 2 + 2];
+#pragma unroll
+  for (int i = 0; i < LC / 2 + 2; ++i) cch[i] = chunk_off((k - 1 + i + 64) & 63);
+  const unsigned smem0 = smem_u32(fp2_smem);
+  const int OW = a.opitch;
+  const long long fstride = (long long)OW * H;
+
+  int slot = sw % K2;
+  for (int u = sw; u < n_pairs; u += NPF) {
+    nb_sync(1 + K2 + slot);  // the IIR warps stored pair u
+    const unsigned base = smem0 + a.off_iir + slot * a.iir_stride;
+    for (int c = 0; c < 2; ++c) {
+      if (c == 1 && 2 * u + 1 >= n_out) break;
+      unsigned char* ox =
+          a.out + (long long)(rg.out0 + 2 * u + c) * fstride + (long long)(by + 3) * OW + xl;
+      const unsigned cbase = base + 4 * c;  // frame c's component of every chunk
+      double acc[5][LC];    // gaussian row g at ring index g % 5
+      float gq[5][LC + 2];  // G row g at ring index g % 5; cols 4L-1 .. 4L+4
+
+      // step p (PM = p % 5): tap rows k in [KMIN, KMAX] of G rows p + 2 - k;
+      // DONE: G row p - 2 completes (k = 4); SOB: Sobel of row p - 3
+      // YC: the first / last Sobel step, where the video's top / bottom row may
+      // clamp G in y (no other step can)
+      auto step = [&](auto pm_t, auto kmin_t, auto kmax_t, auto done_t, auto sob_t, int p,
+                      auto yc_t) {
+        constexpr int PM = decltype(pm_t)::value;
+        constexpr int KMIN = decltype(kmin_t)::value, KMAX = decltype(kmax_t)::value;
+        constexpr bool DONE = decltype(done_t)::value, SOB = decltype(sob_t)::value;
+        constexpr bool YC = decltype(yc_t)::value;
+        double v[LC + 4];  // window row p, cols 4L-2 .. 4L+5 (frame c: +4 c bytes)
+#pragma unroll
+        for (int i = 0; i < LC / 2 + 2; ++i) {
+          float x0, x1;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x0) : "r"(cbase + p * PROW + cch[i]));
+          asm volatile("ld.shared.f32 %0, [%1 + 8];" : "=f"(x1) : "r"(cbase + p * PROW + cch[i]));
+          v[2 * i] = double(x0);
+          v[2 * i + 1] = double(x1);
+        }
+#pragma unroll
+        for (int kk = KMIN; kk <= KMAX; ++kk) {
+          constexpr int dummy = 0;
+          (void)dummy;
+          const int gi = (PM + 2 - kk + 5) % 5;  // compile-time after unrolling
+#pragma unroll
+          for (int j = 0; j < LC; ++j) {
+            double t = kk == 0 ? 0.0 : acc[gi][j];
+#pragma unroll
+            for (int dx = 0; dx < 5; ++dx) t = __fma_rn(a.dtaps[kk * 5 + dx], v[j + dx], t);
+            acc[gi][j] = t;
+          }
+        }
+        if constexpr (DONE) {
+          constexpr int GM = (PM + 3) % 5;  // (p - 2) % 5
+          float gv[LC];
+#pragma unroll
+          for (int j = 0; j < LC; ++j) gv[j] = __double2float_rn(acc[GM][j]);
+          float l = __shfl_up_sync(0xffffffffu, gv[LC - 1], 1);
+          float r = __shfl_down_sync(0xffffffffu, gv[0], 1);
+          if (xlo) l = gv[0];       // the Sobel reads G clamped to the video (x = -1 -> 0)
+          if (xhi) r = gv[LC - 1];  // (x = W -> W - 1)
+          gq[GM][0] = l;
+#pragma unroll
+          for (int j = 0; j < LC; ++j) gq[GM][j + 1] = gv[j];
+          gq[GM][LC + 1] = r;
+        }
+        if constexpr (SOB) {
+          constexpr int QM = (PM + 2) % 5;  // (p - 3) % 5
+          const int yq = by + p - 3;        // video row of the Sobel centre
+          const bool ytop = YC && yq == 0, ybot = YC && yq == H - 1;  // G clamped in y
+          float rm[LC + 2], rc[LC + 2], rp[LC + 2];
+#pragma unroll
+          for (int i = 0; i < LC + 2; ++i) {
+            rc[i] = gq[QM][i];
+            rm[i] = ytop ? rc[i] : gq[(QM + 4) % 5][i];
+            rp[i] = ybot ? rc[i] : gq[(QM + 1) % 5][i];
+          }
+          uint32_t word = 0;
+#pragma unroll
+          for (int j = 0; j < LC; ++j) {
+            auto s = [&](int dx, int dy) {
+              return dy < 0 ? rm[j + 1 + dx] : (dy > 0 ? rp[j + 1 + dx] : rc[j + 1 + dx]);
+            };
+            const float gx =
+                __fsub_rn(__fadd_rn(__fadd_rn(s(1, -1), __fmul_rn(2.0f, s(1, 0))), s(1, 1)),
+                          __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(-1, 0))), s(-1, 1)));
+            const float gy =
+                __fsub_rn(__fadd_rn(__fadd_rn(s(-1, 1), __fmul_rn(2.0f, s(0, 1))), s(1, 1)),
+                          __fadd_rn(__fadd_rn(s(-1, -1), __fmul_rn(2.0f, s(0, -1))), s(1, -1)));
+            const float m = __fadd_rn(__fmul_rn(gx, gx), __fmul_rn(gy, gy));
+            word |= (m >= mstar ? 0xFFu : 0u) << (8 * j);
+          }
+          st_pred_u32(ox, word, outl);
+          ox += OW;
+        }
+      };
+      const auto F = std::false_type{};
+      const auto T = std::true_type{};
+      // head: rows 0..5 start G rows 2 .. 7; G rows 2, 3 complete at steps 4, 5
+      step(ic<0>{}, ic<0>{}, ic<0>{}, F, F, 0, F);
+      step(ic<1>{}, ic<0>{}, ic<1>{}, F, F, 1, F);
+      step(ic<2>{}, ic<0>{}, ic<2>{}, F, F, 2, F);
+      step(ic<3>{}, ic<0>{}, ic<3>{}, F, F, 3, F);
+      step(ic<4>{}, ic<0>{}, ic<4>{}, T, F, 4, F);
+      step(ic<0>{}, ic<0>{}, ic<4>{}, T, F, 5, F);
+      // step 6: the first Sobel (row 3: the video's top row in band 0); body
+      // steps 7 .. R - 5 update all five rows; then the tail R - 4 .. R - 1
+      // (no G rows past R - 3; the last Sobel may be the video's bottom row)
+      static_assert(R - 4 > 6, "exact march layout");
+      step(ic<1>{}, ic<0>{}, ic<4>{}, T, T, 6, T);
+      constexpr int NB = R - 11;  // full steps from p = 7
+#pragma unroll 1
+      for (int p = 7; p + 5 <= 7 + NB; p += 5) {
+        step(ic<2>{}, ic<0>{}, ic<4>{}, T, T, p, F);
+        step(ic<3>{}, ic<0>{}, ic<4>{}, T, T, p + 1, F);
+        step(ic<4>{}, ic<0>{}, ic<4>{}, T, T, p + 2, F);
+        step(ic<0>{}, ic<0>{}, ic<4>{}, T, T, p + 3, F);
+        step(ic<1>{}, ic<0>{}, ic<4>{}, T, T, p + 4, F);
+      }
+      constexpr int PR = 7 + 5 * (NB / 5);  // first remaining full step
+      if constexpr (7 + NB - PR >= 1) step(ic<2>{}, ic<0>{}, ic<4>{}, T, T, PR, F);
+      if constexpr (7 + NB - PR >= 2) step(ic<3>{}, ic<0>{}, ic<4>{}, T, T, PR + 1, F);
+      if constexpr (7 + NB - PR >= 3) step(ic<4>{}, ic<0>{}, ic<4>{}, T, T, PR + 2, F);
+      if constexpr (7 + NB - PR >= 4) step(ic<0>{}, ic<0>{}, ic<4>{}, T, T, PR + 3, F);
+      step(ic<(R - 4) % 5>{}, ic<1>{}, ic<4>{}, T, T, R - 4, F);
+      step(ic<(R - 3) % 5>{}, ic<2>{}, ic<4>{}, T, T, R - 3, F);
+      step(ic<(R - 2) % 5>{}, ic<3>{}, ic<4>{}, T, T, R - 2, F);
+      step(ic<(R - 1) % 5>{}, ic<4>{}, ic<4>{}, T, T, R - 1, T);
+    }
+    if (u + K2 < n_pairs) nb_arrive(1 + slot);  // the IIR warps wait for it
+    slot += NPF;
+    if (slot >= K2) slot -= K2;
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 
-template <int OUT, bool HALF>
+template <int OUT, bool HALF, bool EXACT>
 __global__ void __launch_bounds__(NTHR, 1)
     k_chain_pair(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
   constexpr int R = OUT + 6;
@@ -788,7 +952,10 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int sw = FP2_STENCIL_HI ? warp - NI : warp;  // stencil warp index (or < 0)
   if (sw >= 0 && sw < NS) {
     if (WPF == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(FP2_SREG));
-    stencil_role<OUT>(a, fp2_rg, sw, lane, bx, by);
+    if constexpr (EXACT)
+      exact_stencil_role<OUT>(a, fp2_rg, sw, lane, bx, by);
+    else
+      stencil_role<OUT>(a, fp2_rg, sw, lane, bx, by);
   } else {
     if (WPF == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(FP2_IREG));
     iir_role<OUT, HALF>(a, fp2_rg, FP2_STENCIL_HI ? warp : warp - NS, lane, bx, by, bx - tx0,
@@ -828,11 +995,12 @@ using KernelFn = void (*)(CUtensorMap, Args);
 
 #define FP2_OUT_LIST(X) X(6) X(10) X(14) X(18) X(22) X(26) X(29)  // 30 rows exceed 227 KB
 
-KernelFn kernel_for(int out_rows, bool half) {
+KernelFn kernel_for(int out_rows, bool half, bool exact) {
   switch (out_rows) {
-#define FP2_CASE(N) \
-  case N:           \
-    return half ? k_chain_pair<N, true> : k_chain_pair<N, false>;
+#define FP2_CASE(N)                                                             \
+  case N:                                                                       \
+    return exact ? (half ? k_chain_pair<N, true, true> : k_chain_pair<N, false, true>) \
+                 : (half ? k_chain_pair<N, true, false> : k_chain_pair<N, false, false>);
     FP2_OUT_LIST(FP2_CASE)
 #undef FP2_CASE
   }
@@ -869,12 +1037,13 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, int force, int forc
     const size_t smem = layout(o, nullptr);
     if (smem > size_t(optin) || o > H) continue;  // the last band must fit the video
     cudaError_t e = cudaSuccess;
-    for (int h = 0; h < 2 && e == cudaSuccess; ++h)
-      e = cudaFuncSetAttribute(kernel_for(o, h != 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem));
+    for (int h = 0; h < 4 && e == cudaSuccess; ++h)
+      e = cudaFuncSetAttribute(kernel_for(o, (h & 1) != 0, (h & 2) != 0),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 0;
     if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(o, true), NTHR, smem);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(o, true, false), NTHR,
+                                                        smem);
     if (dbg)
       std::fprintf(stderr, "fc_pipe2 choose: out=%d smem=%zu optin=%d err=%s per_sm=%d\n", o,
                    smem, optin, cudaGetErrorString(e), per_sm);
@@ -943,7 +1112,8 @@ SegScratch& seg_scratch(int dev, cudaStream_t st) {
 }
 
 int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_warm,
-           const float* state_in, float* state_out, void* stream, int pitch, int opitch) {
+           const float* state_in, float* state_out, void* stream, int pitch, int opitch,
+           bool exact) {
   if (d.frames == 0) return 0;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1000,12 +1170,13 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
   a.state_in = state_in;
   a.state_out = state_out;
   a.p = fp;
+  for (int i = 0; i < 25; ++i) a.dtaps[i] = double(fp.taps[i]);
   a.skip = kn.pipe_skip;
   if (kn.band_scale > 0.0f) a.p.band_n *= kn.band_scale;  // tests / diagnostics only
   CUtensorMap map;
   if (!rgb_tensor_map(&map, in, d, BWB, cache.out_rows + 6, pitch ? pitch : d.width)) return -1;
   const int grid = cache.strips * cache.bands * cache.n_segs;
-  KernelFn fn = kernel_for(cache.out_rows, fp.alpha_half != 0);
+  KernelFn fn = kernel_for(cache.out_rows, fp.alpha_half != 0, exact);
   fn<<<grid, NTHR, cache.smem, st>>>(map, a);
   int rc = int(cudaGetLastError());
   if (rc == 0 && verify) {
@@ -1020,6 +1191,25 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
   return rc;
 }
 
+// Host entry of both pipelines (certified / exact).
+int entry(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg, const fc_stage* sthr,
+          const void* video, int in_type, int gray_in, void* out, int out_type, fc_dims d,
+          int n_warm, const float* state_in, float* state_out, int pitch, int opitch,
+          void* stream, bool exact) {
+  FastParams fp;
+  if (pitch == 0) pitch = d.width;
+  if (opitch == 0) opitch = d.width;
+  if (opitch < d.width || opitch % 4 != 0 || reinterpret_cast<uintptr_t>(out) % 4 != 0)
+    return -1;
+  if (d.height < 6) return -1;
+  const bool ok = exact ? exact_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d,
+                                       pitch, &fp)
+                        : fast_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d,
+                                      pitch, &fp);
+  if (!ok) return -1;
+  return launch(fp, video, out, d, n_warm, state_in, state_out, stream, pitch, opitch, exact);
+}
+
 }  // namespace fcpipe2
 
 // Same contract as fc_chain_pipe (fc_pipe.cu): -1 when the chain or the
@@ -1029,16 +1219,19 @@ extern "C" int fc_chain_pipe2(const fc_stage* sgray, const fc_stage* si, const f
                               void* out, int out_type, fc_dims d, int n_warm,
                               const float* state_in, float* state_out, int pitch, int opitch,
                               void* stream) {
-  using namespace fcpipe2;
-  FastParams fp;
-  if (pitch == 0) pitch = d.width;
-  if (opitch == 0) opitch = d.width;
-  if (opitch < d.width || opitch % 4 != 0 || reinterpret_cast<uintptr_t>(out) % 4 != 0)
-    return -1;
-  if (d.height < 6) return -1;
-  if (!fast_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d, pitch, &fp))
-    return -1;
-  return launch(fp, video, out, d, n_warm, state_in, state_out, stream, pitch, opitch);
+  return fcpipe2::entry(sgray, si, sg, sthr, video, in_type, gray_in, out, out_type, d, n_warm,
+                        state_in, state_out, pitch, opitch, stream, false);
+}
+
+// The exact frame-pair pipeline (FP64 gaussian in the reference's order, no
+// certification): -1 when the chain or the layout is outside it.
+extern "C" int fc_chain_pipe2_exact(const fc_stage* sgray, const fc_stage* si,
+                                    const fc_stage* sg, const fc_stage* sthr, const void* video,
+                                    int in_type, int gray_in, void* out, int out_type, fc_dims d,
+                                    int n_warm, const float* state_in, float* state_out,
+                                    int pitch, int opitch, void* stream) {
+  return fcpipe2::entry(sgray, si, sg, sthr, video, in_type, gray_in, out, out_type, d, n_warm,
+                        state_in, state_out, pitch, opitch, stream, true);
 }
 
 extern "C" long long fc_pipe2_recheck_count(void) {

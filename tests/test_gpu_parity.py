@@ -437,6 +437,55 @@ def test_pair_every_window_height_exact(fp, cuda, oracle, monkeypatch, out_rows,
     np.testing.assert_array_equal(out, want)
 
 
+@pytest.mark.parametrize("out_rows", [0, 6, 14, 22, 29])
+@pytest.mark.parametrize("shape,th", [((256, 131, 7), 30.0), ((192, 432, 61), 40.0),
+                                      ((800, 600, 9), 20.0), ((64, 37, 5), 10.0)])
+def test_pair_exact_pipeline(fp, cuda, oracle, monkeypatch, out_rows, shape, th):
+    """The exact frame-pair pipeline (variant "exact": FP64 gaussian in the
+    reference's order, float Sobel, no certification) at several window
+    heights, frame heights that are not multiples of them and odd frame
+    counts: bit-exact, and it is the kernel that ran."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    W, H, F = shape
+    if out_rows > H:
+        pytest.skip("window taller than the video")
+    if out_rows:
+        monkeypatch.setenv("FUSEPLAN_PIPE_OUT", str(out_rows))
+    pipe = spec_chain(W, H, F, th=th)
+    v = hash_video_u8(F, 4, H, W, 270 + out_rows)
+    want = oracle.orc_chain(pipe, v)
+    out, ex = run(fp, pipe, v, {"force_partition": "1-5"}, variant="exact", torch_dev=cuda)
+    assert "exact FP64 frame-pair" in ex.describe()["last_chain_kernel"]
+    np.testing.assert_array_equal(out, want)
+
+
+@pytest.mark.parametrize("segs,seg_warm", [(0, None), (3, 1), (4, None)])
+def test_pair_exact_segments_and_carry(fp, cuda, oracle, monkeypatch, segs, seg_warm):
+    """The exact pipeline with time segments (forced seam fix-ups at a 1-frame
+    warm-up) and a range run carrying the IIR state: bit-exact."""
+    import torch
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    if segs:
+        monkeypatch.setenv("FUSEPLAN_PIPE_SEGS", str(segs))
+    if seg_warm is not None:
+        monkeypatch.setenv("FUSEPLAN_PIPE_SEG_WARM", str(seg_warm))
+    W, H, F = 192, 96, 230
+    pipe = spec_chain(W, H, F, th=30.0)
+    v = hash_video_u8(F, 4, H, W, 77 + segs)
+    want = oracle.orc_chain(pipe, v)
+    p = fp.Pipeline(json.dumps(pipe))
+    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": "1-5"}),
+                     variant="exact")
+    vt = torch.from_numpy(v).to(cuda)
+    st = torch.empty((1, H, W), device=cuda)
+    out = ex.run_range(vt[:F - 11], state_out=st)
+    tail = ex.run_range(vt[F - 11:], state_in=st)
+    torch.cuda.synchronize()
+    assert "exact FP64 frame-pair" in ex.describe()["last_chain_kernel"]
+    got = torch.cat([out, tail]).cpu().numpy().astype(np.float32)
+    np.testing.assert_array_equal(got, want)
+
+
 @pytest.mark.parametrize("shape", [(128, 64, 1), (128, 64, 2), (256, 30, 3), (1024, 12, 7)])
 @pytest.mark.parametrize("segs", [0, 2, 5])
 def test_pipe_tiny_frame_counts_exact(fp, cuda, oracle, monkeypatch, shape, segs):
