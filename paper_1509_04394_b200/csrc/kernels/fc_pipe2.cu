@@ -84,6 +84,13 @@ constexpr int NSF = FP2_NSF;
 // named barriers: 1 + slot = "slot empty", 1 + K2 + slot = "slot full"; the
 // pair's stencil warp(s) and every IIR warp take part
 constexpr unsigned NB_THREADS = (NI + WPF) * 32;
+// The exact pipeline runs two stencil warps per pair, one per frame (frame
+// A on warps 0-3, frame B on warps 4-7 of the stencil group: two stencil
+// warps per SM sub-partition hide the DFMA chains' latency); 16 warps at
+// <= 128 registers.
+constexpr int NS_X = 2 * NPF;
+constexpr int NTHR_X = (NI + NS_X) * 32;
+constexpr unsigned NB_THREADS_X = (NI + 2) * 32;
 constexpr int SW = 120;     // output columns per strip (window 128 = SW + 8)
 constexpr int BWB = 144;    // TMA box row bytes: 128 + worst-case 16-B alignment slack
 constexpr int PROW = 1024;  // bytes per window row of a pair slot
@@ -133,11 +140,15 @@ __device__ __forceinline__ uint64_t* bar_rgb_full(const Args& a, int i) {
   return reinterpret_cast<uint64_t*>(fp2_smem + a.off_bar) + i;
 }
 
+template <bool EXACT = false>
 __device__ __forceinline__ void nb_sync(int id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NB_THREADS) : "memory");
+  constexpr unsigned n = EXACT ? NB_THREADS_X : NB_THREADS;
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+template <bool EXACT = false>
 __device__ __forceinline__ void nb_arrive(int id) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(NB_THREADS) : "memory");
+  constexpr unsigned n = EXACT ? NB_THREADS_X : NB_THREADS;
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void nb_sync_n(int id, unsigned n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -247,7 +258,7 @@ constexpr unsigned NB_RGB_THREADS = NI * 32;
 static_assert(NB_RGB + NSF <= 16, "named barrier ids");
 
 // MR: rows of this warp, p = iw + NI r for r < MR (all inside the window)
-template <int OUT, bool HALF, int MR>
+template <int OUT, bool HALF, int MR, bool EXACT>
 __device__ __forceinline__ void iir_rows(const Args& a, const Range& rg, int iw, int lane,
                                          int bx, int by, int xoff, const CUtensorMap* tmap,
                                          int tx0) {
@@ -418,7 +429,7 @@ __device__ __forceinline__ void iir_rows(const Args& a, const Range& rg, int iw,
   };
   int n_stored = 0;
   auto store_pair = [&]() {
-    if (n_stored >= K2) nb_sync(1 + islot);  // the stencil released pair n_stored - K2
+    if (n_stored >= K2) nb_sync<EXACT>(1 + islot);  // the stencil released pair n_stored - K2
     const unsigned base = smem0 + a.off_iir + islot * a.iir_stride;
 #pragma unroll
     for (int r = 0; r < MR; ++r) {
@@ -427,7 +438,7 @@ __device__ __forceinline__ void iir_rows(const Args& a, const Range& rg, int iw,
       sts128f(base + p * PROW + so0, q[r][0].x, q[r][0].y, q[r][1].x, q[r][1].y);
       sts128f(base + p * PROW + so1, q[r][2].x, q[r][2].y, q[r][3].x, q[r][3].y);
     }
-    nb_arrive(1 + K2 + islot);
+    nb_arrive<EXACT>(1 + K2 + islot);
     ++n_stored;
     if (++islot == K2) islot = 0;
   };
@@ -477,16 +488,16 @@ __device__ __forceinline__ void iir_rows(const Args& a, const Range& rg, int iw,
   write_state(rg.st_out);
 }
 
-template <int OUT, bool HALF>
+template <int OUT, bool HALF, bool EXACT>
 __device__ __forceinline__ void iir_role(const Args& a, const Range& rg, int iw, int lane,
                                          int bx, int by, int xoff, const CUtensorMap* tmap,
                                          int tx0) {
   constexpr int R = OUT + 6;
   constexpr int NR = (R + NI - 1) / NI;  // rows of the first R % NI warps (all, if 0)
   if (!FP2_MRSPLIT || R % NI == 0 || iw < R % NI)
-    iir_rows<OUT, HALF, NR>(a, rg, iw, lane, bx, by, xoff, tmap, tx0);
+    iir_rows<OUT, HALF, NR, EXACT>(a, rg, iw, lane, bx, by, xoff, tmap, tx0);
   else
-    iir_rows<OUT, HALF, NR - 1>(a, rg, iw, lane, bx, by, xoff, tmap, tx0);
+    iir_rows<OUT, HALF, NR - 1, EXACT>(a, rg, iw, lane, bx, by, xoff, tmap, tx0);
 }
 
 // ------------------------------------------------------------------ stencil warps
@@ -771,12 +782,12 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
   const int OW = a.opitch;
   const long long fstride = (long long)OW * H;
 
-  int slot = sw % K2;
-  for (int u = sw; u < n_pairs; u += NPF) {
-    nb_sync(1 + K2 + slot);  // the IIR warps stored pair u
+  const int fp0 = sw % NPF, c = sw / NPF;  // pair phase, frame of the pair (A / B)
+  int slot = fp0 % K2;
+  for (int u = fp0; u < n_pairs; u += NPF) {
+    nb_sync<true>(1 + K2 + slot);  // the IIR warps stored pair u
     const unsigned base = smem0 + a.off_iir + slot * a.iir_stride;
-    for (int c = 0; c < 2; ++c) {
-      if (c == 1 && 2 * u + 1 >= n_out) break;
+    if (c == 0 || 2 * u + 1 < n_out) {
       unsigned char* ox =
           a.out + (long long)(rg.out0 + 2 * u + c) * fstride + (long long)(by + 3) * OW + xl;
       const unsigned cbase = base + 4 * c;  // frame c's component of every chunk
@@ -892,7 +903,7 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
       step(ic<(R - 2) % 5>{}, ic<3>{}, ic<4>{}, T, T, R - 2, F);
       step(ic<(R - 1) % 5>{}, ic<4>{}, ic<4>{}, T, T, R - 1, T);
     }
-    if (u + K2 < n_pairs) nb_arrive(1 + slot);  // the IIR warps wait for it
+    if (u + K2 < n_pairs) nb_arrive<true>(1 + slot);  // the IIR warps wait for it
     slot += NPF;
     if (slot >= K2) slot -= K2;
   }
@@ -901,7 +912,7 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
 // ------------------------------------------------------------------ kernel
 
 template <int OUT, bool HALF, bool EXACT>
-__global__ void __launch_bounds__(NTHR, 1)
+__global__ void __launch_bounds__(EXACT ? NTHR_X : NTHR, 1)
     k_chain_pair(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
   constexpr int R = OUT + 6;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -950,15 +961,15 @@ __global__ void __launch_bounds__(NTHR, 1)
   __syncthreads();  // the only CTA-wide barrier: roles run decoupled from here
   (void)R;
   const int sw = FP2_STENCIL_HI ? warp - NI : warp;  // stencil warp index (or < 0)
-  if (sw >= 0 && sw < NS) {
-    if (WPF == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(FP2_SREG));
+  if (sw >= 0 && sw < (EXACT ? NS_X : NS)) {
+    if (!EXACT && WPF == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(FP2_SREG));
     if constexpr (EXACT)
       exact_stencil_role<OUT>(a, fp2_rg, sw, lane, bx, by);
     else
       stencil_role<OUT>(a, fp2_rg, sw, lane, bx, by);
   } else {
-    if (WPF == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(FP2_IREG));
-    iir_role<OUT, HALF>(a, fp2_rg, FP2_STENCIL_HI ? warp : warp - NS, lane, bx, by, bx - tx0,
+    if (!EXACT && WPF == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(FP2_IREG));
+    iir_role<OUT, HALF, EXACT>(a, fp2_rg, FP2_STENCIL_HI ? warp : warp - NS, lane, bx, by, bx - tx0,
                         &tmap, tx0);
   }
 }
@@ -1177,7 +1188,8 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
   if (!rgb_tensor_map(&map, in, d, BWB, cache.out_rows + 6, pitch ? pitch : d.width)) return -1;
   const int grid = cache.strips * cache.bands * cache.n_segs;
   KernelFn fn = kernel_for(cache.out_rows, fp.alpha_half != 0, exact);
-  fn<<<grid, NTHR, cache.smem, st>>>(map, a);
+  const int nthr = exact ? NTHR_X : NTHR;
+  fn<<<grid, nthr, cache.smem, st>>>(map, a);
   int rc = int(cudaGetLastError());
   if (rc == 0 && verify) {
     k_verify_segments<<<296, 256, 0, st>>>(a.seg_warm_out, a.seg_end, hwl, cache.n_segs,
@@ -1185,7 +1197,7 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
     Args f = a;
     f.fix_k = a.seg_k;
     f.seg_k = nullptr;
-    fn<<<cache.strips * cache.bands, NTHR, cache.smem, st>>>(map, f);
+    fn<<<cache.strips * cache.bands, nthr, cache.smem, st>>>(map, f);
     rc = int(cudaGetLastError());
   }
   return rc;
