@@ -117,7 +117,9 @@ struct Args {
                // 4 no TMA, 8 no gray (IIR warps only hand off slots)
   int opitch;  // output row pitch in bytes (>= W, a multiple of 4)
   FastParams p;
-  double dtaps[25];  // the reference taps widened once (EXACT: DFMA constant operands)
+  double dtaps[25];  // the reference taps widened once
+  double dtap6[6];   // EXACT: the six distinct taps of the symmetric 5x5 gaussian, by
+                     // (min, max) of (|dy|, |dx|): 00 01 02 11 12 22
 };
 
 struct Range {
@@ -435,8 +437,14 @@ __device__ __forceinline__ void iir_rows(const Args& a, const Range& rg, int iw,
     for (int r = 0; r < MR; ++r) {
       const int p = iw + NI * r;
       if (!row_ok(r)) continue;
-      sts128f(base + p * PROW + so0, q[r][0].x, q[r][0].y, q[r][1].x, q[r][1].y);
-      sts128f(base + p * PROW + so1, q[r][2].x, q[r][2].y, q[r][3].x, q[r][3].y);
+      if constexpr (EXACT) {  // frame planes: row p = {A: 128 floats, B: 128 floats}
+        sts128f(base + p * PROW + 16 * lane, q[r][0].x, q[r][1].x, q[r][2].x, q[r][3].x);
+        sts128f(base + p * PROW + 512 + 16 * lane, q[r][0].y, q[r][1].y, q[r][2].y,
+                q[r][3].y);
+      } else {
+        sts128f(base + p * PROW + so0, q[r][0].x, q[r][0].y, q[r][1].x, q[r][1].y);
+        sts128f(base + p * PROW + so1, q[r][2].x, q[r][2].y, q[r][3].x, q[r][3].y);
+      }
     }
     nb_arrive<EXACT>(1 + K2 + islot);
     ++n_stored;
@@ -775,14 +783,23 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
   const int xl = bx + 2 * k;
   const bool outl = lane >= 1 && lane <= 30 && xl < W;
   const bool xlo = xl == 0, xhi = xl + LC - 1 == W - 1;
-  unsigned cch[LC / 2 + 2];
-#pragma unroll
-  for (int i = 0; i < LC / 2 + 2; ++i) cch[i] = chunk_off((k - 1 + i + 64) & 63);
   const unsigned smem0 = smem_u32(fp2_smem);
   const int OW = a.opitch;
   const long long fstride = (long long)OW * H;
 
   const int fp0 = sw % NPF, c = sw / NPF;  // pair phase, frame of the pair (A / B)
+  // the six distinct taps in registers (the symmetric gaussian; exact_params
+  // checked the symmetry bit for bit)
+  double t6[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) t6[i] = a.dtap6[i];
+  auto tap = [&](int dy, int dx) -> double {  // compile-time dy, dx after unrolling
+    const int p = dy < 2 ? 2 - dy : dy - 2, q = dx < 2 ? 2 - dx : dx - 2;
+    const int lo = p < q ? p : q, hi = p < q ? q : p;
+    return t6[lo == 0 ? hi : (lo == 1 ? 2 + hi : 5)];
+  };
+  const unsigned lcol = 16u * unsigned((lane + 31) & 31), mcol = 16u * unsigned(lane),
+                 rcol = 16u * unsigned((lane + 1) & 31);
   int slot = fp0 % K2;
   for (int u = fp0; u < n_pairs; u += NPF) {
     nb_sync<true>(1 + K2 + slot);  // the IIR warps stored pair u
@@ -790,7 +807,7 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
     if (c == 0 || 2 * u + 1 < n_out) {
       unsigned char* ox =
           a.out + (long long)(rg.out0 + 2 * u + c) * fstride + (long long)(by + 3) * OW + xl;
-      const unsigned cbase = base + 4 * c;  // frame c's component of every chunk
+      const unsigned cbase = base + 512 * c;  // frame c's plane of every slot row
       double acc[5][LC];    // gaussian row g at ring index g % 5
       float gq[5][LC + 2];  // G row g at ring index g % 5; cols 4L-1 .. 4L+4
 
@@ -804,14 +821,18 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
         constexpr int KMIN = decltype(kmin_t)::value, KMAX = decltype(kmax_t)::value;
         constexpr bool DONE = decltype(done_t)::value, SOB = decltype(sob_t)::value;
         constexpr bool YC = decltype(yc_t)::value;
-        double v[LC + 4];  // window row p, cols 4L-2 .. 4L+5 (frame c: +4 c bytes)
-#pragma unroll
-        for (int i = 0; i < LC / 2 + 2; ++i) {
-          float x0, x1;
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x0) : "r"(cbase + p * PROW + cch[i]));
-          asm volatile("ld.shared.f32 %0, [%1 + 8];" : "=f"(x1) : "r"(cbase + p * PROW + cch[i]));
-          v[2 * i] = double(x0);
-          v[2 * i + 1] = double(x1);
+        double v[LC + 4];  // window row p, cols 4L-2 .. 4L+5 (frame c's plane)
+        {
+          const unsigned rb = cbase + p * PROW;
+          const float4 ql = lds128(rb + lcol), qm = lds128(rb + mcol), qr = lds128(rb + rcol);
+          v[0] = double(ql.z);
+          v[1] = double(ql.w);
+          v[2] = double(qm.x);
+          v[3] = double(qm.y);
+          v[4] = double(qm.z);
+          v[5] = double(qm.w);
+          v[6] = double(qr.x);
+          v[7] = double(qr.y);
         }
 #pragma unroll
         for (int kk = KMIN; kk <= KMAX; ++kk) {
@@ -822,7 +843,7 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
           for (int j = 0; j < LC; ++j) {
             double t = kk == 0 ? 0.0 : acc[gi][j];
 #pragma unroll
-            for (int dx = 0; dx < 5; ++dx) t = __fma_rn(a.dtaps[kk * 5 + dx], v[j + dx], t);
+            for (int dx = 0; dx < 5; ++dx) t = __fma_rn(tap(kk, dx), v[j + dx], t);
             acc[gi][j] = t;
           }
         }
@@ -975,6 +996,25 @@ __global__ void __launch_bounds__(EXACT ? NTHR_X : NTHR, 1)
 }
 
 // ------------------------------------------------------------------ host
+
+// tap (dy, dx) of the 5x5 grid holding distinct value i (see Args::dtap6)
+inline int tap6_index(int i) {
+  static const int idx[6] = {2 * 5 + 2, 2 * 5 + 1, 2 * 5 + 0, 1 * 5 + 1, 1 * 5 + 0, 0};
+  return idx[i];
+}
+
+// the exact stencil role reads six distinct taps: the 5x5 grid must be the
+// symmetric gaussian bit for bit
+inline bool taps_symmetric(const float* w) {
+  for (int dy = 0; dy < 5; ++dy)
+    for (int dx = 0; dx < 5; ++dx) {
+      const int p = dy < 2 ? 2 - dy : dy - 2, q = dx < 2 ? 2 - dx : dx - 2;
+      const int lo = p < q ? p : q, hi = p < q ? q : p;
+      const int i = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+      if (w[dy * 5 + dx] != w[tap6_index(i)]) return false;
+    }
+  return true;
+}
 
 size_t layout(int out_rows, Args* a) {
   const int R = out_rows + 6;
@@ -1182,6 +1222,7 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
   a.state_out = state_out;
   a.p = fp;
   for (int i = 0; i < 25; ++i) a.dtaps[i] = double(fp.taps[i]);
+  for (int i = 0; i < 6; ++i) a.dtap6[i] = double(fp.taps[tap6_index(i)]);
   a.skip = kn.pipe_skip;
   if (kn.band_scale > 0.0f) a.p.band_n *= kn.band_scale;  // tests / diagnostics only
   CUtensorMap map;
@@ -1218,7 +1259,7 @@ int entry(const fc_stage* sgray, const fc_stage* si, const fc_stage* sg, const f
                                        pitch, &fp)
                         : fast_params(sgray, si, sg, sthr, video, in_type, gray_in, out_type, d,
                                       pitch, &fp);
-  if (!ok) return -1;
+  if (!ok || (exact && !taps_symmetric(fp.taps))) return -1;
   return launch(fp, video, out, d, n_warm, state_in, state_out, stream, pitch, opitch, exact);
 }
 
