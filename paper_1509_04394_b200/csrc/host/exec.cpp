@@ -372,10 +372,15 @@ void Executor::run_device(const void* video, int in_type, void* out, int n_frame
         const bool misaligned = (reinterpret_cast<std::uintptr_t>(cur) & 15) != 0;
         const bool out_misaligned =
             dims_.width % 4 != 0 || (reinterpret_cast<std::uintptr_t>(dst) & 3) != 0;
-        if (opt_.variant != Variant::Exact && cur_type == FC_U8 && !gray_in &&
-            dims_.channels == 4 && (dims_.width % 16 != 0 || misaligned || out_misaligned) &&
-            fc_chain_pipe_applies(sgray, &rest[0], &rest[1], &rest[3], cur_type, gray_in,
-                                  dst_type, d, P)) {
+        // (the certified pipeline, or the exact one: variant "exact" or a chain
+        // outside the certified path)
+        if (cur_type == FC_U8 && !gray_in && dims_.channels == 4 &&
+            (dims_.width % 16 != 0 || misaligned || out_misaligned) &&
+            ((opt_.variant != Variant::Exact &&
+              fc_chain_pipe_applies(sgray, &rest[0], &rest[1], &rest[3], cur_type, gray_in,
+                                    dst_type, d, P)) ||
+             fc_chain_pipe2_exact_applies(sgray, &rest[0], &rest[1], &rest[3], cur_type,
+                                          gray_in, dst_type, d, P))) {
           const std::size_t vbytes = std::size_t(frames) * 4 * dims_.height * P;
           const std::size_t obytes =
               out_misaligned ? std::size_t(frames - warm) * dims_.height * P : 0;

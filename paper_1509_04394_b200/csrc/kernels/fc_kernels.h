@@ -117,6 +117,11 @@ int fc_fused_chain_pitched(const fc_stage* s_gray, const fc_stage* s_iir,
 int fc_chain_pipe_applies(const fc_stage* s_gray, const fc_stage* s_iir,
                           const fc_stage* s_gauss, const fc_stage* s_thr, int in_type,
                           int gray_in, int out_type, fc_dims d, int pitch);
+/* Would the exact frame-pair pipeline (fc_pipe2.cu, FP64 stencil role) take
+ * this chain with a video of row pitch `pitch`? */
+int fc_chain_pipe2_exact_applies(const fc_stage* s_gray, const fc_stage* s_iir,
+                                 const fc_stage* s_gauss, const fc_stage* s_thr, int in_type,
+                                 int gray_in, int out_type, fc_dims d, int pitch);
 /* The kernel the last fc_fused_chain* call on this thread ran. */
 const char* fc_last_chain_kernel(void);
 

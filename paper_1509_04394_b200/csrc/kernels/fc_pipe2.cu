@@ -1287,6 +1287,18 @@ extern "C" int fc_chain_pipe2_exact(const fc_stage* sgray, const fc_stage* si,
                         state_in, state_out, pitch, opitch, stream, true);
 }
 
+extern "C" int fc_chain_pipe2_exact_applies(const fc_stage* sgray, const fc_stage* si,
+                                            const fc_stage* sg, const fc_stage* sthr,
+                                            int in_type, int gray_in, int out_type, fc_dims d,
+                                            int pitch) {
+  using namespace fcpipe2;
+  FastParams fp;
+  alignas(16) static const unsigned char probe[16] = {};
+  return d.height >= 6 &&
+         exact_params(sgray, si, sg, sthr, probe, in_type, gray_in, out_type, d, pitch, &fp) &&
+         taps_symmetric(fp.taps);
+}
+
 extern "C" long long fc_pipe2_recheck_count(void) {
   unsigned long long v = 0;
   if (cudaMemcpyFromSymbol(&v, fcpipe2::g_rechecks2, sizeof v) != cudaSuccess) return -1;

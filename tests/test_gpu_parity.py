@@ -439,12 +439,14 @@ def test_pair_every_window_height_exact(fp, cuda, oracle, monkeypatch, out_rows,
 
 @pytest.mark.parametrize("out_rows", [0, 6, 14, 22, 29])
 @pytest.mark.parametrize("shape,th", [((256, 131, 7), 30.0), ((192, 432, 61), 40.0),
-                                      ((800, 600, 9), 20.0), ((64, 37, 5), 10.0)])
+                                      ((800, 600, 9), 20.0), ((64, 37, 5), 10.0),
+                                      ((196, 50, 6), 25.0)])
 def test_pair_exact_pipeline(fp, cuda, oracle, monkeypatch, out_rows, shape, th):
     """The exact frame-pair pipeline (variant "exact": FP64 gaussian in the
     reference's order, float Sobel, no certification) at several window
-    heights, frame heights that are not multiples of them and odd frame
-    counts: bit-exact, and it is the kernel that ran."""
+    heights, frame heights that are not multiples of them, odd frame counts
+    and a width that needs the pitched copy (196): bit-exact, and it is the
+    kernel that ran."""
     from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
     W, H, F = shape
     if out_rows > H:
