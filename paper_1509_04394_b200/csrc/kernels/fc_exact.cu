@@ -12,6 +12,8 @@
 // holds that stage's value at the clamped position.
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include <algorithm>
 #include <cstdint>
 
@@ -191,107 +193,165 @@ struct GaussW {
   double w[(2 * FC_MAX_GAUSS_RADIUS + 1) * (2 * FC_MAX_GAUSS_RADIUS + 1)];
 };
 
-// Exact FP64 gaussian (simulator.cpp:63-74): every thread computes four
-// consecutive pixels of a row from a double tile (one float->double
-// conversion per staged element), accumulating each pixel's 25 products in
-// the reference's dy-outer / dx-inner order.  CTA tile 64 x 16, frames looped.
-constexpr int GX = 64, GY = 16;
-
-template <int R>
-__global__ void __launch_bounds__(256) k_gaussian_x4(const float* __restrict__ in,
-                                                     float* __restrict__ out, GaussW gw,
-                                                     int W, int H, int F) {
-  constexpr int K = 2 * R + 1, SW = GX + 2 * R, SH = GY + 2 * R;  // SW even: 16-B rows
-  __shared__ __align__(16) double tile[SH][SW];
-  const int x0 = blockIdx.x * GX, y0 = blockIdx.y * GY;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const long long hw = (long long)W * H;
-  for (int t = blockIdx.z; t < F; t += gridDim.z) {
-    const float* f = in + t * hw;
-    for (int i = threadIdx.x; i < SW * SH; i += 256) {
-      const int sy = i / SW, sx = i - sy * SW;
-      const int gx = clampi(x0 + sx - R, 0, W - 1), gy = clampi(y0 + sy - R, 0, H - 1);
-      tile[sy][sx] = double(__ldg(f + (long long)gy * W + gx));
-    }
-    __syncthreads();
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int dy = 0; dy < K; ++dy) {
-      double v[4 + 2 * R + 1];
-      const double* row = &tile[ty + dy][4 * tx];
-#pragma unroll
-      for (int j = 0; j < (4 + 2 * R + 1) / 2; ++j) {
-        const double2 q = *reinterpret_cast<const double2*>(row + 2 * j);
-        v[2 * j] = q.x;
-        v[2 * j + 1] = q.y;
-      }
-#pragma unroll
-      for (int dx = 0; dx < K; ++dx)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j] = __fma_rn(gw.w[dy * K + dx], v[j + dx], acc[j]);
-    }
-    const int x = x0 + 4 * tx, y = y0 + ty;
-    if (y < H) {
-      float* o = out + t * hw + (long long)y * W + x;
-      if (x + 3 < W && (W & 3) == 0) {
-        __stcs(reinterpret_cast<float4*>(o),
-               make_float4(__double2float_rn(acc[0]), __double2float_rn(acc[1]),
-                           __double2float_rn(acc[2]), __double2float_rn(acc[3])));
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (x + j < W) o[j] = __double2float_rn(acc[j]);
-      }
-    }
-    __syncthreads();
+// fn(integral_constant<int, I>) for I = I0 .. N - 1, unrolled at compile time
+template <int I, int N, typename Fn>
+__device__ __forceinline__ void unroll_steps(Fn&& fn) {
+  if constexpr (I < N) {
+    fn(std::integral_constant<int, I>{});
+    unroll_steps<I + 1, N>(fn);
   }
 }
 
-// Sobel magnitude (simulator.cpp:75-83), four consecutive pixels per thread,
-// CTA tile 64 x 16, frames looped.
-__global__ void __launch_bounds__(256) k_gradient_x4(const float* __restrict__ in,
-                                                     float* __restrict__ out, int W, int H,
-                                                     int F) {
-  constexpr int SW = GX + 8, SH = GY + 2;  // columns x0-4 .. x0+67 (aligned loads)
-  __shared__ __align__(16) float tile[SH][SW];
-  const int x0 = blockIdx.x * GX, y0 = blockIdx.y * GY;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+// Row-marching unfused stencils (no shared memory, no CTA barrier): a thread
+// owns 4 consecutive columns of a band of RB rows and marches the band's rows
+// plus the halo, loading each input row once (L1-cached, clamped to the
+// frame: the stage's own per-stage clamp) and keeping the rows it still
+// needs in registers.
+constexpr int RB = 32;     // output rows per band
+constexpr int RTHR = 128;  // threads per CTA (512 columns)
+
+// 4 + 2P consecutive input columns x - P .. x + 3 + P of row y (clamped)
+template <int P>
+__device__ __forceinline__ void load_cols(const float* __restrict__ row, int x, int W,
+                                          bool interior, float (&v)[4 + 2 * P]) {
+  if (interior) {  // x - 4 .. x + 7 in three aligned float4 (W % 4 == 0)
+    const float4 a = __ldg(reinterpret_cast<const float4*>(row + x - 4));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(row + x));
+    const float4 c = __ldg(reinterpret_cast<const float4*>(row + x + 4));
+    const float w12[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int j = 0; j < 4 + 2 * P; ++j) v[j] = w12[4 - P + j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4 + 2 * P; ++j) v[j] = __ldg(row + clampi(x - P + j, 0, W - 1));
+  }
+}
+
+__device__ __forceinline__ void store4(float* __restrict__ o, int x, int W, bool vec,
+                                       float a, float b, float c, float d) {
+  if (vec) {
+    __stcs(reinterpret_cast<float4*>(o), make_float4(a, b, c, d));
+  } else {
+    const float m[4] = {a, b, c, d};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (x + j < W) o[j] = m[j];
+  }
+}
+
+// Exact FP64 gaussian (simulator.cpp:63-74).  Each loaded row r feeds the K
+// output rows g = r - R .. r + R that read it, as their tap row dy = r - g + R:
+// every output's 25 (K^2) products accumulate in the reference's dy-outer /
+// dx-inner order, and a step carries K x 4 independent DFMA chains.
+template <int R>
+__global__ void __launch_bounds__(RTHR) k_gaussian_rows(const float* __restrict__ in,
+                                                        float* __restrict__ out, GaussW gw,
+                                                        int W, int H, int F) {
+  constexpr int K = 2 * R + 1, NV = 4 + 2 * R;
+  const int x = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (x >= W) return;
+  const int y0 = blockIdx.y * RB, y1 = min(y0 + RB, H);
+  const bool interior = (W & 3) == 0 && x >= 4 && x + 8 <= W && R <= 4;
+  const bool vec = (W & 3) == 0 && x + 3 < W;
   const long long hw = (long long)W * H;
   for (int t = blockIdx.z; t < F; t += gridDim.z) {
     const float* f = in + t * hw;
-    for (int i = threadIdx.x; i < SW * SH; i += 256) {
-      const int sy = i / SW, sx = i - sy * SW;
-      const int gx = clampi(x0 + sx - 4, 0, W - 1), gy = clampi(y0 + sy - 1, 0, H - 1);
-      tile[sy][sx] = __ldg(f + (long long)gy * W + gx);
-    }
-    __syncthreads();
-    float v[3][12];  // rows y-1 .. y+1, columns x-4 .. x+7
+    float* o = out + t * hw;
+    double acc[K][4];  // output row g at ring index g % K
+    // steps r = y0 - R .. y1 - 1 + R in bodies of K (ring indices
+    // compile-time: step r uses ring slot (r + R - dy) % K for tap row dy,
+    // counted from the band start so the slots are fixed per body position)
+    auto step = [&](int r, auto pos_t) {
+      constexpr int POS = decltype(pos_t)::value;  // (r - (y0 - R)) % K
+      float vf[NV];
+      load_cols<R>(f + (long long)clampi(r, 0, H - 1) * W, x, W, interior, vf);
+      double v[NV];
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+      for (int j = 0; j < NV; ++j) v[j] = double(vf[j]);
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const float4 q = *reinterpret_cast<const float4*>(&tile[ty + r][4 * tx + 4 * j]);
-        v[r][4 * j] = q.x;
-        v[r][4 * j + 1] = q.y;
-        v[r][4 * j + 2] = q.z;
-        v[r][4 * j + 3] = q.w;
+      for (int dy = 0; dy < K; ++dy) {
+        // output row g = r + R - dy, ring slot (g - (y0 - 2R)) % K = (POS + 2R - dy) % K
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int gs = (POS + 2 * R - dy + K) % K;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          double tt = dy == 0 ? 0.0 : acc[gs][j];
+#pragma unroll
+          for (int dx = 0; dx < K; ++dx) tt = __fma_rn(gw.w[dy * K + dx], v[j + dx], tt);
+          acc[gs][j] = tt;
+        }
       }
-    float m[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      m[j] = sobel_op([&](int dx, int dy) { return v[dy + 1][4 + j + dx]; });
-    const int x = x0 + 4 * tx, y = y0 + ty;
-    if (y < H) {
-      float* o = out + t * hw + (long long)y * W + x;
-      if (x + 3 < W && (W & 3) == 0) {
-        __stcs(reinterpret_cast<float4*>(o), make_float4(m[0], m[1], m[2], m[3]));
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (x + j < W) o[j] = m[j];
+      // the row completing this step: g = r - R (its last tap row dy = 2R)
+      const int g = r - R;
+      if (g >= y0 && g < y1) {
+        const int gs = (POS + 2 * R - (K - 1) + K) % K;
+        store4(o + (long long)g * W + x, x, W, vec, __double2float_rn(acc[gs][0]),
+               __double2float_rn(acc[gs][1]), __double2float_rn(acc[gs][2]),
+               __double2float_rn(acc[gs][3]));
       }
+    };
+    int r = y0 - R;
+    const int rend = y1 + R;  // exclusive
+#pragma unroll 1
+    for (; r + K <= rend; r += K)
+      unroll_steps<0, K>([&](auto i_t) { step(r + decltype(i_t)::value, i_t); });
+    unroll_steps<0, K>([&](auto i_t) {
+      if (r + decltype(i_t)::value < rend) step(r + decltype(i_t)::value, i_t);
+    });
+  }
+}
+
+// Sobel magnitude (simulator.cpp:75-83) on 4 columns per thread, a 3-row
+// window in registers.
+__global__ void __launch_bounds__(RTHR) k_gradient_rows(const float* __restrict__ in,
+                                                        float* __restrict__ out, int W, int H,
+                                                        int F) {
+  const int x = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (x >= W) return;
+  const int y0 = blockIdx.y * RB, y1 = min(y0 + RB, H);
+  const bool interior = (W & 3) == 0 && x >= 4 && x + 8 <= W;
+  const bool vec = (W & 3) == 0 && x + 3 < W;
+  const long long hw = (long long)W * H;
+  for (int t = blockIdx.z; t < F; t += gridDim.z) {
+    const float* f = in + t * hw;
+    float* o = out + t * hw;
+    float w[3][6];  // rows at ring index r % 3, columns x - 1 .. x + 4
+    auto load = [&](int r, auto slot_t) {
+      constexpr int SL = decltype(slot_t)::value;
+      load_cols<1>(f + (long long)clampi(r, 0, H - 1) * W, x, W, interior, w[SL]);
+    };
+    auto emit = [&](int y, auto m_t) {  // rows y-1, y, y+1 at slots (M+2)%3, M, (M+1)%3
+      constexpr int M = decltype(m_t)::value;
+      float m[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        m[j] = sobel_op([&](int dx, int dy) {
+          return w[(M + 3 + dy) % 3][1 + j + dx];
+        });
+      store4(o + (long long)y * W + x, x, W, vec, m[0], m[1], m[2], m[3]);
+    };
+    // slot of row r: (r - (y0 - 1)) % 3; output row y uses rows y-1 .. y+1
+    load(y0 - 1, std::integral_constant<int, 0>{});
+    load(y0, std::integral_constant<int, 1>{});
+    int y = y0;
+#pragma unroll 1
+    for (; y + 3 <= y1; y += 3) {
+      load(y + 1, std::integral_constant<int, 2>{});
+      emit(y, std::integral_constant<int, 1>{});
+      load(y + 2, std::integral_constant<int, 0>{});
+      emit(y + 1, std::integral_constant<int, 2>{});
+      load(y + 3, std::integral_constant<int, 1>{});
+      emit(y + 2, std::integral_constant<int, 0>{});
     }
-    __syncthreads();
+    if (y < y1) {
+      load(y + 1, std::integral_constant<int, 2>{});
+      emit(y, std::integral_constant<int, 1>{});
+    }
+    if (y + 1 < y1) {
+      load(y + 2, std::integral_constant<int, 0>{});
+      emit(y + 1, std::integral_constant<int, 2>{});
+    }
   }
 }
 
@@ -642,15 +702,12 @@ int fc_stage_spatial(const fc_stage* s, const void* in, int in_type, void* out,
   long long hw = (long long)d.width * d.height, n = hw * d.frames;
   if (n == 0) return 0;
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  // 2-D stencil grid: 64 x 16 tiles, frames looped inside (z <= 65535) about
-  // 8 frames per CTA: many short CTAs keep the hardware scheduler's dynamic
-  // balance (a grid sized to one resident wave ran 16 % slower: SMs got 6 or
-  // 7 CTAs of 500 frames each), and the frame loop keeps the per-CTA setup
-  // amortised.
-  const int gx = (d.width + GX - 1) / GX, gy = (d.height + GY - 1) / GY;
-  auto frame_groups = [&](const void*, size_t) {
-    return int(std::max(1, std::min(65535, (d.frames + 7) / 8)));
-  };
+  // row-marching stencils: column groups x bands of RB rows x ~4 frames per
+  // CTA (frames looped inside, z <= 65535): many short CTAs keep the hardware
+  // scheduler's dynamic balance
+  auto rows_frame_groups = [&]() { return std::max(1, std::min(65535, (d.frames + 3) / 4)); };
+  const int quads = (d.width + 3) / 4;  // 4-column groups of a row
+  const int rthr = std::min(RTHR, (quads + 31) / 32 * 32);
   switch (s->op) {
     case FC_RGBA2GRAY:
       if (out_type != FC_F32) return -1;
@@ -671,9 +728,10 @@ int fc_stage_spatial(const fc_stage* s, const void* in, int in_type, void* out,
       GaussW w;
       const int K = 2 * s->g_radius + 1;
       for (int i = 0; i < K * K; ++i) w.w[i] = double(s->g_w[i]);
-#define FC_GK(R)                                                                       \
-  k_gaussian_x4<R><<<dim3(gx, gy, frame_groups((const void*)k_gaussian_x4<R>, 0)), 256, 0, \
-                     st>>>(f, o, w, d.width, d.height, d.frames)
+#define FC_GK(R)                                                                     \
+  k_gaussian_rows<R><<<dim3((quads + rthr - 1) / rthr, (d.height + RB - 1) / RB,         \
+                           rows_frame_groups()),                                         \
+                       rthr, 0, st>>>(f, o, w, d.width, d.height, d.frames)
       switch (s->g_radius) {
         case 0: FC_GK(0); break;
         case 1: FC_GK(1); break;
@@ -687,8 +745,10 @@ int fc_stage_spatial(const fc_stage* s, const void* in, int in_type, void* out,
     }
     case FC_GRADIENT:
       if (in_type != FC_F32 || out_type != FC_F32) return -1;
-      k_gradient_x4<<<dim3(gx, gy, frame_groups((const void*)k_gradient_x4, 0)), 256, 0, st>>>(
-          static_cast<const float*>(in), static_cast<float*>(out), d.width, d.height, d.frames);
+      k_gradient_rows<<<dim3((quads + rthr - 1) / rthr, (d.height + RB - 1) / RB,
+                             rows_frame_groups()),
+                        rthr, 0, st>>>(static_cast<const float*>(in), static_cast<float*>(out),
+                                       d.width, d.height, d.frames);
       return status();
     case FC_THRESHOLD:
     case FC_IDENTITY:
