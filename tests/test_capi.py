@@ -89,10 +89,23 @@ def test_executor_without_gpu_fails_loudly(fp):
         fp.Executor(p, plan)
 
 
-def test_out_of_scope_entry_points_report_input_error(fp):
+def test_malformed_calibration_csv_is_an_input_error(fp):
     L = fp.lib()
     out = ctypes.c_void_p()
     assert L.fp_calibrate_csv(b"n_kernels\n", ctypes.byref(out)) == fp.FP_ERR_INPUT
+
+
+def test_certified_params_of_the_spec_chain(fp):
+    """fp_certified_params (host only): the SPEC chain's normalised taps,
+    threshold and band; FP_ERR_INPUT for other chains."""
+    import json
+    c = fp.Pipeline(json.dumps(fp.spec_chain(64, 32, 4))).certified_params()
+    assert c["mstar"] == 16384.0 and abs(c["g1"] - 0.6065306663513184) < 1e-7
+    assert 0 < c["band_n"] < 1e-3 * c["mlo_n"]  # a band of ~1e-4 relative
+    spec = fp.spec_chain(64, 32, 4)
+    spec["kernels"] = spec["kernels"][:3]
+    with pytest.raises(fp.InputError):
+        fp.Pipeline(json.dumps(spec)).certified_params()
 
 
 CODEGEN_CASES = [
