@@ -51,16 +51,11 @@ namespace fcpipe2 {
 
 using namespace fccommon;
 
-#ifndef FP2_SPLIT
-#define FP2_SPLIT 1  // stencil warps per frame pair (2: row halves of the window + setmaxnreg;
-                     // measured 1.06-1.19 ms vs 0.80 ms: the IIR warps fall behind)
-#endif
-#ifndef FP2_SREG
-#define FP2_SREG 160  // setmaxnreg (SPLIT 2): stencil / IIR warpgroup registers
-#define FP2_IREG 96
-#endif
 constexpr int LC = 4;       // columns per stencil lane
-constexpr int WPF = FP2_SPLIT;  // stencil warps per frame pair
+// stencil warps per frame pair of the certified kernel (two warps splitting
+// the window rows, with setmaxnreg 160 / 96, measured 1.06-1.19 vs 0.80 ms:
+// the IIR warps fall behind; removed)
+constexpr int WPF = 1;
 constexpr int NPF = 4;      // frame pairs in flight in the stencil
 constexpr int NS = WPF * NPF;  // stencil warps
 constexpr int NI = 8;       // IIR warps (two per SM sub-partition)
@@ -557,13 +552,10 @@ __device__ __noinline__ bool exact_white(const Args& a, const unsigned char* bas
 template <int OUT>
 __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int sw, int lane,
                                              int bx, int by0) {
-  // SPLIT 2: warp sw marches the top (sw < NPF) or bottom half of the
-  // window's output rows (ceil(OUT/2) each; with OUT odd the middle row is
-  // computed by both and stored twice with identical values)
-  constexpr int OT = WPF == 2 ? (OUT + 1) / 2 : OUT;  // output rows of this warp
+  constexpr int OT = OUT;  // output rows of this warp: the whole window
   constexpr int NP = OT + 6;
-  const int r0 = sw >= NPF ? OUT - OT : 0;  // first window row of this warp's march
-  const int by = by0 + r0;                  // origin of the march
+  constexpr int r0 = 0;  // first window row of the march
+  const int by = by0;    // origin of the march
   const int W = a.W, H = a.H;
   const int n_out = rg.n - rg.n_warm;
   const int n_pairs = (n_out + 1) / 2;
@@ -983,13 +975,11 @@ __global__ void __launch_bounds__(EXACT ? NTHR_X : NTHR, 1)
   (void)R;
   const int sw = FP2_STENCIL_HI ? warp - NI : warp;  // stencil warp index (or < 0)
   if (sw >= 0 && sw < (EXACT ? NS_X : NS)) {
-    if (!EXACT && WPF == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(FP2_SREG));
     if constexpr (EXACT)
       exact_stencil_role<OUT>(a, fp2_rg, sw, lane, bx, by);
     else
       stencil_role<OUT>(a, fp2_rg, sw, lane, bx, by);
   } else {
-    if (!EXACT && WPF == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(FP2_IREG));
     iir_role<OUT, HALF, EXACT>(a, fp2_rg, FP2_STENCIL_HI ? warp : warp - NS, lane, bx, by, bx - tx0,
                         &tmap, tx0);
   }
