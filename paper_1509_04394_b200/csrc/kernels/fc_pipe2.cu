@@ -108,6 +108,7 @@ struct Args {
   float* seg_warm_out;
   int* fix_k;
   int* seg_k;
+  unsigned long long* prof;  // FUSEPLAN_PIPE_PROFILE: per-CTA {start, end} globaltimer (ns)
   int skip;    // timing experiments only (FUSEPLAN_PIPE_SKIP): 1 IIR math, 2 stencil math,
                // 4 no TMA, 8 no gray (IIR warps only hand off slots)
   int opitch;  // output row pitch in bytes (>= W, a multiple of 4)
@@ -146,6 +147,11 @@ template <bool EXACT = false>
 __device__ __forceinline__ void nb_arrive(int id) {
   constexpr unsigned n = EXACT ? NB_THREADS_X : NB_THREADS;
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 __device__ __forceinline__ void nb_sync_n(int id, unsigned n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -971,6 +977,7 @@ __global__ void __launch_bounds__(EXACT ? NTHR_X : NTHR, 1)
   }
   if (tid < 25) taps[tid] = double(a.p.taps[tid]);
   if (tid == 0) fp2_rg = rg;
+  if (a.prof && tid == 0) a.prof[2 * blockIdx.x] = globaltimer();
   __syncthreads();  // the only CTA-wide barrier: roles run decoupled from here
   (void)R;
   const int sw = FP2_STENCIL_HI ? warp - NI : warp;  // stencil warp index (or < 0)
@@ -983,6 +990,7 @@ __global__ void __launch_bounds__(EXACT ? NTHR_X : NTHR, 1)
     iir_role<OUT, HALF, EXACT>(a, fp2_rg, FP2_STENCIL_HI ? warp : warp - NS, lane, bx, by, bx - tx0,
                         &tmap, tx0);
   }
+  if (a.prof && lane == 0) atomicMax(&a.prof[2 * blockIdx.x + 1], globaltimer());
 }
 
 // ------------------------------------------------------------------ host
@@ -1220,8 +1228,37 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
   const int grid = cache.strips * cache.bands * cache.n_segs;
   KernelFn fn = kernel_for(cache.out_rows, fp.alpha_half != 0, exact);
   const int nthr = exact ? NTHR_X : NTHR;
+  if (kn.profile) {
+    cudaMalloc(&a.prof, sizeof(unsigned long long) * 2 * grid);
+    cudaMemsetAsync(a.prof, 0, sizeof(unsigned long long) * 2 * grid, st);
+  }
   fn<<<grid, nthr, cache.smem, st>>>(map, a);
   int rc = int(cudaGetLastError());
+  if (kn.profile && a.prof) {  // per-CTA spans (diagnostics)
+    std::vector<unsigned long long> h(size_t(2) * grid);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), a.prof, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost);
+    cudaFree(a.prof);
+    a.prof = nullptr;
+    unsigned long long t0 = ~0ull, t1 = 0;
+    double sum = 0, mx = 0, mn = 1e30;
+    for (int b = 0; b < grid; ++b) {
+      t0 = std::min(t0, h[2 * b]);
+      t1 = std::max(t1, h[2 * b + 1]);
+      const double span = double(h[2 * b + 1] - h[2 * b]) / 1e3;
+      sum += span;
+      mx = std::max(mx, span);
+      mn = std::min(mn, span);
+    }
+    std::fprintf(stderr, "fc_pipe2 out=%d segs=%d grid=%d exact=%d: kernel span %.1f us, CTA span "
+                 "avg %.1f min %.1f max %.1f us\n", cache.out_rows, cache.n_segs, grid, int(exact),
+                 double(t1 - t0) / 1e3, sum / grid, mn, mx);
+    if (kn.profile == 2)
+      for (int b = 0; b < grid; ++b)
+        std::fprintf(stderr, "  cta %4d win(%d,%d) start %+.2f us span %.1f us\n", b,
+                     (b % a.n_windows) % cache.strips, (b % a.n_windows) / cache.strips,
+                     double(h[2 * b] - t0) / 1e3, double(h[2 * b + 1] - h[2 * b]) / 1e3);
+  }
   if (rc == 0 && verify) {
     k_verify_segments<<<296, 256, 0, st>>>(a.seg_warm_out, a.seg_end, hwl, cache.n_segs,
                                            a.seg_k);
