@@ -208,7 +208,7 @@ def run_reference_arm(args, W, H, F, desc):
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sample / fps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (u8 in, u8 mask out)",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32/f64 (u8 in, u8 mask out)",
         "data": "synthetic counter-hash u8 RGBA video",
         "config": {"workload": desc, "sample_frames": sample, "chain": "SPEC K1..K5"},
         "mpix_per_s": fps * W * H / 1e6,
