@@ -251,8 +251,12 @@ __global__ void __launch_bounds__(RTHR) k_gaussian_rows(const float* __restrict_
   const int x = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   if (x >= W) return;
   const int y0 = blockIdx.y * RB, y1 = min(y0 + RB, H);
-  const bool interior = (W & 3) == 0 && x >= 4 && x + 8 <= W && R <= 4;
-  const bool vec = (W & 3) == 0 && x + 3 < W;
+  // vector loads / stores need 16-byte aligned planes (W % 4 == 0 keeps the
+  // rows aligned)
+  const bool al_in = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  const bool al_out = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  const bool interior = al_in && (W & 3) == 0 && x >= 4 && x + 8 <= W && R <= 4;
+  const bool vec = al_out && (W & 3) == 0 && x + 3 < W;
   const long long hw = (long long)W * H;
   for (int t = blockIdx.z; t < F; t += gridDim.z) {
     const float* f = in + t * hw;
@@ -310,8 +314,10 @@ __global__ void __launch_bounds__(RTHR) k_gradient_rows(const float* __restrict_
   const int x = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   if (x >= W) return;
   const int y0 = blockIdx.y * RB, y1 = min(y0 + RB, H);
-  const bool interior = (W & 3) == 0 && x >= 4 && x + 8 <= W;
-  const bool vec = (W & 3) == 0 && x + 3 < W;
+  const bool al_in = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  const bool al_out = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  const bool interior = al_in && (W & 3) == 0 && x >= 4 && x + 8 <= W;
+  const bool vec = al_out && (W & 3) == 0 && x + 3 < W;
   const long long hw = (long long)W * H;
   for (int t = blockIdx.z; t < F; t += gridDim.z) {
     const float* f = in + t * hw;
