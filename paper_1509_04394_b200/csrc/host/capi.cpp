@@ -372,14 +372,16 @@ fp_status fp_codegen(const fp_pipeline* p, const fp_device* d, const char* optio
       if (!g.global_aggregation) {
         using V = std::vector<std::string>;
         if (ops == V{"rgba2gray", "iir_temporal", "gaussian", "gradient", "threshold"}) {
-          kernel = "fcpipe::k_chain_pipe<OH, false> (F12345 frame pipeline; exact: k_chain_exact)";
-          src = "fc_pipe.cu / fc_exact.cu";
+          kernel = "fcpipe2::k_chain_pair (F12345 frame-pair pipeline, certified FP32 or exact "
+                   "FP64 stencil; fallback: k_chain_exact)";
+          src = "fc_pipe2.cu / fc_exact.cu";
         } else if (ops == V{"rgba2gray", "iir_temporal"}) {
           kernel = "k_gray_iir_stream / k_gray_iir (F12)";
           src = "fc_f12.cu / fc_exact.cu";
         } else if (ops == V{"gaussian", "gradient", "threshold"}) {
-          kernel = "fcpipe::k_chain_pipe<OH, true> (F345 frame pipeline; exact: k_gauss_grad_thr)";
-          src = "fc_pipe.cu / fc_exact.cu";
+          kernel = "fcpipe::k_chain_pipe<OH, true> (certified F345 row-pair pipeline); exact: "
+                   "fcpipe2::k_chain_pair on f32 planes (fallback: k_gauss_grad_thr)";
+          src = "fc_pipe.cu / fc_pipe2.cu / fc_exact.cu";
         } else {
           kernel = "per-stage kernels (k_rgba2gray, k_iir, k_gaussian<R>, k_gradient, "
                    "k_pointwise, k_box_mean)";

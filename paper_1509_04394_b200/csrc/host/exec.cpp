@@ -432,6 +432,7 @@ void Executor::run_device(const void* video, int in_type, void* out, int n_frame
                                              static_cast<const float*>(cur), dst, dst_type, d,
                                              int(opt_.variant), cur_max, st),
                    "F345 launch");
+        last_chain_ = fc_last_chain_kernel();
         cur_max = -1.0;
         break;
       case LaunchGroup::Stages:

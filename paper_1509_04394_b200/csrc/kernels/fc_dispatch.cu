@@ -33,6 +33,8 @@ extern "C" int fc_chain_pipe2_exact(const fc_stage* sgray, const fc_stage* si,
                                     int in_type, int gray_in, void* out, int out_type, fc_dims d,
                                     int n_warm, const float* state_in, float* state_out,
                                     int pitch, int opitch, void* stream);  // fc_pipe2.cu: exact
+extern "C" int fc_f345_pair_exact(const fc_stage* sg, const fc_stage* sthr, const float* in,
+                                  void* out, int out_type, fc_dims d, void* stream);
 extern "C" int fc_f345_pipe(const fc_stage* sg, const fc_stage* sthr, const float* in,
                             void* out, int out_type, fc_dims d, double in_max, void* stream);
 extern "C" long long fc_pipe_recheck_count(void);
@@ -108,8 +110,8 @@ extern "C" int fc_fused_chain_pitched(const fc_stage* sgray, const fc_stage* si,
   }
   // reference-exact: the frame-pair pipeline with the FP64 stencil role where
   // it applies (u8 RGBA in, 5x5 gaussian, {0, 255} byte mask), else the FP64
-  // tile march
-  {
+  // tile march (FUSEPLAN_PIPE_IMPL=3 forces the tiles)
+  if (fc_get_knobs()->pipe_impl != 3) {
     const int rc = fc_chain_pipe2_exact(sgray, si, sg, sthr, pitched ? pitched : video, in_type,
                                         gray_in, pitched_out ? pitched_out : out, out_type, d,
                                         n_warm, state_in, state_out, pitched ? video_pitch : 0,
@@ -179,7 +181,20 @@ extern "C" int fc_fused_gauss_grad_thr_v(const fc_stage* sg, const fc_stage* sgr
                                          void* stream) {
   if (variant != 1 && in_max > 0.0) {
     const int rc = fc_f345_pipe(sg, sthr, in, out, out_type, d, in_max, stream);
-    if (rc != -1) return rc;  // -1: parameters not covered -> exact
+    if (rc != -1) {  // -1: parameters not covered -> exact
+      g_last_chain = "certified FP32 row-pair pipeline on f32 planes (fc_pipe.cu, F345)";
+      return rc;
+    }
   }
+  // reference-exact: the exact frame-pair pipeline with the plane loader,
+  // else the FP64 tiles
+  if (fc_get_knobs()->pipe_impl != 3) {
+    const int rc = fc_f345_pair_exact(sg, sthr, in, out, out_type, d, stream);
+    if (rc != -1) {
+      g_last_chain = "exact FP64 frame-pair pipeline on f32 planes (fc_pipe2.cu, F345)";
+      return rc;
+    }
+  }
+  g_last_chain = "exact FP64 tiles on f32 planes (fc_exact.cu, F345)";
   return fc_fused_gauss_grad_thr(sg, sgrad, sthr, in, out, out_type, d, stream);
 }

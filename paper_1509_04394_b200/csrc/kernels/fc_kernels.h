@@ -183,7 +183,8 @@ typedef struct {
   int dbg_px_on, dbg_px[3]; /* FUSEPLAN_PIPE_DEBUG_PX=x,y,t */
   int f12_stream;     /* FUSEPLAN_F12_STREAM: force the streaming F12 kernel */
   int f12_legacy;     /* FUSEPLAN_F12_LEGACY: the per-pixel F12 kernel */
-  int pipe_impl;      /* FUSEPLAN_PIPE_IMPL: 0 auto, 1 row-pair pipe, 2 frame-pair pipe */
+  int pipe_impl;      /* FUSEPLAN_PIPE_IMPL: 0 auto, 1 row-pair pipe, 2 frame-pair pipe,
+                         3 no exact pipeline (FP64 tiles / k_chain_exact) */
   int pipe_out;       /* FUSEPLAN_PIPE_OUT: force the frame-pair window's output rows */
 } fc_knobs;
 

@@ -109,6 +109,7 @@ struct Args {
   int* fix_k;
   int* seg_k;
   unsigned long long* prof;  // FUSEPLAN_PIPE_PROFILE: per-CTA {start, end} globaltimer (ns)
+  const float* planes;       // SRC (F345): the f32 IIR planes [t][y][x] the group reads
   int skip;    // timing experiments only (FUSEPLAN_PIPE_SKIP): 1 IIR math, 2 stencil math,
                // 4 no TMA, 8 no gray (IIR warps only hand off slots)
   int opitch;  // output row pitch in bytes (>= W, a multiple of 4)
@@ -752,6 +753,80 @@ __device__ __forceinline__ void stencil_role(const Args& a, const Range& rg, int
   }
 }
 
+// ------------------------------------------------------------------ plane warps (F345)
+
+// The F345 group (gaussian + Sobel + threshold on the f32 planes of an
+// earlier group, e.g. the reference planner's `1-2,3-5`) on the exact
+// pipeline: the IIR role becomes a plane loader -- each lane owns 4 columns of
+// fixed window rows, loads them for both frames of a pair (float4 where the 4
+// columns lie inside the video, clamped scalars at its edges; the next pair
+// is loaded while the current one is stored) and writes the pair slot's frame
+// planes.  Stateless: no warm-up, time segments are independent.  (The
+// certified F345 stays on the row-pair pipeline's TMA ring: with the FP32
+// stencil this loader's one pair of lookahead is too little, DESIGN 4.4.)
+template <int OUT>
+__device__ __forceinline__ void plane_role(const Args& a, const Range& rg, int iw, int lane,
+                                           int bx, int by) {
+  constexpr int R = OUT + 6;
+  constexpr int NR = (R + NI - 1) / NI;
+  const int W = a.W, H = a.H;
+  const int n_out = rg.n;
+  const int n_pairs = (n_out + 1) / 2;
+  const int xl = bx + 4 * lane;
+  const bool vec = (W & 3) == 0 && xl >= 0 && xl + 3 <= W - 1 &&
+                   (reinterpret_cast<uintptr_t>(a.planes) & 15) == 0;
+  int cols[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) cols[j] = clampi(xl + j, 0, W - 1);
+  long long rowoff[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+    rowoff[r] = (long long)clampi(by + min(iw + NI * r, R - 1), 0, H - 1) * W;
+  const long long hw = (long long)W * H;
+  const float* base = a.planes + (long long)rg.f0 * hw;
+  const unsigned smem0 = smem_u32(fp2_smem);
+
+  auto load = [&](int u, float4 (&dst)[NR][2]) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      if (iw + NI * r >= R) continue;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int fr = 2 * u + c < n_out ? 2 * u + c : 2 * u;  // odd tail: {A, A}
+        const float* row = base + fr * hw + rowoff[r];
+        if (vec)
+          dst[r][c] = __ldg(reinterpret_cast<const float4*>(row + xl));
+        else
+          dst[r][c] = make_float4(__ldg(row + cols[0]), __ldg(row + cols[1]),
+                                  __ldg(row + cols[2]), __ldg(row + cols[3]));
+      }
+    }
+  };
+  float4 cur[NR][2], nxt[NR][2];
+  if (n_pairs > 0) load(0, cur);
+  int islot = 0;
+  for (int u = 0; u < n_pairs; ++u) {
+    if (u + 1 < n_pairs) load(u + 1, nxt);
+    if (u >= K2) nb_sync<true>(1 + islot);  // the stencil released pair u - K2
+    const unsigned sb = smem0 + a.off_iir + islot * a.iir_stride;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int p = iw + NI * r;
+      if (p >= R) continue;
+      const float4 A = cur[r][0], B = cur[r][1];
+      sts128f(sb + p * PROW + 16 * lane, A.x, A.y, A.z, A.w);  // frame planes
+      sts128f(sb + p * PROW + 512 + 16 * lane, B.x, B.y, B.z, B.w);
+    }
+    nb_arrive<true>(1 + K2 + islot);
+    if (++islot == K2) islot = 0;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      cur[r][0] = nxt[r][0];
+      cur[r][1] = nxt[r][1];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ exact stencil warps
 
 // Reference-exact stencil role (the EXACT pipeline, variant "exact"): for each
@@ -930,7 +1005,7 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
 
 // ------------------------------------------------------------------ kernel
 
-template <int OUT, bool HALF, bool EXACT>
+template <int OUT, bool HALF, bool EXACT, bool SRC>
 __global__ void __launch_bounds__(EXACT ? NTHR_X : NTHR, 1)
     k_chain_pair(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Args a) {
   constexpr int R = OUT + 6;
@@ -987,8 +1062,11 @@ __global__ void __launch_bounds__(EXACT ? NTHR_X : NTHR, 1)
     else
       stencil_role<OUT>(a, fp2_rg, sw, lane, bx, by);
   } else {
-    iir_role<OUT, HALF, EXACT>(a, fp2_rg, FP2_STENCIL_HI ? warp : warp - NS, lane, bx, by, bx - tx0,
-                        &tmap, tx0);
+    if constexpr (SRC)
+      plane_role<OUT>(a, fp2_rg, FP2_STENCIL_HI ? warp : warp - NS_X, lane, bx, by);
+    else
+      iir_role<OUT, HALF, EXACT>(a, fp2_rg, FP2_STENCIL_HI ? warp : warp - NS, lane, bx, by,
+                                 bx - tx0, &tmap, tx0);
   }
   if (a.prof && lane == 0) atomicMax(&a.prof[2 * blockIdx.x + 1], globaltimer());
 }
@@ -1044,12 +1122,14 @@ using KernelFn = void (*)(CUtensorMap, Args);
 
 #define FP2_OUT_LIST(X) X(6) X(10) X(14) X(18) X(22) X(26) X(29)  // 30 rows exceed 227 KB
 
-KernelFn kernel_for(int out_rows, bool half, bool exact) {
+KernelFn kernel_for(int out_rows, bool half, bool exact, bool src = false) {
   switch (out_rows) {
-#define FP2_CASE(N)                                                             \
-  case N:                                                                       \
-    return exact ? (half ? k_chain_pair<N, true, true> : k_chain_pair<N, false, true>) \
-                 : (half ? k_chain_pair<N, true, false> : k_chain_pair<N, false, false>);
+#define FP2_CASE(N)                                                                        \
+  case N:                                                                                  \
+    if (src) return k_chain_pair<N, true, true, true>; /* exact F345 on f32 planes */      \
+    return exact ? (half ? k_chain_pair<N, true, true, false> : k_chain_pair<N, false, true, false>) \
+                 : (half ? k_chain_pair<N, true, false, false>                             \
+                         : k_chain_pair<N, false, false, false>);
     FP2_OUT_LIST(FP2_CASE)
 #undef FP2_CASE
   }
@@ -1069,7 +1149,7 @@ constexpr int SEG_WARM = 48;  // IIR warm-up of a time segment (verified + fixed
 // frames at ~0.4 of a full frame).  Pick (OUT, segments) minimising the
 // busiest SM's load; ties go to the taller window.
 bool choose(int W, int H, int frames, bool segs_ok, int dev, int force, int force_segs,
-            PairPlan* pp) {
+            PairPlan* pp, bool stateless = false) {
   int sms = 0, optin = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -1086,8 +1166,8 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, int force, int forc
     const size_t smem = layout(o, nullptr);
     if (smem > size_t(optin) || o > H) continue;  // the last band must fit the video
     cudaError_t e = cudaSuccess;
-    for (int h = 0; h < 4 && e == cudaSuccess; ++h)
-      e = cudaFuncSetAttribute(kernel_for(o, (h & 1) != 0, (h & 2) != 0),
+    for (int h = 0; h < 5 && e == cudaSuccess; ++h)
+      e = cudaFuncSetAttribute(kernel_for(o, (h & 1) != 0, (h & 2) != 0, h == 4),
                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 0;
     if (e == cudaSuccess)
@@ -1110,11 +1190,11 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, int force, int forc
       // 15 segments); an empty trailing segment would march warm-up frames
       // past the end of its range
       const int nseg = L > 0 ? int((frames + L - 1) / L) : 1;
-      if (!force_segs && segs > 1 && L < 2 * SEG_WARM) break;
+      if (!force_segs && !stateless && segs > 1 && L < 2 * SEG_WARM) break;
       if (segs > 1 && L < 2) break;
       const long long ctas = windows * nseg;
       const long long per_busiest = (ctas + sms - 1) / sms;
-      const double cta_frames = double(L) + (segs > 1 ? 0.4 * SEG_WARM : 0.0);
+      const double cta_frames = double(L) + (segs > 1 && !stateless ? 0.4 * SEG_WARM : 0.0);
       const double cost = double(per_busiest) * (o + 6) * cta_frames * (1.0 - 1e-4 * o);
       if (cost < best) {
         best = cost;
@@ -1128,7 +1208,7 @@ bool choose(int W, int H, int frames, bool segs_ok, int dev, int force, int forc
     }
   }
   if (best >= 1e300 && force_segs)
-    return choose(W, H, frames, segs_ok, dev, force, 0, pp);
+    return choose(W, H, frames, segs_ok, dev, force, 0, pp, stateless);
   if (dbg && best < 1e300)
     std::fprintf(stderr, "fc_pipe2 choose: -> out=%d segs=%d seg_len=%d\n", pp->out_rows,
                  pp->n_segs, pp->seg_len);
@@ -1160,9 +1240,10 @@ SegScratch& seg_scratch(int dev, cudaStream_t st) {
   return all[{dev, st}];
 }
 
+// src: `in` are f32 planes (the exact F345 group: stateless, no TMA, no seam check)
 int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_warm,
            const float* state_in, float* state_out, void* stream, int pitch, int opitch,
-           bool exact) {
+           bool exact, bool src = false) {
   if (d.frames == 0) return 0;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1172,13 +1253,14 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
   // plans per (device, shape, frames, segment eligibility, forcing knobs): a
   // host thread driving several devices or executors does not re-plan (and
   // re-set the kernels' shared-memory attributes) on every launch
-  using Key = std::tuple<int, int, int, int, int, bool, int, int>;
+  using Key = std::tuple<int, int, int, int, int, bool, int, int, bool>;
   static thread_local std::map<Key, PairPlan> plans;
-  const Key key{dev, d.width, d.height, d.frames, n_warm, segs_ok, force_out, force_segs};
+  const Key key{dev, d.width, d.height, d.frames, n_warm, segs_ok, force_out, force_segs, src};
   auto it = plans.find(key);
   if (it == plans.end()) {
     PairPlan pp;
-    if (!choose(d.width, d.height, d.frames - n_warm, segs_ok, dev, force_out, force_segs, &pp))
+    if (!choose(d.width, d.height, d.frames - n_warm, segs_ok, dev, force_out, force_segs, &pp,
+                src))
       return -1;
     if (plans.size() > 256) plans.clear();
     it = plans.emplace(key, pp).first;
@@ -1197,9 +1279,10 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
   a.n_windows = cache.strips * cache.bands;
   a.n_segs = cache.n_segs;
   a.seg_len = cache.seg_len;
-  a.seg_warm = kn.pipe_seg_warm > 0 ? kn.pipe_seg_warm : SEG_WARM;
+  a.seg_warm = src ? 0 : (kn.pipe_seg_warm > 0 ? kn.pipe_seg_warm : SEG_WARM);
+  a.planes = src ? static_cast<const float*>(in) : nullptr;
   const long long hwl = (long long)d.width * d.height;
-  const bool verify = cache.n_segs > 1;
+  const bool verify = cache.n_segs > 1 && !src;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (verify) {
     SegScratch& sc = seg_scratch(dev, st);
@@ -1224,9 +1307,11 @@ int launch(const FastParams& fp, const void* in, void* out, fc_dims d, int n_war
   a.skip = kn.pipe_skip;
   if (kn.band_scale > 0.0f) a.p.band_n *= kn.band_scale;  // tests / diagnostics only
   CUtensorMap map;
-  if (!rgb_tensor_map(&map, in, d, BWB, cache.out_rows + 6, pitch ? pitch : d.width)) return -1;
+  std::memset(&map, 0, sizeof map);  // src: the plane warps load with LDG, no TMA
+  if (!src && !rgb_tensor_map(&map, in, d, BWB, cache.out_rows + 6, pitch ? pitch : d.width))
+    return -1;
   const int grid = cache.strips * cache.bands * cache.n_segs;
-  KernelFn fn = kernel_for(cache.out_rows, fp.alpha_half != 0, exact);
+  KernelFn fn = kernel_for(cache.out_rows, fp.alpha_half != 0, exact, src);
   const int nthr = exact ? NTHR_X : NTHR;
   if (kn.profile) {
     cudaMalloc(&a.prof, sizeof(unsigned long long) * 2 * grid);
@@ -1312,6 +1397,25 @@ extern "C" int fc_chain_pipe2_exact(const fc_stage* sgray, const fc_stage* si,
                                     int pitch, int opitch, void* stream) {
   return fcpipe2::entry(sgray, si, sg, sthr, video, in_type, gray_in, out, out_type, d, n_warm,
                         state_in, state_out, pitch, opitch, stream, true);
+}
+
+// The exact F345 group (FP64 gaussian in the reference's order, float Sobel,
+// m >= M*) on f32 planes: the exact frame-pair pipeline with the plane
+// loader role.  -1 when outside it (the caller runs the FP64 tiles).
+extern "C" int fc_f345_pair_exact(const fc_stage* sg, const fc_stage* sthr, const float* in,
+                                  void* out, int out_type, fc_dims d, void* stream) {
+  using namespace fcpipe2;
+  FastParams fp;
+  std::memset(&fp, 0, sizeof fp);
+  if (d.width % 4 != 0 || d.height < 6 || reinterpret_cast<uintptr_t>(out) % 4 != 0) return -1;
+  if (out_type != FC_U8 || sg->g_radius != 2 || !(sthr->th > 0.0f)) return -1;
+  if (sthr->white != 255.0f || sthr->black != 0.0f) return -1;
+  std::memcpy(fp.taps, sg->g_w, sizeof fp.taps);
+  if (!taps_symmetric(fp.taps)) return -1;
+  fp.th_val = sthr->th;
+  fp.mstar = threshold_mstar(sthr->th);
+  fp.mlo = std::nextafter(fp.mstar, 0.0f);
+  return launch(fp, in, out, d, 0, nullptr, nullptr, stream, 0, 0, true, true);
 }
 
 extern "C" int fc_chain_pipe2_exact_applies(const fc_stage* sgray, const fc_stage* si,

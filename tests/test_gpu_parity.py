@@ -488,6 +488,40 @@ def test_pair_exact_segments_and_carry(fp, cuda, oracle, monkeypatch, segs, seg_
     np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("tiles", [False, True])
+@pytest.mark.parametrize("out_rows,segs", [(0, 0), (6, 0), (14, 3), (29, 0), (22, 7)])
+@pytest.mark.parametrize("shape,th", [((256, 131, 7), 30.0), ((192, 432, 61), 40.0),
+                                      ((800, 600, 9), 20.0), ((64, 37, 5), 10.0),
+                                      ((196, 50, 6), 25.0), ((98, 40, 4), 15.0)])
+def test_f345_exact_pipeline(fp, cuda, oracle, monkeypatch, tiles, out_rows, segs, shape, th):
+    """The exact F345 group of the reference planner's `1-2,3-5` (gaussian +
+    Sobel + threshold on the f32 IIR planes, variant "exact") on the exact
+    frame-pair pipeline with the plane-loader role -- window heights, time
+    segments (stateless), odd frame counts, widths that are not multiples of
+    128 -- and, forced, on the FP64 tiles (and for a width the pipeline does
+    not take, 98): bit-exact either way, and the expected kernel ran."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    W, H, F = shape
+    if out_rows > H:
+        pytest.skip("window taller than the video")
+    if out_rows:
+        monkeypatch.setenv("FUSEPLAN_PIPE_OUT", str(out_rows))
+    if segs:
+        monkeypatch.setenv("FUSEPLAN_PIPE_SEGS", str(segs))
+    if tiles:
+        monkeypatch.setenv("FUSEPLAN_PIPE_IMPL", "3")
+    pipe = spec_chain(W, H, F, th=th)
+    v = hash_video_u8(F, 4, H, W, 310 + out_rows + segs)
+    want = oracle.orc_chain(pipe, v)
+    out, ex = run(fp, pipe, v, {"force_partition": "1-2,3-5"}, variant="exact", torch_dev=cuda)
+    kern = ex.describe()["last_chain_kernel"]
+    if tiles or W % 4:
+        assert "exact FP64 tiles on f32 planes" in kern, kern
+    else:
+        assert "exact FP64 frame-pair pipeline on f32 planes" in kern, kern
+    np.testing.assert_array_equal(out, want)
+
+
 @pytest.mark.parametrize("shape", [(128, 64, 1), (128, 64, 2), (256, 30, 3), (1024, 12, 7)])
 @pytest.mark.parametrize("segs", [0, 2, 5])
 def test_pipe_tiny_frame_counts_exact(fp, cuda, oracle, monkeypatch, shape, segs):
