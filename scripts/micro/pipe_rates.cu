@@ -136,6 +136,29 @@ __device__ __forceinline__ void step(float* a, uint32_t* u, float x, float y, ui
     if (OP == 38) {  // mixed f16 x f16 + f32 (sm_100 FFMA with f16 sources)
       asm volatile("{.reg .f16 h;\n mov.b32 {h, _}, %1;\n fma.rn.f32.f16 %0, h, h, %0;}" : "+f"(a[i]) : "r"(s));
     }
+    if ((OP == 39 || OP == 40) && (i & 7) == 0) {  // 3 DFMA + 1 F2F (f32 -> f64 / f64 -> f32)
+#pragma unroll
+      for (int k = 0; k < 6; k += 2)
+        asm volatile(
+            "{.reg .f64 p, q;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %3};\n"
+            " fma.rn.f64 p, p, q, q;\n mov.b64 {%0, %1}, p;}"
+            : "+f"(a[i + k]), "+f"(a[i + k + 1])
+            : "f"(x), "f"(y));
+      if (OP == 39)
+        asm volatile("{.reg .f64 p;\n cvt.f64.f32 p, %0;\n mov.b64 {%0, %1}, p;}"
+                     : "+f"(a[i + 6]), "+f"(a[i + 7]));
+      else
+        asm volatile("{.reg .f64 p;\n mov.b64 p, {%0, %1};\n cvt.rn.f32.f64 %0, p;}"
+                     : "+f"(a[i + 6]), "+f"(a[i + 7]));
+    }
+    if (OP == 41 && (i & 1) == 0) {  // DFMA + IADD interleaved
+      asm volatile(
+          "{.reg .f64 p, q;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %3};\n"
+          " fma.rn.f64 p, p, q, q;\n mov.b64 {%0, %1}, p;}"
+          : "+f"(a[i]), "+f"(a[i + 1])
+          : "f"(x), "f"(y));
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(u[i]) : "r"(s));
+    }
     if (OP == 27 && (i & 1) == 0) {  // FFMA2 + SHFL
       asm volatile(
           "{.reg .b64 p, q, r;\n mov.b64 p, {%0, %1};\n mov.b64 q, {%2, %2};\n mov.b64 r, {%3, %3};\n"
@@ -233,5 +256,8 @@ int main() {
   run<36>("IADD3 (2 adds)", CH, 1, out, cyc);
   run<37>("SHF funnel", CH, 1, out, cyc);
   run<38>("FFMA f32.f16", CH, 1, out, cyc);
+  run<39>("3 DFMA + F2F.F64.F32", CH / 2, 1, out, cyc);
+  run<40>("3 DFMA + F2F.F32.F64", CH / 2, 1, out, cyc);
+  run<41>("DFMA + IADD", CH, 1, out, cyc);
   return 0;
 }
