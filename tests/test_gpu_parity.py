@@ -626,3 +626,33 @@ def test_certified_pipeline_any_width_and_base(fp, cuda, oracle, shape, offset):
     kern = ex.describe()["last_chain_kernel"]
     assert "certified" in kern
     assert ("pitched" in kern) == (W % 16 != 0 or offset != 0)
+
+
+def _fuzz_cases(n, seed):
+    rng = np.random.default_rng(seed)
+    for i in range(n):
+        big = i % 5 == 0
+        W = int(rng.integers(4, 1100 if big else 520))
+        H = int(rng.integers(6, 700 if big else 260))
+        F = int(rng.integers(1, 12 if big else 48))
+        alpha = float(rng.choice([0.5, 0.5, 0.25, 0.8125, 0.37]))
+        sigma = float(rng.choice([1.0, 1.0, 0.7, 1.6]))
+        th = float(rng.choice([8.0, 20.0, 45.0, 128.0]))
+        yield i, (W, H, F, alpha, sigma, th, int(rng.integers(1 << 30)))
+
+
+@pytest.mark.parametrize("part,variant", [("1-5", "auto"), ("1-5", "exact"),
+                                          ("1-2,3-5", "auto"), ("1-2,3-5", "exact")])
+@pytest.mark.parametrize("case", list(_fuzz_cases(40, 4242)), ids=lambda c: f"c{c[0]}")
+def test_fuzz_shapes_every_pipeline(fp, cuda, oracle, part, variant, case):
+    """Random frame sizes (any width / height, 1-47 frames), IIR alphas,
+    gaussian sigmas and thresholds through every fused pipeline the executor
+    routes to (certified / exact frame-pair, row-pair F345, exact F345 on
+    planes, the FP64 tile fallbacks for shapes outside them): bit-exact."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    _, (W, H, F, alpha, sigma, th, seed) = case
+    pipe = spec_chain(W, H, F, alpha=alpha, sigma=sigma, th=th)
+    v = hash_video_u8(F, 4, H, W, seed)
+    want = oracle.orc_chain(pipe, v)
+    out, ex = run(fp, pipe, v, {"force_partition": part}, variant=variant, torch_dev=cuda)
+    np.testing.assert_array_equal(out, want, err_msg=ex.describe()["last_chain_kernel"])
