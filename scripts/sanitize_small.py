@@ -7,7 +7,8 @@ import torch
 from paper_1509_04394_b200 import fuseplan as fp
 for (W, H, F, part, variant) in [(136, 61, 9, "1-5", "auto"), (136, 61, 9, "1-5", "exact"),
                                  (192, 96, 130, "1-5", "auto"), (196, 50, 6, "1-5", "exact"),
-                                 (136, 61, 9, "1,2,3,4,5", "exact"), (136, 61, 9, "1-2,3-5", "auto")]:
+                                 (136, 61, 9, "1,2,3,4,5", "exact"), (136, 61, 9, "1-2,3-5", "auto"),
+                                 (136, 61, 9, "1-2,3-5", "exact"), (196, 50, 7, "1-2,3-5", "exact")]:
     pipe = fp.Pipeline(json.dumps(fp.spec_chain(W, H, F, th=30.0)))
     ex = fp.Executor(pipe, fp.Plan(pipe, fp.Device.load("b200"), {"force_partition": part}),
                      variant=variant)
