@@ -131,6 +131,24 @@ fp_status fp_exec_state_planes(const fp_exec* e, int* n_planes);
 fp_status fp_exec_run(fp_exec* e, const void* video, int in_type, void* out,
                       int flags, void* stream);
 
+/* CUDA graph of a whole device-buffer run (fp_exec_run with
+ * FP_EXEC_DEVICE_PTRS) on fixed buffers: the launches of one run (for small
+ * frames several per run: time segments, seam check, fix-up) replay with one
+ * cudaGraphLaunch.  fp_exec_graph_create runs the pipeline once uncaptured
+ * (out is written), then captures a second run on `stream` (NULL: a
+ * temporary non-blocking stream; the legacy default stream cannot capture)
+ * and instantiates it.  Refill `video` in place between launches; the graph
+ * always reads `video` and writes `out`.  fp_exec_graph_launch is
+ * asynchronous on `stream` (NULL = the legacy default stream).  The
+ * executor must outlive its graphs (they use its scratch buffers), and one
+ * executor's graph launches must not overlap each other or its runs.
+ * fp_exec_graph_free synchronises the graph's device. */
+typedef struct fp_graph fp_graph;
+fp_status fp_exec_graph_create(fp_exec* e, const void* video, int in_type, void* out,
+                               void* stream, fp_graph** graph);
+fp_status fp_exec_graph_launch(fp_graph* g, void* stream);
+void fp_exec_graph_free(fp_graph* g);
+
 /* Frame-range run on device buffers, for T-sharding: video holds n_frames
  * frames; the first n_warm only advance the IIR state (no output); out gets
  * n_frames - n_warm frames.  state_in (may be NULL = restart the recurrence

@@ -47,6 +47,14 @@ struct fp_exec {
   std::unique_ptr<Executor> ex;
 };
 
+struct fp_graph {
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t capture_stream = nullptr;  // keys the launchers' scratch the graph uses
+  int device = 0;
+};
+
+extern "C" void fc_release_stream_scratch(int device, void* stream);
+
 namespace {
 
 constexpr int kTrackPts = 23;
@@ -725,6 +733,54 @@ fp_status fp_exec_run(fp_exec* e, const void* video, int in_type, void* out, int
     else
       e->ex->run_host(video, in_type, out);
   });
+}
+
+fp_status fp_exec_graph_create(fp_exec* e, const void* video, int in_type, void* out,
+                               void* stream, fp_graph** graph) {
+  return guarded([&] {
+    need(e && video && out && graph);
+    require(in_type == FP_ELEM_U8 || in_type == FP_ELEM_F32, ErrorKind::Input,
+            "in_type must be FP_ELEM_U8 or FP_ELEM_F32");
+    cuda_ok(cudaSetDevice(e->ex->device()), "cudaSetDevice");
+    std::unique_ptr<fp_graph, void (*)(fp_graph*)> g(new fp_graph, fp_exec_graph_free);
+    g->device = e->ex->device();
+    cuda_ok(cudaStreamCreateWithFlags(&g->capture_stream, cudaStreamNonBlocking),
+               "capture stream");
+    // the capture stream starts after the caller's stream's pending work
+    if (stream) {
+      cudaEvent_t ev;
+      cuda_ok(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+      cudaEventRecord(ev, static_cast<cudaStream_t>(stream));
+      cudaStreamWaitEvent(g->capture_stream, ev, 0);
+      cudaEventDestroy(ev);
+    }
+    g->exec = static_cast<cudaGraphExec_t>(e->ex->capture(video, in_type, out,
+                                                           g->capture_stream));
+    *graph = g.release();
+  });
+}
+
+fp_status fp_exec_graph_launch(fp_graph* g, void* stream) {
+  return guarded([&] {
+    need(g && g->exec);
+    cuda_ok(cudaSetDevice(g->device), "cudaSetDevice");
+    cuda_ok(cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)), "graph launch");
+  });
+}
+
+void fp_exec_graph_free(fp_graph* g) {
+  if (!g) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(g->device);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->capture_stream) {
+    cudaDeviceSynchronize();  // replays in flight on any stream use the scratch
+    fc_release_stream_scratch(g->device, g->capture_stream);
+    cudaStreamDestroy(g->capture_stream);
+  }
+  cudaSetDevice(cur);
+  delete g;
 }
 
 fp_status fp_exec_run_range(fp_exec* e, const void* video, int in_type, void* out,

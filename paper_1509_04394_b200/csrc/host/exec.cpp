@@ -229,6 +229,30 @@ int Executor::converge(const void* video, int in_type, int n_frames, const float
   return k;
 }
 
+void* Executor::capture(const void* video, int in_type, void* out, void* stream) {
+  require(stream != nullptr, ErrorKind::Input, "capture needs a non-default stream");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  run_device(video, in_type, out, dims_.frames, 0, nullptr, nullptr, st);  // settle lazies
+  cuda_check(cudaStreamSynchronize(st), "capture warm-up");
+  cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+  try {
+    run_device(video, in_type, out, dims_.frames, 0, nullptr, nullptr, st);
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(st, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraph_t g = nullptr;
+  cuda_check(cudaStreamEndCapture(st, &g), "end capture");
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  cuda_check(e, "graph instantiate");
+  return exec;
+}
+
 Executor::~Executor() {
   if (pitched_) cudaFree(pitched_);
   if (k_dev_) cudaFree(k_dev_);

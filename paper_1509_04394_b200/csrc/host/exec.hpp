@@ -78,6 +78,15 @@ class Executor {
   int converge(const void* video, int in_type, int n_frames, const float* s_true,
                const float* s_warm, void* stream);
 
+  // CUDA graph of one whole run on fixed device buffers (run_device over all
+  // frames): one uncaptured run first (every lazy allocation, plan and
+  // kernel attribute is settled outside the capture), then the run captured
+  // on `stream` and instantiated.  Returns the cudaGraphExec_t; replays
+  // reuse the buffers, including the launchers' per-stream scratch of
+  // `stream` -- so the caller owns `stream` for the graph's lifetime.
+  void* capture(const void* video, int in_type, void* out, void* stream);
+  int device() const { return device_; }
+
   std::string describe() const;  // JSON: launch groups and kernels
   std::int64_t launches_per_run() const;
 

@@ -143,6 +143,14 @@ extern "C" int fc_fused_chain(const fc_stage* sgray, const fc_stage* si,
 
 extern "C" const char* fc_last_chain_kernel(void) { return g_last_chain; }
 
+extern "C" void fc_pipe_release_scratch(int device, void* stream);
+extern "C" void fc_pipe2_release_scratch(int device, void* stream);
+// the time-segment scratch both pipelines keep per (device, stream)
+extern "C" void fc_release_stream_scratch(int device, void* stream) {
+  fc_pipe_release_scratch(device, stream);
+  fc_pipe2_release_scratch(device, stream);
+}
+
 // Would the certified frame pipeline take this chain with a video of row
 // pitch `pitch` (values only: the pointer alignment is the caller's)?
 extern "C" int fc_chain_pipe_applies(const fc_stage* sgray, const fc_stage* si,

@@ -1130,11 +1130,31 @@ struct SegScratch {
   float* dbg_px = nullptr;
 };
 
-SegScratch& seg_scratch(int dev, cudaStream_t st) {
+// per (device, stream): launches on one stream are ordered, so they may share
+std::mutex& seg_mu() {
   static std::mutex mu;
+  return mu;
+}
+std::map<std::pair<int, cudaStream_t>, SegScratch>& seg_all() {
   static std::map<std::pair<int, cudaStream_t>, SegScratch> all;
-  std::lock_guard<std::mutex> lock(mu);
-  return all[{dev, st}];
+  return all;
+}
+
+SegScratch& seg_scratch(int dev, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(seg_mu());
+  return seg_all()[{dev, st}];
+}
+
+// frees a stream's scratch (a CUDA graph captured on it is gone; the caller
+// synchronised the device)
+void release_scratch(int dev, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(seg_mu());
+  auto it = seg_all().find({dev, st});
+  if (it == seg_all().end()) return;
+  if (it->second.buf) cudaFree(it->second.buf);
+  if (it->second.k) cudaFree(it->second.k);
+    if (it->second.dbg_px) cudaFree(it->second.dbg_px);
+  seg_all().erase(it);
 }
 
 // Shared launcher of both modes (src_f32: F345 from f32 planes).
@@ -1301,6 +1321,10 @@ int launch_pipe(bool src_f32, const FastParams& fp, const void* in, void* out, f
 }  // namespace FP_NAMESPACE
 
 using namespace FP_NAMESPACE;
+
+extern "C" void fc_pipe_release_scratch(int device, void* stream) {
+  release_scratch(device, static_cast<cudaStream_t>(stream));
+}
 
 // pitch: the video's row pitch in bytes (0 = width); the planes stay
 // [t][4][H][pitch].  -1: the chain or the layout is outside the certified path.

@@ -1233,11 +1233,30 @@ struct SegScratch {
   int* k = nullptr;
 };
 
-SegScratch& seg_scratch(int dev, cudaStream_t st) {
+// per (device, stream): launches on one stream are ordered, so they may share
+std::mutex& seg_mu() {
   static std::mutex mu;
+  return mu;
+}
+std::map<std::pair<int, cudaStream_t>, SegScratch>& seg_all() {
   static std::map<std::pair<int, cudaStream_t>, SegScratch> all;
-  std::lock_guard<std::mutex> lock(mu);
-  return all[{dev, st}];
+  return all;
+}
+
+SegScratch& seg_scratch(int dev, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(seg_mu());
+  return seg_all()[{dev, st}];
+}
+
+// frees a stream's scratch (a CUDA graph captured on it is gone; the caller
+// synchronised the device)
+void release_scratch(int dev, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(seg_mu());
+  auto it = seg_all().find({dev, st});
+  if (it == seg_all().end()) return;
+  if (it->second.buf) cudaFree(it->second.buf);
+  if (it->second.k) cudaFree(it->second.k);
+  seg_all().erase(it);
 }
 
 // src: `in` are f32 planes (the exact F345 group: stateless, no TMA, no seam check)
@@ -1428,6 +1447,10 @@ extern "C" int fc_chain_pipe2_exact_applies(const fc_stage* sgray, const fc_stag
   return d.height >= 6 &&
          exact_params(sgray, si, sg, sthr, probe, in_type, gray_in, out_type, d, pitch, &fp) &&
          taps_symmetric(fp.taps);
+}
+
+extern "C" void fc_pipe2_release_scratch(int device, void* stream) {
+  fcpipe2::release_scratch(device, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" long long fc_pipe2_recheck_count(void) {

@@ -95,6 +95,9 @@ def lib() -> ctypes.CDLL:
         "fp_exec_state_planes": ([P, ctypes.POINTER(ctypes.c_int)], I),
         "fp_exec_run": ([P, P, I, P, I, P], I),
         "fp_exec_run_range": ([P, P, I, P, I, I, P, P, P], I),
+        "fp_exec_graph_create": ([P, P, I, P, P, PP], I),
+        "fp_exec_graph_launch": ([P, P], I),
+        "fp_exec_graph_free": ([P], V),
         "fp_exec_describe": ([P, PP], I),
         "fp_certified_params": ([P, PP], I),
         "fp_exec_run_file": ([P, S, S], I),
@@ -384,6 +387,29 @@ class Executor(_Handle):
                                  out.ctypes.data, FP_EXEC_HOST_PTRS, None))
         return out
 
+    def capture(self, video, out=None, stream=None) -> "Graph":
+        """fp_exec_graph_create: a CUDA graph of one whole run on these device
+        buffers (runs once uncaptured, then captures).  Refill `video` in place
+        and call Graph.launch() to re-run; the result lands in Graph.out."""
+        torch = _torch()
+        W, H, F, C = self.pipeline.dims
+        if not (type(video).__module__.startswith("torch") and video.is_cuda):
+            raise InputError("capture needs a CUDA video tensor")
+        if tuple(video.shape) != (F, C, H, W) or not video.is_contiguous():
+            raise InputError(f"video must be a contiguous {(F, C, H, W)} tensor")
+        if out is None:
+            out = torch.empty((F, H, W), device=video.device,
+                              dtype=torch.uint8 if self.out_elem == FP_ELEM_U8
+                              else torch.float32)
+        else:
+            self._check_out(out, (F, H, W), True, video.device)
+        stream = _stream_handle(torch.cuda.current_stream(video.device)
+                                if stream is None else stream)
+        g = ctypes.c_void_p()
+        _check(lib().fp_exec_graph_create(self.ptr, video.data_ptr(), self._elem(video.dtype),
+                                          out.data_ptr(), stream, ctypes.byref(g)))
+        return Graph(self, g, video, out)
+
     def converge(self, video, s_true, s_warm, stream=None) -> int:
         """fp_exec_converge: how many leading frames of a shard (CUDA video
         [n, C, H, W]) that ran from s_warm differ from a run from s_true."""
@@ -499,6 +525,33 @@ def hash_video_u8(frames: int, channels: int, height: int, width: int, seed: int
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         z = z ^ (z >> np.uint64(31))
     return (z >> np.uint64(56)).astype(np.uint8)
+
+
+class Graph:
+    """A captured run (Executor.capture): launch() replays it on the captured
+    video / out buffers, asynchronously on `stream` (default: the current
+    torch stream).  Holds the executor and the buffers alive."""
+
+    def __init__(self, ex, handle, video, out):
+        self.ex, self.ptr, self.video, self.out = ex, handle, video, out
+
+    def launch(self, stream=None):
+        torch = _torch()
+        st = _stream_handle(torch.cuda.current_stream(self.video.device)
+                            if stream is None else stream)
+        _check(lib().fp_exec_graph_launch(self.ptr, st))
+        return self.out
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            lib().fp_exec_graph_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def spec_chain(width: int, height: int, frames: int, alpha: float = 0.5,

@@ -656,3 +656,36 @@ def test_fuzz_shapes_every_pipeline(fp, cuda, oracle, part, variant, case):
     want = oracle.orc_chain(pipe, v)
     out, ex = run(fp, pipe, v, {"force_partition": part}, variant=variant, torch_dev=cuda)
     np.testing.assert_array_equal(out, want, err_msg=ex.describe()["last_chain_kernel"])
+
+
+@pytest.mark.parametrize("shape,part,variant", [((192, 432, 600), "1-5", "auto"),
+                                                ((192, 432, 120), "1-5", "exact"),
+                                                ((136, 61, 40), "1-5", "auto"),
+                                                ((256, 96, 50), "1-2,3-5", "auto"),
+                                                ((128, 64, 30), "1,2,3,4,5", "auto")])
+def test_graph_capture_replay(fp, cuda, oracle, shape, part, variant):
+    """A run captured as a CUDA graph (fp_exec_graph_create; config 1 takes
+    three launches: time segments, seam check, fix-up) replays bit-exact, and
+    a replay after refilling the video in place gives the new video's mask."""
+    import torch
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    W, H, F = shape
+    pipe = spec_chain(W, H, F, th=30.0)
+    p = fp.Pipeline(json.dumps(pipe))
+    ex = fp.Executor(p, fp.Plan(p, fp.Device.load("b200"), {"force_partition": part}),
+                     variant=variant)
+    v1 = hash_video_u8(F, 4, H, W, 11)
+    v2 = hash_video_u8(F, 4, H, W, 12)
+    dv = torch.from_numpy(v1).to(cuda)
+    g = ex.capture(dv)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(g.out.cpu().numpy().astype(np.float32),
+                                  oracle.orc_chain(pipe, v1))
+    g.out.zero_()
+    dv.copy_(torch.from_numpy(v2))
+    g.launch()
+    g.launch()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(g.out.cpu().numpy().astype(np.float32),
+                                  oracle.orc_chain(pipe, v2))
+    g.close()
