@@ -52,7 +52,7 @@ CUDA_SRCS = ["kernels/fc_exact.cu", "kernels/fc_pipe.cu", "kernels/fc_pipe2.cu",
              "kernels/fc_track.cu", "kernels/fc_tiled.cu", "kernels/fc_shard.cu",
              "kernels/fc_dispatch.cu"]
 HEADERS = ["kernels/fc_pipe.cu", "host/exec.hpp", "host/video.hpp",
-           "kernels/fc_kernels.h", "kernels/fc_common.cuh"]
+           "kernels/fc_kernels.h", "kernels/fc_common.cuh", "kernels/fc_sobel.cuh"]
 PUBLIC_HEADERS = ["fuseplan.h", "fuseplan/fuseplan.hpp", "fuseplan/video.hpp",
                   "fuseplan/simulator.hpp"]
 

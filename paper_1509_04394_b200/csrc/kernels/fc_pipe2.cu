@@ -46,6 +46,7 @@
 #include <vector>
 
 #include "fc_common.cuh"
+#include "fc_sobel.cuh"
 
 namespace fcpipe2 {
 
@@ -945,33 +946,11 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
             rm[i] = ytop ? rc[i] : gq[(QM + 4) % 5][i];
             rp[i] = ybot ? rc[i] : gq[(QM + 1) % 5][i];
           }
-          // the reference's float Sobel (simulator.cpp:75-83) on column pairs
-          // in packed f32x2 ops, each lane of a pair rounded exactly as the
-          // scalar op: a + 2 b == FMA(2, b, a) and a - b == FMA(-1, b, a)
-          // (2 b and -b are exact)
-          // S_i = (rm_i + 2 rc_i) + rp_i; gx_j = S_{j+2} - S_j
-          float2 S[3];
-#pragma unroll
-          for (int h = 0; h < 3; ++h)
-            S[h] = __fadd2_rn(__ffma2_rn(splat(2.0f), f2(rc[2 * h], rc[2 * h + 1]),
-                                         f2(rm[2 * h], rm[2 * h + 1])),
-                              f2(rp[2 * h], rp[2 * h + 1]));
+          float m[LC];
+          sobel_m4(rm, rc, rp, m);  // fc_sobel.cuh: packed, the reference's rounding
           uint32_t word = 0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {  // outputs j = 2h, 2h + 1
-            const float2 gx = __ffma2_rn(splat(-1.0f), S[h], S[h + 1]);
-            // T_j(row) = (row_j + 2 row_{j+1}) + row_{j+2}; gy_j = T_j(rp) - T_j(rm)
-            const float2 tp = __fadd2_rn(
-                __ffma2_rn(splat(2.0f), f2(rp[2 * h + 1], rp[2 * h + 2]), f2(rp[2 * h], rp[2 * h + 1])),
-                f2(rp[2 * h + 2], rp[2 * h + 3]));
-            const float2 tm = __fadd2_rn(
-                __ffma2_rn(splat(2.0f), f2(rm[2 * h + 1], rm[2 * h + 2]), f2(rm[2 * h], rm[2 * h + 1])),
-                f2(rm[2 * h + 2], rm[2 * h + 3]));
-            const float2 gy = __ffma2_rn(splat(-1.0f), tm, tp);
-            const float2 m = __fadd2_rn(__fmul2_rn(gx, gx), __fmul2_rn(gy, gy));
-            word |= (m.x >= mstar ? 0xFFu : 0u) << (16 * h);
-            word |= (m.y >= mstar ? 0xFFu : 0u) << (16 * h + 8);
-          }
+          for (int j = 0; j < LC; ++j) word |= (m[j] >= mstar ? 0xFFu : 0u) << (8 * j);
           st_pred_u32(ox, word, outl);
           ox += OW;
         }
