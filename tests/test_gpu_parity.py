@@ -689,3 +689,24 @@ def test_graph_capture_replay(fp, cuda, oracle, shape, part, variant):
     np.testing.assert_array_equal(g.out.cpu().numpy().astype(np.float32),
                                   oracle.orc_chain(pipe, v2))
     g.close()
+
+
+@pytest.mark.parametrize("part,variant", [("1-5", "exact"), ("1-5", "auto"),
+                                          ("1-2,3-5", "exact"), ("1-2,3-5", "auto")])
+def test_threshold_at_exact_gradient_values(fp, cuda, oracle, part, variant):
+    """Adversarial thresholds: th equal to gradient magnitudes the reference
+    actually produces, so pixels sit exactly on the decision boundary and a
+    one-ulp difference anywhere in the gaussian / Sobel / m arithmetic (e.g.
+    a contracted multiply-add) flips them.  Every fused route stays exact."""
+    from paper_1509_04394_b200.fuseplan import hash_video_u8, spec_chain
+    W, H, F = 200, 120, 8
+    v = hash_video_u8(F, 4, H, W, 2718)
+    grad = oracle.orc_run_sequential(spec_chain(W, H, F), v)[3]
+    vals = np.unique(grad[grad > 1.0])
+    rng = np.random.default_rng(5)
+    for th in rng.choice(vals, 48, replace=False):
+        pipe = spec_chain(W, H, F, th=float(th))
+        want = np.where(grad >= th, np.float32(255), np.float32(0))  # simulator.cpp:84-89
+        out, ex = run(fp, pipe, v, {"force_partition": part}, variant=variant, torch_dev=cuda)
+        np.testing.assert_array_equal(out, want, err_msg=f"th={float(th)!r} "
+                                      f"{ex.describe()['last_chain_kernel']}")
