@@ -692,7 +692,8 @@ def test_graph_capture_replay(fp, cuda, oracle, shape, part, variant):
 
 
 @pytest.mark.parametrize("part,variant", [("1-5", "exact"), ("1-5", "auto"),
-                                          ("1-2,3-5", "exact"), ("1-2,3-5", "auto")])
+                                          ("1-2,3-5", "exact"), ("1-2,3-5", "auto"),
+                                          ("1,2,3,4,5", "auto")])
 def test_threshold_at_exact_gradient_values(fp, cuda, oracle, part, variant):
     """Adversarial thresholds: th equal to gradient magnitudes the reference
     actually produces, so pixels sit exactly on the decision boundary and a
