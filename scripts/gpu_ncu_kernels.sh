@@ -10,5 +10,8 @@ FUSEPLAN_VARIANT=exact run -k regex:k_chain_pair -c 1 python scripts/tile_sweep.
 run -k regex:"k_chain_pair|k_verify" -c 3 python scripts/small_frames.py 192 432 600
 run -k regex:"k_rgba2gray|k_iir|k_gaussian|k_gradient|k_pointwise" -c 5 python scripts/unfused_launches.py 1000
 run -k regex:"k_gray_iir|k_chain_pipe" -c 2 python scripts/time_partition.py 800 600 1000 "1-2,3-5"
+FUSEPLAN_VARIANT=exact run -k regex:"k_chain_pair" -c 1 python scripts/time_partition.py 800 600 1000 "1-2,3-5"
 } > gpurun_out/kernels_ncu.csv
 wc -l gpurun_out/kernels_ncu.csv
+python scripts/ncu_kernels_table.py gpurun_out/kernels_ncu.csv > gpurun_out/kernels_ncu.txt
+cat gpurun_out/kernels_ncu.txt

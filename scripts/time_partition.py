@@ -6,7 +6,8 @@ from paper_1509_04394_b200 import fuseplan as fp
 W, H, F, part = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
 pipe = fp.Pipeline(json.dumps(fp.spec_chain(W, H, F)))
 opts = None if part == "plan" else {"force_partition": part}
-ex = fp.Executor(pipe, fp.Plan(pipe, fp.Device.load("b200"), opts))
+ex = fp.Executor(pipe, fp.Plan(pipe, fp.Device.load("b200"), opts),
+                 variant=os.environ.get("FUSEPLAN_VARIANT", "auto"))
 v = torch.empty((F, 4, H, W), dtype=torch.uint8, device="cuda")
 fp.synth_hash_u8(v, seed=1)
 out = torch.empty((F, H, W), dtype=torch.uint8, device="cuda")
