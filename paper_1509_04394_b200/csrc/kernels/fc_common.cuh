@@ -100,13 +100,13 @@ __device__ __forceinline__ float2 wprod(float2 m, float w, float wm) {
   return __ffma2_rn(splat(w), m, splat(wm));
 }
 
-// One separable FP32 gaussian tap row: h0 (|d| = 2), h1 (|d| = 1), h2 (centre).
-// The certified band (certify_band) is derived for exactly this order.
-__device__ __forceinline__ float2 tap5(float2 a, float2 b, float2 c, float2 d, float2 e,
-                                       float h0, float h1, float h2) {
-  float2 acc = __fmul2_rn(splat(h0), __fadd2_rn(a, e));
-  acc = __ffma2_rn(splat(h1), __fadd2_rn(b, d), acc);
-  return __ffma2_rn(splat(h2), c, acc);
+// Centre-normalised separable 5-tap pass (centre tap 1; g0 at |d| = 2, g1 at
+// |d| = 1): 4 packed ops, at most 3 roundings per term -- the order
+// certify_band_scaled and tests/cpp/fast_model.c assume.  No packed multiply
+// feeds a packed add (ptxas would contract the pair, fc_sobel.cuh).
+__device__ __forceinline__ float2 tap4n(float2 a, float2 b, float2 c, float2 d, float2 e,
+                                        float g0, float g1) {
+  return __ffma2_rn(splat(g1), __fadd2_rn(b, d), __ffma2_rn(splat(g0), __fadd2_rn(a, e), c));
 }
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }

@@ -1,8 +1,11 @@
-// F12345 certified fast path, FRAME PIPELINE (the headline kernel).
+// F12345 certified fast path, ROW-PAIR PIPELINE (the round-1 headline kernel,
+// superseded by the frame-pair pipeline fc_pipe2.cu; this
+// one still runs the certified F345 group of two-fusion plans and, with
+// FUSEPLAN_PIPE_IMPL=1, the whole chain).
 //
-// Same arithmetic contract as fc_fast.cu / fc_strip.cu (exact S1+S2,
-// certified packed-FP32 S3-S5, exact FP64 recheck inside the error band; see
-// fc_fast.cu's header and fccommon::certify_band).  What changes is the work
+// Arithmetic contract: exact S1+S2, certified packed-FP32 S3-S5, exact FP64
+// recheck inside the error band (fc_common.cuh certify_band /
+// certify_band_scaled; tests/test_certified_band.py).  What changes is the work
 // decomposition, built around the one serial dependency of the chain: only
 // the IIR (S2) carries state across frames; S3-S5 of different frames are
 // independent once the frame's IIR plane exists.  A CTA owns a spatial window
@@ -253,13 +256,6 @@ __device__ __forceinline__ void sts128(unsigned addr, float2 a, float2 b) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a.x), "f"(a.y),
                "f"(b.x), "f"(b.y)
                : "memory");
-}
-
-// Centre-normalised 5-tap pass (centre tap 1): 4 packed ops, at most 3
-// roundings per term (certify_band_scaled).
-__device__ __forceinline__ float2 tap4n(float2 a, float2 b, float2 c, float2 d, float2 e,
-                                        float g0, float g1) {
-  return __ffma2_rn(splat(g1), __fadd2_rn(b, d), __ffma2_rn(splat(g0), __fadd2_rn(a, e), c));
 }
 
 // 0xFF where nd < 0 for two values -> the low 16 bits (sign-replicate PRMT)

@@ -226,12 +226,6 @@ __device__ __forceinline__ void sts128f(unsigned addr, float a, float b, float c
                : "memory");
 }
 
-// Centre-normalised 5-tap pass (centre tap 1): 4 packed ops
-__device__ __forceinline__ float2 tap4n(float2 a, float2 b, float2 c, float2 d, float2 e,
-                                        float g0, float g1) {
-  return __ffma2_rn(splat(g1), __fadd2_rn(b, d), __ffma2_rn(splat(g0), __fadd2_rn(a, e), c));
-}
-
 __device__ __forceinline__ float2 shfl_up2(float2 v) {
   return make_float2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
 }
