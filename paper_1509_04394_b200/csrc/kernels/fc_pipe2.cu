@@ -866,8 +866,7 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
     const int lo = p < q ? p : q, hi = p < q ? q : p;
     return t6[lo == 0 ? hi : (lo == 1 ? 2 + hi : 5)];
   };
-  const unsigned lcol = 16u * unsigned((lane + 31) & 31), mcol = 16u * unsigned(lane),
-                 rcol = 16u * unsigned((lane + 1) & 31);
+  const unsigned mcol = 16u * unsigned(lane);
   int slot = fp0 % K2;
   for (int u = fp0; u < n_pairs; u += NPF) {
     nb_sync<true>(1 + K2 + slot);  // the IIR warps stored pair u
@@ -892,7 +891,15 @@ __device__ __forceinline__ void exact_stencil_role(const Args& a, const Range& r
         double v[LC + 4];  // window row p, cols 4L-2 .. 4L+5 (frame c's plane)
         {
           const unsigned rb = cbase + p * PROW;
-          const float4 ql = lds128(rb + lcol), qm = lds128(rb + mcol), qr = lds128(rb + rcol);
+          // the lane's 4 columns from shared memory, the 2 + 2 halo columns
+          // from the neighbouring lanes by shuffle (lane 0 / 31 wrap: their
+          // outputs are not stored)
+          const float4 qm = lds128(rb + mcol);
+          float4 ql, qr;
+          ql.z = __shfl_sync(0xffffffffu, qm.z, (lane + 31) & 31);
+          ql.w = __shfl_sync(0xffffffffu, qm.w, (lane + 31) & 31);
+          qr.x = __shfl_sync(0xffffffffu, qm.x, (lane + 1) & 31);
+          qr.y = __shfl_sync(0xffffffffu, qm.y, (lane + 1) & 31);
           v[0] = double(ql.z);
           v[1] = double(ql.w);
           v[2] = double(qm.x);
